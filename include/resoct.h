@@ -1,0 +1,208 @@
+/*
+ * resoct.h -- C ABI of the B200-native residency-octree render path.
+ *
+ * libresoct.so replaces the reference's numba/numpy hot path behind the
+ * reference's Python API.  Every entry point takes plain pointers and sizes
+ * (device pointers unless noted), never torch types.  The reference interface
+ * each call replaces is cited; all paths are under /root/reference/pkg/src/
+ * resoctree/.
+ *
+ *   ro_render            kernels.py:209-704  raycast_frame (MODE_RESIDENCY /
+ *                        MODE_REFERENCE, check_skips audit), driven by
+ *                        render.py:125-208 (_run) and camera.py:32-51
+ *   ro_feedback_collect  render.py:210-215  bricks-first request budget over
+ *                        the first-seen request lists of kernels.py:457-517
+ *   ro_note_sampled      engine.py:72-81    Engine.note_sampled
+ *   ro_apply_bricks      engine.py:85-89    Engine.apply_brick, batched:
+ *                        paging.py:187-218 insert_brick (LRU) +
+ *                        octree.py:193-246 on_brick_evicted/inserted
+ *   ro_evict_bricks      verify.py:110-121  explicit eviction (unmap, release
+ *                        slot, octree.on_brick_evicted)
+ *   ro_mark_empty        paging.py:228-234  MultiChannelPaging.mark_empty
+ *   ro_apply_metadata    engine.py:91-96    Engine.apply_metadata /
+ *                        octree.py:263-269 set_node_metadata
+ *   ro_write_level_metadata engine.py:138-152 fill_metadata_from_volumes (one
+ *                        octree level of one slot from device min/max grids)
+ *   ro_swap_channel      engine.py:98-105   Engine.swap_channel =
+ *                        paging.py:263-284 + octree.py:271-273
+ *   ro_octree_update     octree.py:193-246  on_brick_inserted / on_brick_evicted
+ *                        for a list of changed bricks (incremental pass)
+ *   ro_rebuild_masks     octree.py:355-395  masks from the resident set
+ *                        (ground truth + OR closure), for verification
+ *
+ * Errors: every call returns 0 on success or a negative RO_E* code; the
+ * message is available from ro_last_error() (thread-local).  Asynchronous
+ * kernel faults surface at the next synchronising call (ro_sync,
+ * ro_feedback_collect, ro_apply_bricks).
+ *
+ * Threading: single writer per context (paging.py:84-87).  All work of a
+ * context is ordered on the caller's stream; ro_apply_bricks additionally
+ * uses the context's own upload stream for host->device payload copies.
+ */
+#ifndef RESOCT_H
+#define RESOCT_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RO_ABI_VERSION 1
+#define RO_MAX_LEVELS 16
+#define RO_MAX_PT 256
+#define RO_MAX_CH 8
+#define RO_MAX_TF_POINTS 16
+#define RO_NUM_COUNTERS 8
+
+#define RO_MODE_RESIDENCY 0
+#define RO_MODE_REFERENCE 1
+
+/* packed page-table entry: >= 0 cache slot (MAPPED), else: */
+#define RO_PT_UNMAPPED (-1)
+#define RO_PT_EMPTY (-2)
+
+#define RO_OK 0
+#define RO_EINVAL (-1)
+#define RO_ECUDA (-2)
+#define RO_ENOMEM (-3)
+#define RO_ESTATE (-4)
+
+/* Static volume / cache geometry (paging.py:27-112, octree.py:26-39). */
+typedef struct ro_layout {
+    int32_t m, k, depth;               /* channel slots, levels, octree depth */
+    int32_t brick[3];                  /* brick size x, y, z */
+    int32_t level_dims[RO_MAX_LEVELS][3];   /* voxels per level, x, y, z */
+    int32_t level_grids[RO_MAX_LEVELS][3];  /* bricks per level, x, y, z */
+    int64_t pt_offsets[RO_MAX_PT + 1]; /* page-table offsets, m*k+1 used */
+    int64_t num_slots;                 /* cache slots S */
+} ro_layout;
+
+/* Mutable render state in device memory, owned by the caller. */
+typedef struct ro_state {
+    uint32_t *words;         /* [N*m] octree words (mask|min<<16|max<<24); may be NULL */
+    int32_t *pt;             /* [E]   packed page-table entries */
+    uint8_t *cache;          /* [S*bz*by*bx] brick cache */
+    int64_t *slot_brick;     /* [S]   brick id per slot, -1 free */
+    int64_t *slot_last_used; /* [S]   LRU frame stamp */
+    int32_t *free_stack;     /* [S]   LIFO free list, top at free_count-1 */
+    int32_t *free_count;     /* [1]   device scalar */
+} ro_state;
+
+/* One visible channel in importance order (render.py:35-44,101-122). */
+typedef struct ro_channel {
+    int32_t slot, lo, hi, npoints;
+    double tf_x[RO_MAX_TF_POINTS];
+    double tf_rgba[RO_MAX_TF_POINTS][4];
+    /* interval emptiness (kernels.py:201-206): metadata (mn, mx) is
+       transparent iff mx < empty_below[mn] */
+    uint16_t empty_below[256];
+} ro_channel;
+
+/* Per-frame constants, filled on the host. */
+typedef struct ro_frame {
+    int32_t mode;                 /* RO_MODE_* */
+    int32_t n_ch;
+    int32_t width, height;        /* full image */
+    double cam_pos[3], cam_fwd[3], cam_right[3], cam_up[3];
+    double tan_half, aspect;
+    double base_step, t0, early_alpha, eps_h;
+    int32_t start_level;
+    int32_t check_skips;
+    /* LOD: raw level L holds iff ratio >= lod_threshold[L] (L = 1..15),
+       thresholds found with the same libm log2 the reference calls */
+    double lod_threshold[RO_MAX_LEVELS + 1];
+    double step_tab[RO_MAX_LEVELS];      /* base_step * 2^maxlev(raw) */
+    int32_t maxlev_tab[RO_MAX_LEVELS];   /* max over channels of clamp(raw) */
+    int32_t dt_tab[RO_MAX_LEVELS];       /* traversal_depth(step_tab[raw]) */
+    /* sort-first partition: rows are cut in blocks of tile_rows; block b is
+       rendered by part (b % n_parts).  Outputs are local (compacted rows). */
+    int32_t n_parts, part, tile_rows, _pad0;
+    const int32_t *ref_pt;        /* audit paging (check_skips), device */
+    const uint8_t *ref_cache;
+    ro_channel ch[RO_MAX_CH];
+} ro_frame;
+
+typedef struct ro_outputs {
+    float *image;          /* [local_rows*width*4] f32 RGBA */
+    uint8_t *required;     /* [E] usage mask (zeroed by ro_render) */
+    int32_t *pix_required; /* [local_rows*width] */
+    int64_t *hist;         /* [n_ch*k] (zeroed by ro_render) */
+    int64_t *counters;     /* [RO_NUM_COUNTERS]: steps, evaluated, skipped,
+                              violations, livelocks (zeroed by ro_render) */
+} ro_outputs;
+
+typedef struct ro_feedback {
+    int64_t *brick_keys, *brick_ids; /* [budget] device */
+    int64_t *meta_keys, *meta_ids;   /* [budget] device; meta id = node*m+slot */
+    int64_t *counts;                 /* [4] HOST: unique bricks, unique metas,
+                                        bricks emitted, metas emitted */
+} ro_feedback;
+
+typedef struct ro_ctx ro_ctx;
+
+int ro_abi_version(void);
+const char *ro_last_error(void);
+
+int ro_create(const ro_layout *layout, ro_ctx **out);
+int ro_destroy(ro_ctx *ctx);
+
+/* Row count this part renders for a (height, n_parts, part, tile_rows). */
+int64_t ro_local_rows(int32_t height, int32_t n_parts, int32_t part,
+                      int32_t tile_rows);
+
+int ro_render(ro_ctx *ctx, const ro_frame *frame, const ro_state *state,
+              const ro_outputs *out, void *stream);
+
+/* Order the frame's first-seen requests and truncate them: with
+   bricks_first=1 metas get budget-(bricks emitted) (render.py:210-215),
+   otherwise each list is cut to `budget` independently (per-part lists of a
+   sort-first frame, merged later).  Synchronises the stream. */
+int ro_feedback_collect(ro_ctx *ctx, int64_t budget, int32_t bricks_first,
+                        const ro_feedback *fb, void *stream);
+
+int ro_note_sampled(ro_ctx *ctx, const ro_state *state,
+                    const uint8_t *required, int64_t frame, void *stream);
+
+/* Insert n bricks in order.  ids: HOST array.  payloads: n*brick bytes on the
+   host (payload_on_device=0) or device (=1).  update_octree=0 for paging-only
+   inserts.  slots_out / evicted_out: optional HOST arrays of n.  Synchronises
+   the stream. */
+int ro_apply_bricks(ro_ctx *ctx, const ro_state *state, const int64_t *ids,
+                    int64_t n, const void *payloads, int32_t payload_on_device,
+                    int64_t frame, int32_t update_octree, int32_t *slots_out,
+                    int64_t *evicted_out, void *stream);
+
+int ro_evict_bricks(ro_ctx *ctx, const ro_state *state, const int64_t *ids,
+                    int64_t n, int32_t update_octree, void *stream);
+int ro_mark_empty(ro_ctx *ctx, const ro_state *state, const int64_t *ids,
+                  int64_t n, void *stream);
+
+/* HOST arrays of n; later entries win on duplicates. */
+int ro_apply_metadata(ro_ctx *ctx, const ro_state *state,
+                      const int64_t *node_idx, const int32_t *slot,
+                      const int32_t *mn, const int32_t *mx, int64_t n,
+                      void *stream);
+
+/* Device grids [side^3] (z, y, x order) of node min/max for octree depth d. */
+int ro_write_level_metadata(ro_ctx *ctx, const ro_state *state, int32_t slot,
+                            int32_t d, const uint8_t *mins, const uint8_t *maxs,
+                            void *stream);
+
+int ro_swap_channel(ro_ctx *ctx, const ro_state *state, int32_t channel_slot,
+                    int32_t invalidate_octree, void *stream);
+
+/* ids: HOST array of changed bricks; their leaves are recomputed from the
+   current page table, then ancestors re-ORed. */
+int ro_octree_update(ro_ctx *ctx, const ro_state *state, const int64_t *ids,
+                     int64_t n, void *stream);
+
+int ro_rebuild_masks(ro_ctx *ctx, const ro_state *state, void *stream);
+
+int ro_sync(ro_ctx *ctx, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RESOCT_H */

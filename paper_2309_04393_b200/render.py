@@ -1,0 +1,347 @@
+"""Render entry points: the drop-in for render.py of the reference.
+
+``render_frame`` / ``render_reference`` keep the reference signatures
+(``render.py:236-250``) and return the same ``FrameOutput`` (numpy image,
+ordered brick / metadata request lists, usage mask, level histogram,
+per-pixel brick switches, stats).  Underneath, one call is:
+
+  host: pack channels + LOD/step tables (render.py:101-122, µs)
+  GPU : k_raycast (kernel 1), then request ordering + budget (kernel 3a)
+  D2H : image, usage mask, histogram, counters, <= budget request entries
+
+``render_frame_device`` is the same pass without the host copies; the
+Session uses it so the usage mask feeds ``note_sampled`` on the device.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .camera import Camera, ray_basis
+from .octree import ResidencyOctree
+from .paging import MultiChannelPaging
+from .transfer import TransferFunction
+
+MODE_RESIDENCY = N.RO_MODE_RESIDENCY
+MODE_REFERENCE = N.RO_MODE_REFERENCE
+
+
+class RenderError(ValueError):
+    pass
+
+
+@dataclass(frozen=True)
+class ChannelSettings:
+    """One active channel; list order is importance order."""
+    slot: int
+    tf: TransferFunction
+    level_range: tuple = (0, 15)
+
+    def __post_init__(self):
+        if self.level_range[0] > self.level_range[1]:
+            raise RenderError(f"level range {self.level_range} inverted")
+
+
+@dataclass(frozen=True)
+class RenderConfig:
+    image_dims: tuple = (256, 256)
+    base_step: float = 1.0 / 256.0
+    lod_reference_distance: float = 1.0
+    early_term_alpha: float = 0.99
+    max_requests_per_frame: int = 256
+    traversal_start_level: int = 2
+    homogeneity_eps: float = 0.0
+
+    def __post_init__(self):
+        if self.base_step <= 0.0:
+            raise RenderError("base step must be positive")
+        if self.lod_reference_distance <= 0.0:
+            raise RenderError("lod reference distance must be positive")
+        if not 0.0 < self.early_term_alpha <= 1.0:
+            raise RenderError("early termination alpha outside (0, 1]")
+        if self.max_requests_per_frame < 1:
+            raise RenderError("request budget must be positive")
+        if self.traversal_start_level < 0:
+            raise RenderError("traversal start level must be >= 0")
+
+
+@dataclass
+class FrameStats:
+    traversal_steps: int = 0
+    samples_evaluated: int = 0
+    samples_skipped: int = 0
+    skip_violations: int = 0
+    required_bricks: int = 0
+    required_bytes: int = 0
+    requests_issued: int = 0
+    render_ms: float = 0.0
+    livelocked_rays: int = 0
+
+
+@dataclass
+class FrameOutput:
+    image: np.ndarray
+    brick_requests: list
+    metadata_requests: list
+    stats: FrameStats
+    required_mask: np.ndarray = field(repr=False, default=None)
+    level_histogram: np.ndarray = field(repr=False, default=None)
+    pixel_required: np.ndarray = field(repr=False, default=None)
+    required_mask_device: torch.Tensor = field(repr=False, default=None)
+
+
+# ---------------------------------------------------------------------------
+# host tables
+# ---------------------------------------------------------------------------
+
+_LOD_THRESHOLDS = None
+
+
+def lod_thresholds() -> list:
+    """T[L] = smallest ratio >= 1 with floor(log2(ratio)) >= L, found with
+    the platform libm log2 -- the function kernels.py:49 calls."""
+    global _LOD_THRESHOLDS
+    if _LOD_THRESHOLDS is None:
+        out = [1.0]
+        for L in range(1, N.RO_MAX_LEVELS):
+            r = float(2 ** L)
+            if math.floor(math.log2(r)) < L:
+                raise RuntimeError("libm log2 is not exact at powers of two")
+            while True:
+                p = math.nextafter(r, 0.0)
+                if math.floor(math.log2(p)) >= L:
+                    r = p
+                else:
+                    break
+            out.append(r)
+        out.append(float("inf"))
+        _LOD_THRESHOLDS = out
+    return _LOD_THRESHOLDS
+
+
+def traversal_depth(step: float, max_depth: int) -> int:
+    """kernels.py:57-66"""
+    if step >= 1.0:
+        return 0
+    d = int(math.floor(math.log2(1.0 / step)))
+    return min(max(d, 0), max_depth)
+
+
+def choose_resolution_level(t, t0, lo=0, hi=15) -> int:
+    """kernels.py:43-54 (host mirror)."""
+    ratio = t / t0
+    lev = 0 if ratio < 1.0 else int(math.floor(math.log2(ratio)))
+    return min(max(lev, lo), hi)
+
+
+def choose_traversal_depth(step, max_depth) -> int:
+    return traversal_depth(step, max_depth)
+
+
+def _pack_frame(mode, paging: MultiChannelPaging, channels, camera: Camera,
+                config: RenderConfig, depth: int, eps_h: float,
+                reference_paging: MultiChannelPaging | None = None,
+                partition=(1, 0, 8)) -> N.Frame:
+    if not channels:
+        raise RenderError("need at least one active channel")
+    if len(channels) > N.RO_MAX_CH:
+        raise RenderError(f"at most {N.RO_MAX_CH} active channels")
+    k = paging.config.k
+    w, h = config.image_dims
+    F = N.Frame()
+    F.mode = mode
+    F.n_ch = len(channels)
+    F.width, F.height = int(w), int(h)
+    b = ray_basis(camera, w, h)
+    for a in range(3):
+        F.cam_pos[a] = b.pos[a]
+        F.cam_fwd[a] = b.fwd[a]
+        F.cam_right[a] = b.right[a]
+        F.cam_up[a] = b.up[a]
+    F.tan_half, F.aspect = b.tan_half, b.aspect
+    F.base_step = config.base_step
+    F.t0 = config.lod_reference_distance
+    F.early_alpha = config.early_term_alpha
+    F.eps_h = eps_h
+    F.start_level = config.traversal_start_level
+    for i, t in enumerate(lod_thresholds()):
+        F.lod_threshold[i] = t
+    los, his = [], []
+    for i, c in enumerate(channels):
+        if not 0 <= c.slot < paging.config.m:
+            raise RenderError(f"channel slot {c.slot} out of range")
+        lo = max(0, min(c.level_range[0], k - 1))
+        hi = max(0, min(c.level_range[1], k - 1))
+        los.append(lo)
+        his.append(hi)
+        ch = F.ch[i]
+        ch.slot, ch.lo, ch.hi = c.slot, lo, hi
+        pts = c.tf.points
+        if len(pts) > N.RO_MAX_TF_POINTS:
+            raise RenderError(f"transfer function with > {N.RO_MAX_TF_POINTS} points")
+        ch.npoints = len(pts)
+        for j, (x, rgba) in enumerate(pts):
+            ch.tf_x[j] = float(x)
+            for q in range(4):
+                ch.tf_rgba[j][q] = float(rgba[q])
+        eb = c.tf.empty_below()
+        for j in range(256):
+            ch.empty_below[j] = int(eb[j])
+    for raw in range(N.RO_MAX_LEVELS):
+        maxlev = 0
+        for lo, hi in zip(los, his):
+            lev = min(max(raw, lo), hi)
+            maxlev = max(maxlev, lev)
+        step = config.base_step * (1 << maxlev)
+        F.maxlev_tab[raw] = maxlev
+        F.step_tab[raw] = step
+        F.dt_tab[raw] = traversal_depth(step, depth)
+    F.n_parts, F.part, F.tile_rows = partition
+    if reference_paging is not None:
+        F.check_skips = 1
+        F.ref_pt = reference_paging.pt.data_ptr()
+        F.ref_cache = reference_paging.cache_dev.data_ptr()
+    return F
+
+
+# ---------------------------------------------------------------------------
+# device frame
+# ---------------------------------------------------------------------------
+
+class DeviceFrame:
+    """Device-side results of one pass (plus the host feedback lists)."""
+
+    def __init__(self, paging, n_ch, k, npix_local, budget):
+        dev = paging.device
+        self.image = torch.empty((npix_local, 4), dtype=torch.float32, device=dev)
+        self.required = torch.empty(paging.total_entries, dtype=torch.uint8, device=dev)
+        self.pix_required = torch.empty(npix_local, dtype=torch.int32, device=dev)
+        self.hist = torch.empty((n_ch, k), dtype=torch.int64, device=dev)
+        self.counters = torch.empty(N.RO_NUM_COUNTERS, dtype=torch.int64, device=dev)
+        self.fb = torch.empty((4, max(budget, 1)), dtype=torch.int64, device=dev)
+        self.budget = budget
+        self.counts = np.zeros(4, dtype=np.int64)
+        self.outputs = N.Outputs(self.image.data_ptr(), self.required.data_ptr(),
+                                 self.pix_required.data_ptr(), self.hist.data_ptr(),
+                                 self.counters.data_ptr())
+        self.feedback = N.Feedback(self.fb[0].data_ptr(), self.fb[1].data_ptr(),
+                                   self.fb[2].data_ptr(), self.fb[3].data_ptr(),
+                                   self.counts.ctypes.data)
+
+    @property
+    def n_bricks(self) -> int:
+        return int(self.counts[2])
+
+    @property
+    def n_metas(self) -> int:
+        return int(self.counts[3])
+
+
+def _buffers(paging, n_ch, npix_local, budget) -> DeviceFrame:
+    key = (n_ch, npix_local, budget)
+    cache = paging.__dict__.setdefault("_frame_buffers", {})
+    buf = cache.get(key)
+    if buf is None:
+        if len(cache) > 4:
+            cache.clear()
+        buf = DeviceFrame(paging, n_ch, paging.config.k, npix_local, budget)
+        cache[key] = buf
+    return buf
+
+
+def render_frame_device(mode, paging: MultiChannelPaging, octree: ResidencyOctree | None,
+                        channels, camera: Camera, config: RenderConfig,
+                        reference_paging=None, partition=(1, 0, 8),
+                        bricks_first: bool = True, collect: bool = True) -> DeviceFrame:
+    """One ray-cast pass + feedback ordering, results left on the device.
+
+    Not re-entrant per paging: the returned buffers are reused by the next
+    call with the same shape."""
+    N.require_cuda()
+    if mode == MODE_RESIDENCY:
+        if octree is None:
+            raise RenderError("residency mode needs the octree")
+        depth, eps_h = octree.config.depth, octree.config.homogeneity_eps
+    else:
+        depth, eps_h = 0, config.homogeneity_eps
+    F = _pack_frame(mode, paging, channels, camera, config, depth, eps_h,
+                    reference_paging, partition)
+    w, h = config.image_dims
+    rows = N.lib().ro_local_rows(h, *partition)
+    buf = _buffers(paging, len(channels), rows * w, config.max_requests_per_frame)
+    st = paging.state(with_words=(mode == MODE_RESIDENCY))
+    s = N.stream_ptr()
+    N.check(N.lib().ro_render(paging.ctx, C.byref(F), C.byref(st),
+                              C.byref(buf.outputs), s))
+    if collect:
+        N.check(N.lib().ro_feedback_collect(paging.ctx, config.max_requests_per_frame,
+                                            1 if bricks_first else 0,
+                                            C.byref(buf.feedback), s))
+    return buf
+
+
+def _run(mode, paging, channels, camera, config, octree=None,
+         reference_paging=None) -> FrameOutput:
+    start = time.perf_counter()
+    buf = render_frame_device(mode, paging, octree, channels, camera, config,
+                              reference_paging)
+    m = paging.config.m
+    nb, nm = buf.n_bricks, buf.n_metas
+    # device -> pinned host (torch's caching host allocator recycles blocks)
+    pin = dict(pin_memory=True)
+    img = torch.empty(buf.image.shape, dtype=torch.float32, **pin)
+    req = torch.empty(buf.required.shape, dtype=torch.uint8, **pin)
+    pixr = torch.empty(buf.pix_required.shape, dtype=torch.int32, **pin)
+    small = torch.empty(buf.hist.numel() + N.RO_NUM_COUNTERS + 4 * buf.fb.shape[1],
+                        dtype=torch.int64, **pin)
+    img.copy_(buf.image, non_blocking=True)
+    req.copy_(buf.required, non_blocking=True)
+    pixr.copy_(buf.pix_required, non_blocking=True)
+    nh = buf.hist.numel()
+    small[:nh].copy_(buf.hist.reshape(-1), non_blocking=True)
+    small[nh:nh + N.RO_NUM_COUNTERS].copy_(buf.counters, non_blocking=True)
+    small[nh + N.RO_NUM_COUNTERS:].copy_(buf.fb.reshape(-1), non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    elapsed_ms = (time.perf_counter() - start) * 1000.0
+    sm = small.numpy()
+    hist = sm[:nh].reshape(buf.hist.shape).copy()
+    counters = sm[nh:nh + N.RO_NUM_COUNTERS]
+    fb = sm[nh + N.RO_NUM_COUNTERS:].reshape(4, -1)
+    bricks = [int(v) for v in fb[1][:nb]]
+    metas = [(int(v) // m, int(v) % m) for v in fb[3][:nm]]
+    required = req.numpy()
+    nreq = int(required.sum())
+    sx, sy, sz = paging.config.brick_size
+    stats = FrameStats(traversal_steps=int(counters[0]), samples_evaluated=int(counters[1]),
+                       samples_skipped=int(counters[2]), skip_violations=int(counters[3]),
+                       required_bricks=nreq, required_bytes=nreq * sx * sy * sz,
+                       requests_issued=len(bricks) + len(metas), render_ms=elapsed_ms,
+                       livelocked_rays=int(counters[4]))
+    w, h = config.image_dims
+    return FrameOutput(image=img.numpy().reshape(h, w, 4), brick_requests=bricks,
+                       metadata_requests=metas, stats=stats, required_mask=required,
+                       level_histogram=hist, pixel_required=pixr.numpy(),
+                       required_mask_device=buf.required)
+
+
+def render_frame(paging: MultiChannelPaging, octree: ResidencyOctree,
+                 channels, camera: Camera, config: RenderConfig,
+                 reference_paging: MultiChannelPaging | None = None) -> FrameOutput:
+    """Residency-octree renderer (render.py:236-243); pass reference paging to
+    audit every skip."""
+    return _run(MODE_RESIDENCY, paging, channels, camera, config, octree=octree,
+                reference_paging=reference_paging)
+
+
+def render_reference(paging: MultiChannelPaging, channels, camera: Camera,
+                     config: RenderConfig) -> FrameOutput:
+    """In-core oracle mode (render.py:246-250): every sample translated and
+    evaluated, no skipping or substitution."""
+    return _run(MODE_REFERENCE, paging, channels, camera, config)

@@ -1,0 +1,305 @@
+"""Generate golden fixtures by running the REFERENCE itself.
+
+Run in the build container (the only place /root/reference exists):
+
+    NUMBA_CACHE_DIR=/tmp/nbcache python tests/golden/make_golden.py
+
+It imports ``resoctree`` from /root/reference/pkg/src, drives the
+reference's own Session / Engine / render_frame / render_reference on small
+synthetic scenes and stores inputs + outputs under tests/golden/*.npz.  The
+fixtures pin the CPU oracle (tests/test_oracle_golden.py) and, through it,
+the CUDA path (tests/test_gpu_parity.py).  Nothing at test time reads
+/root/reference.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import sys
+import tempfile
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REF)
+
+from resoctree import bench, datasets  # noqa: E402
+from resoctree.camera import orbit_pose  # noqa: E402
+from resoctree.engine import Engine, EngineConfig  # noqa: E402
+from resoctree.ingest import build_hierarchy  # noqa: E402
+from resoctree.render import (ChannelSettings, RenderConfig,  # noqa: E402
+                              render_frame, render_reference)
+from resoctree.service import DatasetStore, LocalTransport  # noqa: E402
+from resoctree.session import Session  # noqa: E402
+from resoctree.transfer import TransferFunction, grayscale_ramp_tf  # noqa: E402
+
+
+def h(a) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def state_hashes(eng) -> dict:
+    p, o = eng.paging, eng.octree
+    return {"words": h(o.words), "pt_status": h(p.pt_status),
+            "pt_slot": h(p.pt_slot), "slot_brick": h(p.slot_brick),
+            "slot_last_used": h(p.slot_last_used), "cache": h(p.cache),
+            "free": h(np.array(p._free, dtype=np.int64))}
+
+
+def frame_record(prefix, out, rec):
+    rec[prefix + "image"] = out.image
+    rec[prefix + "bricks"] = np.array(out.brick_requests, dtype=np.int64)
+    rec[prefix + "metas"] = np.array(out.metadata_requests,
+                                     dtype=np.int64).reshape(-1, 2)
+    rec[prefix + "required"] = out.required_mask
+    rec[prefix + "hist"] = out.level_histogram
+    rec[prefix + "pixreq"] = out.pixel_required
+    s = out.stats
+    rec[prefix + "counters"] = np.array(
+        [s.traversal_steps, s.samples_evaluated, s.samples_skipped,
+         s.skip_violations], dtype=np.int64)
+
+
+def tf_points(tf):
+    return [[float(x), [float(v) for v in c]] for x, c in tf.points]
+
+
+def pyramid_hash(store, channels):
+    hh = hashlib.sha256()
+    for c in channels:
+        for l in range(len(store.manifest.levels)):
+            hh.update(np.ascontiguousarray(store.level_array(c, l)).tobytes())
+    return hh.hexdigest()
+
+
+# ---------------------------------------------------------------------------
+
+def session_mc64(tmp):
+    """Cold multi-channel session with mixed level ranges, LRU pressure and a
+    mid-stream channel swap (scaled down)."""
+    root = os.path.join(tmp, "mc64")
+    build_hierarchy(datasets.sparse_multichannel(64, channels=4), (16, 16, 16),
+                    3, (2, 2, 2), root, name="mc64")
+    store = DatasetStore(root)
+    tf_a = grayscale_ramp_tf(40.0)
+    tf_b = TransferFunction(points=((0.0, (0, 0, 0, 0)), (30.0, (0, 0, 0, 0)),
+                                    (120.0, (1.0, 0.2, 0.1, 0.6)),
+                                    (255.0, (0.2, 0.4, 1.0, 0.9))))
+    chans = [ChannelSettings(slot=2, tf=tf_a, level_range=(0, 2)),
+             ChannelSettings(slot=0, tf=tf_b, level_range=(1, 2)),
+             ChannelSettings(slot=3, tf=tf_a, level_range=(0, 0)),
+             ChannelSettings(slot=1, tf=tf_b, level_range=(0, 2))]
+    econf = EngineConfig(octree_depth=3, cache_slots=(4, 4, 4), channel_slots=4)
+    rconf = RenderConfig(image_dims=(48, 40), base_step=1.0 / 64.0,
+                         max_requests_per_frame=64, traversal_start_level=2)
+    sess = Session(LocalTransport(store), econf, rconf, chans)
+    rec = {}
+    script = []
+    poses = [orbit_pose(0.7)] * 9 + [orbit_pose(2.1)] * 9
+    for i, pose in enumerate(poses):
+        if i == 9:
+            sess.swap_channel(1, 3)
+            sess.swap_channel(3, 0)
+            script.append({"swap": [[1, 3], [3, 0]],
+                           "after_swap": state_hashes(sess.engine)})
+        r = sess.step_frame(pose)
+        frame_record(f"f{i}_", r.output, rec)
+        script.append({"frame": i, "pose": [list(pose.position),
+                                            list(pose.target), list(pose.up),
+                                            pose.fov_deg],
+                       "after": state_hashes(sess.engine),
+                       "bricks_applied": r.bricks_applied,
+                       "metadata_applied": r.metadata_applied})
+    meta = {
+        "volume": {"kind": "sparse_multichannel", "n": 64, "channels": 4,
+                   "seed": 11, "brick": [16, 16, 16], "levels": 3},
+        "pyramid_sha": pyramid_hash(store, range(4)),
+        "engine": {"depth": 3, "cache_slots": [4, 4, 4], "m": 4,
+                   "pad": sess.engine.metadata_pad},
+        "render": {"image_dims": [48, 40], "base_step": 1.0 / 64.0,
+                   "budget": 64, "start_level": 2, "t0": 1.0,
+                   "early_alpha": 0.99},
+        "channels": [{"slot": c.slot, "tf": tf_points(c.tf),
+                      "level_range": list(c.level_range)} for c in chans],
+        "script": script,
+    }
+    sess.close()
+    return meta, rec
+
+
+def vessel256_full():
+    """Config 1: vessel 256^3, fully resident, D=5, 256^2, step 1/128
+    (test_acceptance.py:44-123): residency and reference renders."""
+    tmp = tempfile.mkdtemp()
+    root = os.path.join(tmp, "vessel256")
+    build_hierarchy([datasets.vessel_volume(256)], (32, 32, 32), 4, (2, 2, 2),
+                    root, name="vessel")
+    store = DatasetStore(root)
+    econf = bench.full_engine_config(store, 1, depth=5)
+    eng = bench.prepare_engine(store, {0: 0}, econf)
+    rconf = RenderConfig(image_dims=(256, 256), base_step=1.0 / 128.0,
+                         max_requests_per_frame=2048, traversal_start_level=2)
+    tf = grayscale_ramp_tf(threshold=40.0)
+    chans = [ChannelSettings(slot=0, tf=tf)]
+    angles = (0.0, 1.1, 2.4, 3.7, 5.2)
+    rec = {}
+    for i, a in enumerate(angles):
+        pose = orbit_pose(a)
+        out = render_frame(eng.paging, eng.octree, chans, pose, rconf)
+        frame_record(f"res{i}_", out, rec)
+        ref = render_reference(eng.paging, chans, pose, rconf)
+        frame_record(f"ref{i}_", ref, rec)
+        assert np.array_equal(out.image, ref.image)
+    meta = {
+        "volume": {"kind": "vessel", "n": 256, "seed": 7,
+                   "brick": [32, 32, 32], "levels": 4},
+        "pyramid_sha": pyramid_hash(store, [0]),
+        "engine": {"depth": 5, "cache_slots": list(econf.cache_slots), "m": 1,
+                   "pad": eng.metadata_pad},
+        "state": state_hashes(eng),
+        "render": {"image_dims": [256, 256], "base_step": 1.0 / 128.0,
+                   "budget": 2048, "start_level": 2, "t0": 1.0,
+                   "early_alpha": 0.99},
+        "channels": [{"slot": 0, "tf": tf_points(tf), "level_range": [0, 15]}],
+        "angles": list(angles),
+    }
+    return meta, rec
+
+
+def skip_audit_shell64(tmp):
+    """Skip soundness (test_acceptance.py:138-160): converged sessions under
+    random TFs, rendered with reference_paging auditing every skip."""
+    root = os.path.join(tmp, "shell64")
+    build_hierarchy([datasets.shell_volume(64)], (16, 16, 16), 3, (2, 2, 2),
+                    root, name="shell")
+    store = DatasetStore(root)
+    ref_eng = bench.prepare_engine(store, {0: 0},
+                                   bench.full_engine_config(store, 1, depth=3))
+    econf = EngineConfig(octree_depth=3, cache_slots=(9, 9, 9), channel_slots=1)
+    rconf = RenderConfig(image_dims=(64, 64), base_step=1.0 / 64.0,
+                         max_requests_per_frame=512, traversal_start_level=2)
+    rng = np.random.default_rng(42)
+    rec = {}
+    runs = []
+    poses = [orbit_pose(a) for a in (0.3, 2.0, 4.4)]
+    for r in range(3):
+        xs = np.sort(rng.choice(np.arange(1.0, 255.0), size=5, replace=False))
+        pts = [(0.0, (0.0, 0.0, 0.0, 0.0))]
+        for x in xs:
+            alpha = 0.0 if rng.random() < 0.5 else float(rng.uniform(0.05, 1.0))
+            pts.append((float(x), (float(rng.random()), float(rng.random()),
+                                   float(rng.random()), alpha)))
+        tf = TransferFunction(points=tuple(pts))
+        chans = [ChannelSettings(slot=0, tf=tf)]
+        sess = Session(LocalTransport(store), econf, rconf, chans)
+        recs = sess.run_until_converged(poses[0], max_frames=50)
+        for j, pose in enumerate(poses):
+            out = render_frame(sess.engine.paging, sess.engine.octree, chans,
+                               pose, rconf, reference_paging=ref_eng.paging)
+            frame_record(f"r{r}p{j}_", out, rec)
+        runs.append({"tf": tf_points(tf), "frames": len(recs),
+                     "state": state_hashes(sess.engine)})
+        sess.close()
+    meta = {
+        "volume": {"kind": "shell", "n": 64, "brick": [16, 16, 16],
+                   "levels": 3},
+        "pyramid_sha": pyramid_hash(store, [0]),
+        "engine": {"depth": 3, "cache_slots": [9, 9, 9], "m": 1,
+                   "pad": ref_eng.metadata_pad},
+        "ref_state": state_hashes(ref_eng),
+        "render": {"image_dims": [64, 64], "base_step": 1.0 / 64.0,
+                   "budget": 512, "start_level": 2, "t0": 1.0,
+                   "early_alpha": 0.99},
+        "poses": [0.3, 2.0, 4.4],
+        "runs": runs,
+    }
+    return meta, rec
+
+
+def lru_replay():
+    """Randomised insert / explicit-evict / note_sampled / swap / metadata
+    sequence with frame advances (verify.py:88-136 plus LRU tiers),
+    recorded op by op."""
+    from resoctree.manifest import VolumeManifest, plan_levels
+    man = VolumeManifest(name="t", channel_count=3, dtype_original="u8",
+                         brick_size=(16, 16, 16),
+                         levels=plan_levels((64, 48, 40), (16, 16, 16), 3,
+                                            (2, 2, 2)))
+    eng = Engine(man, EngineConfig(octree_depth=3, cache_slots=(3, 2, 2),
+                                   channel_slots=2))
+    rng = np.random.default_rng(5)
+    k = len(man.levels)
+    ops = []
+    for i in range(1500):
+        op = rng.random()
+        slot = int(rng.integers(2))
+        lev = int(rng.integers(k))
+        grid = man.levels[lev].brick_grid_dims
+        coord = tuple(int(rng.integers(grid[a])) for a in range(3))
+        bid = eng.paging.encode(slot, lev, coord)
+        if op < 0.6:
+            val = int(rng.integers(256))
+            payload = np.full((16, 16, 16), val, dtype=np.uint8)
+            _, evicted = eng.paging.insert_brick(bid, payload, eng.frame)
+            if evicted is not None:
+                eng.octree.on_brick_evicted(evicted)
+            eng.octree.on_brick_inserted(bid)
+            ops.append(["insert", bid, val, -1 if evicted is None else evicted])
+        elif op < 0.7:
+            resident = eng.paging.resident_brick_ids()
+            if resident:
+                victim = int(resident[int(rng.integers(len(resident)))])
+                lin = eng.paging.resident_slot(victim)
+                s, l2, c2 = eng.paging.decode(victim)
+                idx = eng.paging._entry_index(s, l2, c2)
+                eng.paging.pt_status[idx] = 0
+                eng.paging.pt_slot[idx] = -1
+                eng.paging._release_slot(lin)
+                eng.octree.on_brick_evicted(victim)
+                ops.append(["evict", victim])
+        elif op < 0.8:
+            eng.advance_frame()
+            mask = (rng.random(int(eng.paging.pt_offsets[-1])) < 0.2
+                    ).astype(np.uint8)
+            eng.note_sampled(mask)
+            ops.append(["advance_note", np.flatnonzero(mask).tolist()])
+        elif op < 0.95:
+            nidx = int(rng.integers(eng.octree.num_nodes))
+            mn = int(rng.integers(256))
+            mx = int(rng.integers(mn, 256))
+            eng.apply_metadata(nidx, slot, mn, mx)
+            ops.append(["meta", nidx, slot, mn, mx])
+        else:
+            ch = int(rng.integers(3))
+            eng.swap_channel(slot, ch)
+            ops.append(["swap", slot, ch])
+        if i % 50 == 49:
+            ops.append(["check", state_hashes(eng)])
+    ops.append(["check", state_hashes(eng)])
+    eng.paging.check_bijection()
+    eng.octree.check_mask_consistency()
+    eng.octree.check_leaf_ground_truth()
+    meta = {"dims": [64, 48, 40], "brick": [16, 16, 16], "levels": 3,
+            "depth": 3, "cache_slots": [3, 2, 2], "m": 2, "ops": ops}
+    return meta, {}
+
+
+def main():
+    tmp = tempfile.mkdtemp()
+    for name, fn in (("session_mc64", lambda: session_mc64(tmp)),
+                     ("vessel256_full", vessel256_full),
+                     ("skip_audit_shell64", lambda: skip_audit_shell64(tmp)),
+                     ("lru_replay", lru_replay)):
+        print("generating", name, flush=True)
+        meta, rec = fn()
+        with open(os.path.join(HERE, name + ".json"), "w") as f:
+            json.dump(meta, f)
+        if rec:
+            np.savez_compressed(os.path.join(HERE, name + ".npz"), **rec)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,185 @@
+"""Pin the CPU oracle to the reference's own outputs (tests/golden/).
+
+The fixtures were produced by running the reference (tests/golden/
+make_golden.py); these tests need no GPU and no /root/reference.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+import scenes
+
+
+def test_restated_ingest_matches_reference_pyramids():
+    for name, kind, chans in (("session_mc64", "mc64", range(4)),
+                              ("skip_audit_shell64", "shell64", [0]),
+                              ("vessel256_full", "vessel256", [0])):
+        meta, _ = load_golden(name)
+        assert scenes.pyramid_sha(scenes.store(kind), chans) == meta["pyramid_sha"], name
+
+
+def test_oracle_session_mc64_matches_reference(oracle_lib):
+    """Cold 4-channel session with LRU pressure, mixed level ranges and a
+    mid-stream double channel swap: every frame's image, ordered requests,
+    usage mask, histogram, counters and the full state after each step."""
+    from oracle.session import OracleSession, state_hashes
+    meta, rec = load_golden("session_mc64")
+    e = meta["engine"]
+    sess = OracleSession(scenes.store("mc64"), e["m"], e["depth"], e["cache_slots"],
+                         scenes.oracle_channels(meta["channels"]),
+                         scenes.render_kw(meta["render"]), e["pad"])
+    for item in meta["script"]:
+        if "swap" in item:
+            for slot, ch in item["swap"]:
+                sess.swap_channel(slot, ch)
+            assert state_hashes(sess.st) == item["after_swap"]
+            continue
+        i = item["frame"]
+        out = sess.step_frame(tuple(item["pose"]))
+        bad = scenes.check_frame(rec, f"f{i}_", out.image, out.brick_requests,
+                                 out.metadata_requests, out.required_mask,
+                                 out.level_histogram, out.pixel_required, out.counters)
+        assert not bad, (i, bad)
+        assert state_hashes(sess.st) == item["after"], i
+
+
+def test_oracle_vessel256_matches_reference(oracle_lib):
+    """Config 1: fully resident vessel 256^3, residency and reference modes,
+    five orbit poses, bit-identical to the reference (test_acceptance.py:104-123)."""
+    from oracle import raycast as orc
+    from oracle.session import prepare_full, state_hashes
+    from paper_2309_04393_b200.camera import orbit_pose
+    from paper_2309_04393_b200.volume import box_minmax_grid
+    meta, rec = load_golden("vessel256_full")
+    e = meta["engine"]
+    st = prepare_full(scenes.store("vessel256"), {0: 0}, 1, e["depth"],
+                      e["cache_slots"], e["pad"], box_minmax_grid)
+    assert state_hashes(st) == meta["state"]
+    ostate = orc.OracleState(m=1, k=st.k, brick_size=st.brick_size,
+                             level_dims=st.level_dims, level_grids=st.level_grids,
+                             pt_offsets=st.pt_offsets, pt_status=st.pt_status,
+                             pt_slot=st.pt_slot, cache=st.cache, words=st.words,
+                             depth=st.depth)
+    chans = scenes.oracle_channels(meta["channels"])
+    kw = scenes.render_kw(meta["render"])
+    for i, a in enumerate(meta["angles"]):
+        p = orbit_pose(a)
+        cam = (p.position, p.target, p.up, p.fov_deg)
+        for mode, pre in ((orc.MODE_RESIDENCY, "res"), (orc.MODE_REFERENCE, "ref")):
+            out = orc.render(ostate, chans, cam, mode=mode, threads=4, **kw)
+            bad = scenes.check_frame(rec, f"{pre}{i}_", out.image, out.brick_requests,
+                                     out.metadata_requests, out.required_mask,
+                                     out.level_histogram, out.pixel_required,
+                                     out.counters)
+            assert not bad, (i, pre, bad)
+
+
+def test_oracle_skip_audit_matches_reference(oracle_lib):
+    """Skip soundness audit (test_acceptance.py:138-160): converged sessions
+    under random TFs, audited against a fully resident reference paging."""
+    from oracle import raycast as orc
+    from oracle.session import OracleSession, prepare_full, state_hashes
+    from paper_2309_04393_b200.camera import orbit_pose
+    from paper_2309_04393_b200.volume import box_minmax_grid
+    meta, rec = load_golden("skip_audit_shell64")
+    e = meta["engine"]
+    store = scenes.store("shell64")
+    ref = prepare_full(store, {0: 0}, 1, e["depth"], scenes.full_cache_slots(store, 1),
+                       e["pad"], box_minmax_grid)
+    assert state_hashes(ref) == meta["ref_state"]
+    ref_state = orc.OracleState(m=1, k=ref.k, brick_size=ref.brick_size,
+                                level_dims=ref.level_dims, level_grids=ref.level_grids,
+                                pt_offsets=ref.pt_offsets, pt_status=ref.pt_status,
+                                pt_slot=ref.pt_slot, cache=ref.cache)
+    poses = [orbit_pose(a) for a in meta["poses"]]
+    cams = [(p.position, p.target, p.up, p.fov_deg) for p in poses]
+    for r, run in enumerate(meta["runs"]):
+        chans = scenes.oracle_channels([{"slot": 0, "tf": run["tf"],
+                                         "level_range": [0, 15]}])
+        sess = OracleSession(store, 1, e["depth"], e["cache_slots"], chans,
+                             scenes.render_kw(meta["render"]), e["pad"])
+        streak, last, frames = 0, None, 0
+        for _ in range(50):
+            out = sess.step_frame(cams[0])
+            frames += 1
+            dig = out.image.tobytes()
+            nreq = len(out.brick_requests) + len(out.metadata_requests)
+            streak = streak + 1 if (nreq == 0 and dig == last) else (1 if nreq == 0 else 0)
+            last = dig
+            if streak >= 2:
+                break
+        assert frames == run["frames"]
+        assert state_hashes(sess.st) == run["state"]
+        for j, cam in enumerate(cams):
+            out = sess.render(cam, reference_state=ref_state)
+            bad = scenes.check_frame(rec, f"r{r}p{j}_", out.image, out.brick_requests,
+                                     out.metadata_requests, out.required_mask,
+                                     out.level_histogram, out.pixel_required,
+                                     out.counters)
+            assert not bad, (r, j, bad)
+            assert out.counters[3] == 0
+
+
+def test_oracle_lru_replay_matches_reference():
+    """Randomised insert / explicit evict / LRU touch / metadata / swap
+    sequence (verify.py:88-136 + frame advances): state hashes at every
+    checkpoint and every evicted id."""
+    from oracle.session import state_hashes
+    from oracle.state import OracleResidency
+    meta, _ = load_golden("lru_replay")
+    from paper_2309_04393_b200.volume import plan_levels
+    levels = plan_levels(tuple(meta["dims"]), tuple(meta["brick"]), meta["levels"], (2, 2, 2))
+    st = OracleResidency(meta["m"], meta["levels"], tuple(meta["brick"]),
+                         [l.dims for l in levels], [l.brick_grid_dims for l in levels],
+                         tuple(meta["cache_slots"]), meta["depth"])
+    frame = 0
+    sx, sy, sz = meta["brick"]
+    for op in meta["ops"]:
+        kind = op[0]
+        if kind == "insert":
+            payload = np.full((sz, sy, sx), op[2], dtype=np.uint8)
+            _, ev = st.apply_brick(op[1], payload, frame)
+            assert (-1 if ev is None else ev) == op[3]
+        elif kind == "evict":
+            slot, lev, coord = __import__("oracle.state", fromlist=["decode"]).decode(op[1], st.k)
+            e = st.entry(slot, lev, coord)
+            lin = int(st.pt_slot[e])
+            st.pt_status[e] = 0
+            st.pt_slot[e] = -1
+            st.release_slot(lin)
+            st.on_brick_evicted(op[1])
+        elif kind == "advance_note":
+            frame += 1
+            mask = np.zeros(int(st.pt_offsets[-1]), dtype=np.uint8)
+            mask[op[1]] = 1
+            st.note_sampled(mask, frame)
+        elif kind == "meta":
+            st.set_node_metadata(op[1], op[2], op[3], op[4])
+        elif kind == "swap":
+            st.swap_channel(op[1])
+        elif kind == "check":
+            assert state_hashes(st) == op[1]
+
+
+@pytest.mark.parametrize("threads", [1, 3])
+def test_oracle_row_bands_merge_to_full_frame(oracle_lib, threads):
+    """Row-band rendering + scanline-order merge equals one full pass (the
+    CPU-baseline and sort-first merge rule)."""
+    from oracle import raycast as orc
+    from oracle.session import OracleSession
+    meta, _ = load_golden("session_mc64")
+    e = meta["engine"]
+    sess = OracleSession(scenes.store("mc64"), e["m"], e["depth"], e["cache_slots"],
+                         scenes.oracle_channels(meta["channels"]),
+                         scenes.render_kw(meta["render"]), e["pad"])
+    cam = tuple(meta["script"][0]["pose"])
+    for _ in range(3):
+        sess.step_frame(cam)
+    full = sess.render(cam)
+    par = sess.render(cam, threads=threads)
+    assert np.array_equal(full.image, par.image)
+    assert full.all_brick_requests == par.all_brick_requests
+    assert full.all_metadata_requests == par.all_metadata_requests
+    assert np.array_equal(full.required_mask, par.required_mask)
+    assert np.array_equal(full.counters, par.counters)
