@@ -1,0 +1,149 @@
+"""Sort-first multi-GPU frames.
+
+Rows are cut in blocks of ``tile_rows``; block b is rendered by part
+b % n_parts (round-robin, so every GPU gets a fair share of the dense middle
+of the image).  Every GPU holds its own replica of the render state (octree
+words, page tables, brick cache) and renders its rows with the same kernel.
+
+One exchange step per frame, over NCCL / NVLink:
+  * image tiles      -> gathered to rank 0 (f32 RGBA, 33 MB at 1080p)
+  * request lists    -> all-gathered (key, id) pairs, <= budget per rank;
+                        merged by key = (pixel << 32 | event), keep-first,
+                        bricks-first budget -- identical on every rank, so
+                        every replica applies the same uploads (parity mode)
+  * usage mask       -> all-reduce MAX (u8), then note_sampled everywhere
+  * counters / hist  -> all-reduce SUM
+The merged result is bit-identical to a single-GPU frame (tested in
+tests/test_gpu_parity.py and, for the exchange itself, with gloo on CPU in
+tests/test_distributed.py).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+
+def part_rows(height: int, n_parts: int, part: int, tile_rows: int) -> list:
+    rows = []
+    blocks = (height + tile_rows - 1) // tile_rows
+    for b in range(part, blocks, n_parts):
+        rows.extend(range(b * tile_rows, min((b + 1) * tile_rows, height)))
+    return rows
+
+
+def _np(x):
+    if isinstance(x, torch.Tensor):
+        return x.detach().cpu().numpy()
+    return np.asarray(x)
+
+
+def merge_feedback(key_id_lists, budget: int, m: int):
+    """key_id_lists: [(bkeys, bids, mkeys, mids)] per part (numpy).
+
+    Returns (bricks, metas) exactly as one full-frame pass would."""
+    def merge(keys, ids):
+        if not keys:
+            return []
+        k = np.concatenate(keys)
+        v = np.concatenate(ids)
+        order = np.argsort(k, kind="stable")
+        out, seen = [], set()
+        for i in order:
+            x = int(v[i])
+            if x not in seen:
+                seen.add(x)
+                out.append(x)
+        return out
+
+    bricks = merge([p[0] for p in key_id_lists], [p[1] for p in key_id_lists])[:budget]
+    metas = merge([p[2] for p in key_id_lists], [p[3] for p in key_id_lists])
+    metas = [(v // m, v % m) for v in metas[:budget - len(bricks)]]
+    return bricks, metas
+
+
+def merge_parts(parts, image_dims, n_parts, tile_rows, budget, m) -> dict:
+    """Assemble per-part device/host results into the full-frame outputs."""
+    w, h = image_dims
+    image = np.zeros((h, w, 4), dtype=np.float32)
+    pixreq = np.zeros(h * w, dtype=np.int32)
+    lists = []
+    required = None
+    hist = None
+    counters = None
+    for p, part in enumerate(parts):
+        rows = part_rows(h, n_parts, p, tile_rows)
+        img = _np(part["image"]).reshape(-1, w, 4)[:len(rows)]
+        image[rows] = img
+        pr = _np(part["pix_required"]).reshape(-1, w)[:len(rows)]
+        pixreq.reshape(h, w)[rows] = pr
+        counts = _np(part["counts"])
+        fb = _np(part["fb"])
+        nb, nm = int(counts[2]), int(counts[3])
+        lists.append((fb[0][:nb], fb[1][:nb], fb[2][:nm], fb[3][:nm]))
+        r = _np(part["required"])
+        required = r.copy() if required is None else (required | r)
+        hs = _np(part["hist"])
+        hist = hs.copy() if hist is None else hist + hs
+        c = _np(part["counters"])
+        counters = c.copy() if counters is None else counters + c
+    bricks, metas = merge_feedback(lists, budget, m)
+    return dict(image=image, pix_required=pixreq, bricks=bricks, metas=metas,
+                required=required, hist=hist, counters=counters)
+
+
+def exchange(local: dict, image_dims, tile_rows: int, budget: int, m: int,
+             gather_image: bool = True) -> dict:
+    """One frame's collective step; every rank returns the merged feedback,
+    rank 0 also the assembled image.
+
+    local: image (local_rows*w, 4), required (E,) u8, pix_required, hist,
+    counters (tensors on this rank's device), fb (4, budget) i64 tensor,
+    counts (4,) host array."""
+    world = dist.get_world_size()
+    rank = dist.get_rank()
+    w, h = image_dims
+    dev = local["required"].device
+    # usage mask, histogram, counters
+    required = local["required"].clone()
+    dist.all_reduce(required, op=dist.ReduceOp.MAX)
+    hist = local["hist"].clone()
+    dist.all_reduce(hist)
+    counters = local["counters"].clone()
+    dist.all_reduce(counters)
+    # request lists: fixed-size (4, budget) blocks + counts
+    fb = local["fb"].contiguous()
+    counts = torch.as_tensor(np.asarray(local["counts"], dtype=np.int64), device=dev)
+    fbs = [torch.empty_like(fb) for _ in range(world)]
+    cts = [torch.empty_like(counts) for _ in range(world)]
+    dist.all_gather(fbs, fb)
+    dist.all_gather(cts, counts)
+    lists = []
+    for f, c in zip(fbs, cts):
+        f = f.cpu().numpy()
+        c = c.cpu().numpy()
+        nb, nm = int(c[2]), int(c[3])
+        lists.append((f[0][:nb], f[1][:nb], f[2][:nm], f[3][:nm]))
+    bricks, metas = merge_feedback(lists, budget, m)
+    out = dict(bricks=bricks, metas=metas, required=required, hist=hist,
+               counters=counters)
+    if gather_image:
+        max_rows = max(len(part_rows(h, world, p, tile_rows)) for p in range(world))
+        img = torch.zeros((max_rows * w, 4), dtype=torch.float32, device=dev)
+        img[:local["image"].shape[0]] = local["image"]
+        parts = [torch.empty_like(img) for _ in range(world)] if rank == 0 else None
+        try:
+            dist.gather(img, parts, dst=0)
+        except (RuntimeError, ValueError):
+            parts_all = [torch.empty_like(img) for _ in range(world)]
+            dist.all_gather(parts_all, img)
+            parts = parts_all if rank == 0 else None
+        if rank == 0:
+            full = torch.empty((h, w, 4), dtype=torch.float32, device=dev)
+            for p in range(world):
+                rows = part_rows(h, world, p, tile_rows)
+                idx = torch.as_tensor(rows, device=dev, dtype=torch.long)
+                full.index_copy_(0, idx, parts[p][:len(rows) * w].reshape(len(rows), w, 4))
+            out["image"] = full
+    return out

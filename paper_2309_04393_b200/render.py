@@ -256,6 +256,43 @@ def _buffers(paging, n_ch, npix_local, budget) -> DeviceFrame:
     return buf
 
 
+class FramePass:
+    """A packed frame bound to its state and output buffers: ``render()``
+    launches kernel 1, ``collect()`` orders/truncates the requests (kernel
+    3a, synchronising).  Reusable across frames with the same camera."""
+
+    def __init__(self, mode, paging: MultiChannelPaging, octree: ResidencyOctree | None,
+                 channels, camera: Camera, config: RenderConfig, reference_paging=None,
+                 partition=(1, 0, 8), bricks_first: bool = True):
+        N.require_cuda()
+        if mode == MODE_RESIDENCY:
+            if octree is None:
+                raise RenderError("residency mode needs the octree")
+            depth, eps_h = octree.config.depth, octree.config.homogeneity_eps
+        else:
+            depth, eps_h = 0, config.homogeneity_eps
+        self.paging = paging
+        self.config = config
+        self.bricks_first = bricks_first
+        self.frame = _pack_frame(mode, paging, channels, camera, config, depth, eps_h,
+                                 reference_paging, partition)
+        w, h = config.image_dims
+        self.local_rows = N.lib().ro_local_rows(h, *partition)
+        self.buf = _buffers(paging, len(channels), self.local_rows * w,
+                            config.max_requests_per_frame)
+        self.state = paging.state(with_words=(mode == MODE_RESIDENCY))
+
+    def render(self):
+        N.check(N.lib().ro_render(self.paging.ctx, C.byref(self.frame), C.byref(self.state),
+                                  C.byref(self.buf.outputs), N.stream_ptr()))
+
+    def collect(self):
+        N.check(N.lib().ro_feedback_collect(self.paging.ctx,
+                                            self.config.max_requests_per_frame,
+                                            1 if self.bricks_first else 0,
+                                            C.byref(self.buf.feedback), N.stream_ptr()))
+
+
 def render_frame_device(mode, paging: MultiChannelPaging, octree: ResidencyOctree | None,
                         channels, camera: Camera, config: RenderConfig,
                         reference_paging=None, partition=(1, 0, 8),
@@ -264,27 +301,12 @@ def render_frame_device(mode, paging: MultiChannelPaging, octree: ResidencyOctre
 
     Not re-entrant per paging: the returned buffers are reused by the next
     call with the same shape."""
-    N.require_cuda()
-    if mode == MODE_RESIDENCY:
-        if octree is None:
-            raise RenderError("residency mode needs the octree")
-        depth, eps_h = octree.config.depth, octree.config.homogeneity_eps
-    else:
-        depth, eps_h = 0, config.homogeneity_eps
-    F = _pack_frame(mode, paging, channels, camera, config, depth, eps_h,
-                    reference_paging, partition)
-    w, h = config.image_dims
-    rows = N.lib().ro_local_rows(h, *partition)
-    buf = _buffers(paging, len(channels), rows * w, config.max_requests_per_frame)
-    st = paging.state(with_words=(mode == MODE_RESIDENCY))
-    s = N.stream_ptr()
-    N.check(N.lib().ro_render(paging.ctx, C.byref(F), C.byref(st),
-                              C.byref(buf.outputs), s))
+    fp = FramePass(mode, paging, octree, channels, camera, config, reference_paging,
+                   partition, bricks_first)
+    fp.render()
     if collect:
-        N.check(N.lib().ro_feedback_collect(paging.ctx, config.max_requests_per_frame,
-                                            1 if bricks_first else 0,
-                                            C.byref(buf.feedback), s))
-    return buf
+        fp.collect()
+    return fp.buf
 
 
 def _run(mode, paging, channels, camera, config, octree=None,

@@ -1,0 +1,394 @@
+"""CUDA path vs the reference's golden outputs and the CPU oracle.
+
+Bar: request lists (ordered), usage mask, octree words,
+page tables, slot arrays, counters and histograms bit-exact; images
+bit-exact too (the kernel replays the reference's fp64 operation order,
+-fmad=false).  IMAGE_ATOL is the north-star bound (1/255) used only by the
+full-size property tests where the oracle is not run on every pixel.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import cuda_ok, load_golden
+import scenes
+from gpu_helpers import (cam_tuple, device_state_hashes, diff_hashes,
+                         oracle_state_from_device)
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not cuda_ok(), reason="needs a CUDA device")]
+
+IMAGE_ATOL = 1.0 / 255.0
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib(native_lib, oracle_lib):
+    return native_lib
+
+
+def _check(rec, prefix, out):
+    return scenes.check_frame(rec, prefix, out.image, out.brick_requests,
+                              out.metadata_requests, out.required_mask,
+                              out.level_histogram, out.pixel_required,
+                              [out.stats.traversal_steps, out.stats.samples_evaluated,
+                               out.stats.samples_skipped, out.stats.skip_violations])
+
+
+def test_gpu_session_mc64_matches_reference():
+    from paper_2309_04393_b200 import EngineConfig, LocalTransport, Session
+    meta, rec = load_golden("session_mc64")
+    e = meta["engine"]
+    sess = Session(LocalTransport(scenes.store("mc64")),
+                   EngineConfig(octree_depth=e["depth"], cache_slots=tuple(e["cache_slots"]),
+                                channel_slots=e["m"]),
+                   scenes.render_config(meta["render"]),
+                   scenes.product_channels(meta["channels"]))
+    from paper_2309_04393_b200 import Camera
+    for item in meta["script"]:
+        if "swap" in item:
+            for slot, ch in item["swap"]:
+                sess.swap_channel(slot, ch)
+            assert not diff_hashes(device_state_hashes(sess.engine), item["after_swap"])
+            continue
+        i = item["frame"]
+        pos, tgt, up, fov = item["pose"]
+        r = sess.step_frame(Camera(position=tuple(pos), target=tuple(tgt), up=tuple(up),
+                                   fov_deg=fov))
+        bad = _check(rec, f"f{i}_", r.output)
+        assert not bad, (i, bad)
+        assert r.bricks_applied == item["bricks_applied"]
+        assert r.metadata_applied == item["metadata_applied"]
+        d = diff_hashes(device_state_hashes(sess.engine), item["after"])
+        assert not d, (i, d)
+    sess.close()
+
+
+def _prepared_engine(kind, m=1, depth=5, slots_to_channels=None):
+    from paper_2309_04393_b200 import Engine, EngineConfig
+    st = scenes.store(kind)
+    slots_to_channels = slots_to_channels or {0: 0}
+    eng = Engine(st.manifest, EngineConfig(octree_depth=depth,
+                                           cache_slots=scenes.full_cache_slots(st, m),
+                                           channel_slots=m))
+    for s, c in slots_to_channels.items():
+        eng.paging.channel_mapping[s] = c
+    eng.prefill(lambda s, lev, c: st.brick(slots_to_channels[s], lev, c),
+                slots=sorted(slots_to_channels))
+    eng.fill_metadata_from_volumes({s: st.level_array(c, 0)
+                                    for s, c in slots_to_channels.items()})
+    return eng
+
+
+def test_gpu_vessel256_matches_reference():
+    """Config 1 (test_acceptance.py:44-123): fully resident vessel 256^3,
+    residency == reference mode == reference outputs, five poses."""
+    from paper_2309_04393_b200 import orbit_pose, render_frame, render_reference
+    meta, rec = load_golden("vessel256_full")
+    eng = _prepared_engine("vessel256", depth=meta["engine"]["depth"])
+    assert not diff_hashes(device_state_hashes(eng), meta["state"])
+    chans = scenes.product_channels(meta["channels"])
+    cfg = scenes.render_config(meta["render"])
+    for i, a in enumerate(meta["angles"]):
+        pose = orbit_pose(a)
+        out = render_frame(eng.paging, eng.octree, chans, pose, cfg)
+        assert not _check(rec, f"res{i}_", out), i
+        ref = render_reference(eng.paging, chans, pose, cfg)
+        assert not _check(rec, f"ref{i}_", ref), i
+        assert np.array_equal(out.image, ref.image)
+
+
+def test_gpu_skip_audit_matches_reference():
+    from paper_2309_04393_b200 import (EngineConfig, LocalTransport, Session,
+                                       orbit_pose, render_frame)
+    meta, rec = load_golden("skip_audit_shell64")
+    e = meta["engine"]
+    ref_eng = _prepared_engine("shell64", depth=e["depth"])
+    assert not diff_hashes(device_state_hashes(ref_eng), meta["ref_state"])
+    cfg = scenes.render_config(meta["render"])
+    poses = [orbit_pose(a) for a in meta["poses"]]
+    for r, run in enumerate(meta["runs"]):
+        chans = scenes.product_channels([{"slot": 0, "tf": run["tf"], "level_range": [0, 15]}])
+        sess = Session(LocalTransport(scenes.store("shell64")),
+                       EngineConfig(octree_depth=e["depth"],
+                                    cache_slots=tuple(e["cache_slots"]), channel_slots=1),
+                       cfg, chans)
+        recs = sess.run_until_converged(poses[0], max_frames=50)
+        assert sess.converged and len(recs) == run["frames"]
+        assert not diff_hashes(device_state_hashes(sess.engine), run["state"])
+        for j, pose in enumerate(poses):
+            out = render_frame(sess.engine.paging, sess.engine.octree, chans, pose, cfg,
+                               reference_paging=ref_eng.paging)
+            assert not _check(rec, f"r{r}p{j}_", out), (r, j)
+            assert out.stats.skip_violations == 0
+        sess.close()
+
+
+def test_gpu_lru_replay_matches_reference():
+    """Op-by-op replay of the reference's randomised residency workload."""
+    from paper_2309_04393_b200 import Engine, EngineConfig
+    from paper_2309_04393_b200.volume import VolumeManifest, plan_levels
+    meta, _ = load_golden("lru_replay")
+    levels = plan_levels(tuple(meta["dims"]), tuple(meta["brick"]), meta["levels"], (2, 2, 2))
+    man = VolumeManifest(name="t", channel_count=3, brick_size=tuple(meta["brick"]),
+                         levels=levels)
+    eng = Engine(man, EngineConfig(octree_depth=meta["depth"],
+                                   cache_slots=tuple(meta["cache_slots"]),
+                                   channel_slots=meta["m"]))
+    sx, sy, sz = meta["brick"]
+    E = eng.paging.total_entries
+    for op in meta["ops"]:
+        kind = op[0]
+        if kind == "insert":
+            payload = np.full((1, sz, sy, sx), op[2], dtype=np.uint8)
+            _, ev = eng.apply_bricks([op[1]], payload, return_slots=True)
+            assert int(ev[0]) == op[3]
+        elif kind == "evict":
+            eng.evict_bricks([op[1]])
+        elif kind == "advance_note":
+            eng.advance_frame()
+            mask = np.zeros(E, dtype=np.uint8)
+            mask[op[1]] = 1
+            eng.note_sampled(mask)
+        elif kind == "meta":
+            eng.apply_metadata(op[1], op[2], op[3], op[4])
+        elif kind == "swap":
+            eng.swap_channel(op[1], op[2])
+        elif kind == "check":
+            d = diff_hashes(device_state_hashes(eng), op[1])
+            assert not d, d
+    eng.paging.check_bijection()
+    eng.octree.check_mask_consistency()
+    eng.octree.check_leaf_ground_truth()
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_gpu_batched_lru_equals_sequential(seed):
+    """Whole-frame batches (free-list pops, stale victims in (last_used, slot)
+    order, slot-0 thrash once every slot is stamped this frame) equal the
+    reference's one-by-one insert_brick + octree updates."""
+    from oracle.session import state_hashes
+    from oracle.state import OracleResidency
+    from paper_2309_04393_b200 import Engine, EngineConfig
+    from paper_2309_04393_b200.volume import VolumeManifest, plan_levels
+    rng = np.random.default_rng(seed)
+    levels = plan_levels((64, 40, 48), (8, 8, 8), 3, (2, 2, 2))
+    man = VolumeManifest(name="t", channel_count=2, brick_size=(8, 8, 8), levels=levels)
+    cache = (5, 3, 2)
+    eng = Engine(man, EngineConfig(octree_depth=4, cache_slots=cache, channel_slots=2))
+    ora = OracleResidency(2, 3, (8, 8, 8), [l.dims for l in levels],
+                          [l.brick_grid_dims for l in levels], cache, 4)
+    E = eng.paging.total_entries
+    for step in range(40):
+        eng.advance_frame()
+        mask = (rng.random(E) < 0.3).astype(np.uint8)
+        eng.note_sampled(mask)
+        ora.note_sampled(mask, eng.frame)
+        # a batch of unique, currently unmapped bricks (size up to 2x cache)
+        unm = np.flatnonzero(ora.pt_status == 0)
+        nb = int(rng.integers(1, min(len(unm), 60) + 1))
+        entries = rng.choice(unm, size=nb, replace=False)
+        ids = []
+        for e in entries:
+            pt = int(np.searchsorted(ora.pt_offsets, e, side="right") - 1)
+            slot, lev = pt // 3, pt % 3
+            g = ora.level_grids[lev]
+            loc = int(e - ora.pt_offsets[pt])
+            x, y, z = loc % g[0], (loc // g[0]) % g[1], loc // (g[0] * g[1])
+            ids.append(((slot * 3 + lev) << 24) | (int(z) << 16) | (int(y) << 8) | int(x))
+        pay = rng.integers(0, 256, size=(nb, 8, 8, 8), dtype=np.uint8)
+        slots, evicted = eng.apply_bricks(ids, pay, return_slots=True)
+        for i, b in enumerate(ids):
+            lin, ev = ora.apply_brick(b, pay[i], eng.frame)
+            assert int(slots[i]) == lin and int(evicted[i]) == (-1 if ev is None else ev)
+        if step % 7 == 3:
+            s = int(rng.integers(2))
+            eng.swap_channel(s, int(rng.integers(2)))
+            ora.swap_channel(s)
+        d = diff_hashes(device_state_hashes(eng), state_hashes(ora))
+        assert not d, (step, d)
+
+
+def _random_partial_engine(seed, eps=0.0, depth=3, m=4, cache=(6, 6, 6)):
+    """mc64 channels with a random resident subset and random INVALID /
+    valid metadata: exercises MISSU, MISSP, substitution, meta requests."""
+    from paper_2309_04393_b200 import Engine, EngineConfig
+    st = scenes.store("mc64")
+    rng = np.random.default_rng(seed)
+    eng = Engine(st.manifest, EngineConfig(octree_depth=depth, cache_slots=cache,
+                                           channel_slots=m, homogeneity_eps=eps))
+    k = len(st.manifest.levels)
+    ids, pays = [], []
+    for s in range(m):
+        for lev in range(k):
+            gx, gy, gz = st.manifest.levels[lev].brick_grid_dims
+            for z in range(gz):
+                for y in range(gy):
+                    for x in range(gx):
+                        if rng.random() < 0.45:
+                            ids.append(eng.paging.encode(s, lev, (x, y, z)))
+                            pays.append(st.brick(s % 4, lev, (x, y, z)))
+    order = rng.permutation(len(ids))
+    ids = [ids[i] for i in order][:eng.paging.num_slots]
+    pays = np.stack([pays[i] for i in order][:eng.paging.num_slots])
+    eng.apply_bricks(ids, pays)
+    eng.fill_metadata_from_volumes({s: st.level_array(s % 4, 0) for s in range(m)})
+    # knock out metadata at random nodes -> INVALID words
+    words = eng.octree.words.copy()
+    kill = rng.random(words.shape) < 0.25
+    words[kill] = (words[kill] & np.uint32(0xFFFF)) | np.uint32(0x00FF0000)
+    eng.octree.upload_words(words)
+    return eng
+
+
+@pytest.mark.parametrize("seed,eps,ranges", [
+    (0, 0.0, [(0, 2), (0, 2), (0, 2), (0, 2)]),
+    (1, 0.0, [(0, 0), (1, 2), (2, 2), (0, 1)]),
+    (2, 12.0, [(0, 2), (1, 1), (0, 2), (2, 2)]),
+    (3, 3.0, [(1, 2), (0, 2), (0, 0), (0, 2)]),
+])
+def test_gpu_partial_residency_matches_oracle(seed, eps, ranges):
+    from oracle import raycast as orc
+    from paper_2309_04393_b200 import (ChannelSettings, RenderConfig, TransferFunction,
+                                       grayscale_ramp_tf, orbit_pose, render_frame,
+                                       render_reference)
+    eng = _random_partial_engine(seed, eps=eps)
+    tfs = [grayscale_ramp_tf(40.0),
+           TransferFunction(points=((0.0, (0, 0, 0, 0)), (20.0, (0.1, 0.9, 0.2, 0.0)),
+                                    (90.0, (1.0, 0.2, 0.1, 0.5)), (255.0, (0.2, 0.4, 1.0, 0.8)))),
+           grayscale_ramp_tf(10.0, max_alpha=0.4),
+           TransferFunction(points=((0.0, (0, 0, 0, 0)), (100.0, (1, 1, 0, 0.9)),
+                                    (101.0, (0, 0, 0, 0)), (255.0, (0, 0, 0, 0))))]
+    order = [2, 0, 3, 1] if seed % 2 else [0, 1, 2, 3]
+    chans = [ChannelSettings(slot=s, tf=tfs[s], level_range=ranges[s]) for s in order]
+    ost = oracle_state_from_device(eng)
+    och = [orc.OracleChannel(slot=c.slot, points=c.tf.points, level_range=c.level_range)
+           for c in chans]
+    for angle, dims, step, budget in ((0.4, (61, 37), 1 / 64, 40), (2.9, (32, 48), 1 / 100, 7),
+                                      (4.6, (50, 50), 1 / 40, 300)):
+        cfg = RenderConfig(image_dims=dims, base_step=step, max_requests_per_frame=budget)
+        pose = orbit_pose(angle, radius=1.7)
+        out = render_frame(eng.paging, eng.octree, chans, pose, cfg)
+        want = orc.render(ost, och, cam_tuple(pose), dims, step, budget=budget)
+        assert np.array_equal(out.image, want.image), (
+            int((out.image != want.image).sum()), float(np.abs(out.image - want.image).max()))
+        assert out.brick_requests == want.brick_requests
+        assert out.metadata_requests == want.metadata_requests
+        assert np.array_equal(out.required_mask, want.required_mask)
+        assert np.array_equal(out.level_histogram, want.level_histogram)
+        assert np.array_equal(out.pixel_required, want.pixel_required)
+        assert [out.stats.traversal_steps, out.stats.samples_evaluated,
+                out.stats.samples_skipped] == list(want.counters[:3])
+        ref = render_reference(eng.paging, chans, pose, cfg)
+        wr = orc.render(ost, och, cam_tuple(pose), dims, step, budget=budget,
+                        mode=orc.MODE_REFERENCE)
+        assert np.array_equal(ref.image, wr.image)
+        assert np.array_equal(ref.required_mask, wr.required_mask)
+        assert np.array_equal(ref.level_histogram, wr.level_histogram)
+
+
+@pytest.mark.parametrize("n_parts", [2, 3, 5])
+def test_gpu_sort_first_parts_merge_to_full_frame(n_parts):
+    """Sort-first partition (row blocks round-robin over parts): per-part
+    images, usage masks, counters and (key, id) request lists merge into the
+    single-GPU frame exactly -- the multi-GPU parity mode of SURVEY §8(e)."""
+    import torch
+    from paper_2309_04393_b200 import (ChannelSettings, RenderConfig, grayscale_ramp_tf,
+                                       orbit_pose, render_frame)
+    from paper_2309_04393_b200.distributed import merge_parts, part_rows
+    from paper_2309_04393_b200.render import MODE_RESIDENCY, render_frame_device
+    eng = _random_partial_engine(7)
+    chans = [ChannelSettings(slot=s, tf=grayscale_ramp_tf(30.0)) for s in range(4)]
+    cfg = RenderConfig(image_dims=(45, 70), base_step=1 / 64, max_requests_per_frame=50)
+    pose = orbit_pose(1.3, radius=1.8)
+    full = render_frame(eng.paging, eng.octree, chans, pose, cfg)
+    parts = []
+    for p in range(n_parts):
+        buf = render_frame_device(MODE_RESIDENCY, eng.paging, eng.octree, chans, pose, cfg,
+                                  partition=(n_parts, p, 8), bricks_first=False)
+        parts.append({k: v.clone() if isinstance(v, torch.Tensor) else v
+                      for k, v in dict(image=buf.image, required=buf.required,
+                                       pix_required=buf.pix_required, hist=buf.hist,
+                                       counters=buf.counters, fb=buf.fb,
+                                       counts=buf.counts.copy()).items()})
+    merged = merge_parts(parts, cfg.image_dims, n_parts, 8, cfg.max_requests_per_frame,
+                         eng.paging.config.m)
+    assert np.array_equal(merged["image"], full.image)
+    assert merged["bricks"] == full.brick_requests
+    assert merged["metas"] == full.metadata_requests
+    assert np.array_equal(merged["required"], full.required_mask)
+    assert np.array_equal(merged["hist"], full.level_histogram)
+    assert np.array_equal(merged["pix_required"], full.pixel_required)
+    assert merged["counters"][0] == full.stats.traversal_steps
+    rows = sum(len(part_rows(cfg.image_dims[1], n_parts, p, 8)) for p in range(n_parts))
+    assert rows == cfg.image_dims[1]
+
+
+def test_gpu_edge_cases():
+    """1x1 image, a camera looking away from the volume (every ray misses),
+    single channel k=1 depth 0, budget 1, eight channel slots."""
+    from oracle import raycast as orc
+    from paper_2309_04393_b200 import (Camera, ChannelSettings, Engine, EngineConfig,
+                                       RenderConfig, grayscale_ramp_tf, orbit_pose,
+                                       render_frame)
+    from paper_2309_04393_b200 import volume as V
+    st = V.VolumeStore([V.ramp_volume(32)] * 8, (16, 16, 16), 1, (2, 2, 2), normalize=False)
+    eng = Engine(st.manifest, EngineConfig(octree_depth=0, cache_slots=(4, 4, 4),
+                                           channel_slots=8))
+    eng.prefill(lambda s, lev, c: st.brick(s, lev, c))
+    eng.fill_metadata_from_volumes({s: st.level_array(s, 0) for s in range(8)})
+    chans = [ChannelSettings(slot=s, tf=grayscale_ramp_tf(20.0 * s, max_alpha=0.1))
+             for s in range(8)]
+    ost = oracle_state_from_device(eng)
+    och = [orc.OracleChannel(slot=c.slot, points=c.tf.points, level_range=c.level_range)
+           for c in chans]
+    for cam, dims, budget in ((orbit_pose(0.3), (1, 1), 1),
+                              (Camera(position=(3.0, 3.0, 3.0), target=(6.0, 6.0, 6.0)),
+                               (9, 7), 1),
+                              (orbit_pose(2.2, radius=1.3), (23, 19), 1)):
+        cfg = RenderConfig(image_dims=dims, base_step=1 / 50, max_requests_per_frame=budget)
+        out = render_frame(eng.paging, eng.octree, chans, cam, cfg)
+        want = orc.render(ost, och, cam_tuple(cam), dims, 1 / 50, budget=budget)
+        assert np.array_equal(out.image, want.image)
+        assert out.brick_requests == want.brick_requests
+        assert out.metadata_requests == want.metadata_requests
+        assert np.array_equal(out.level_histogram, want.level_histogram)
+
+
+def test_gpu_octree_incremental_equals_rebuild():
+    """Incremental octree pass after many batches == masks recomputed from
+    the resident set (leaf ground truth + OR closure)."""
+    eng = _random_partial_engine(11, depth=4, cache=(4, 4, 4))
+    before = eng.octree.words.copy()
+    eng.octree.rebuild_masks()
+    assert np.array_equal(before, eng.octree.words)
+    eng.octree.check_mask_consistency()
+    eng.octree.check_leaf_ground_truth()
+
+
+def test_gpu_cycif_small_scenario_matches_oracle():
+    """The bench scenario builder at reduced size: engine state built through
+    apply_bricks / write_level_metadata equals the numpy reference-layout
+    state, and a partial-residency multi-channel frame equals the oracle."""
+    import torch
+    from oracle import raycast as orc
+    from paper_2309_04393_b200 import render_frame, scenarios
+    scn = scenarios.cycif(device="cuda", dims=(256, 256, 32), n_cells=400,
+                          image_dims=(96, 54), depth=4)
+    eng = scenarios.build_engine(scn)
+    ref = orc.OracleState(**scenarios.reference_state(scn))
+    assert np.array_equal(eng.octree.words, ref.words)
+    assert np.array_equal(eng.paging.pt_status, ref.pt_status)
+    assert np.array_equal(eng.paging.pt_slot, ref.pt_slot)
+    out = render_frame(eng.paging, eng.octree, scn.channels, scn.camera, scn.render)
+    och = [orc.OracleChannel(slot=c.slot, points=c.tf.points, level_range=c.level_range)
+           for c in scn.channels]
+    want = orc.render(ref, och, cam_tuple(scn.camera), scn.render.image_dims,
+                      scn.render.base_step, budget=scn.render.max_requests_per_frame)
+    assert np.array_equal(out.image, want.image)
+    assert out.brick_requests == want.brick_requests
+    assert out.metadata_requests == want.metadata_requests
+    assert np.array_equal(out.required_mask, want.required_mask)
+    assert np.array_equal(out.level_histogram, want.level_histogram)
+    torch.cuda.synchronize()
