@@ -522,7 +522,7 @@ int apply_bricks(ro_ctx *c, const ro_state *st, const int64_t *ids_h, int64_t n6
     int64_t *d_ids = (int64_t *)p;
     int64_t *d_evicted = d_ids + n;
     int64_t *d_entries = d_evicted + n;
-    int32_t *d_slots = (int32_t *)(d_evicted + n);
+    int32_t *d_slots = (int32_t *)(d_entries + n);
     uint8_t *d_final = (uint8_t *)(d_slots + n);
     int32_t *d_flag = (int32_t *)(((uintptr_t)(d_final + n) + 15) & ~(uintptr_t)15);
 
@@ -566,7 +566,21 @@ int apply_bricks(ro_ctx *c, const ro_state *st, const int64_t *ids_h, int64_t n6
     RO_CUDA(cudaMemcpyAsync(h + 1, st->free_count, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     RO_CUDA(cudaStreamSynchronize(s));
     const int32_t flag = h[0], free_count = h[1];
-    if (flag & 2) return fail(RO_EINVAL, "brick id outside the layout");
+    if (flag & 2) {
+        std::vector<int64_t> back(n), ent(n);
+        cudaMemcpy(back.data(), d_ids, sizeof(int64_t) * n, cudaMemcpyDeviceToHost);
+        cudaMemcpy(ent.data(), d_entries, sizeof(int64_t) * n, cudaMemcpyDeviceToHost);
+        int32_t bad = -1;
+        for (int32_t i = 0; i < n; ++i)
+            if (ent[i] < 0) { bad = i; break; }
+        char msg[256];
+        snprintf(msg, sizeof msg,
+                 "brick id outside the layout (flag %d, n %d, first bad index %d, "
+                 "device id %lld, host id %lld)", flag, n, bad,
+                 bad >= 0 ? (long long)back[bad] : -1LL,
+                 bad >= 0 ? (long long)ids_h[bad] : -1LL);
+        return fail(RO_EINVAL, msg);
+    }
 
     int32_t p3 = n;  // first phase-(iii) index
     if (flag == 0) {
