@@ -194,7 +194,9 @@ def run_ours(args):
     setup_s = time.perf_counter() - t_setup
     cfg = scn.render
     w, h = cfg.image_dims
-    fp = FramePass(MODE_RESIDENCY, eng.paging, eng.octree, scn.channels, scn.camera, cfg,
+    from paper_2309_04393_b200.render import MODE_REFERENCE
+    mode = MODE_REFERENCE if args.mode == "reference" else MODE_RESIDENCY
+    fp = FramePass(mode, eng.paging, eng.octree, scn.channels, scn.camera, cfg,
                    partition=(world, rank, 8), bricks_first=(world == 1))
     stream = torch.cuda.current_stream()
     m = eng.paging.config.m
@@ -356,6 +358,9 @@ def main():
     ap.add_argument("--cpu-fraction", type=float, default=0.02)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--mode", default="residency", choices=["residency", "reference"],
+                    help="render mode of the timed pass (reference = MODE_REFERENCE, "
+                         "a diagnostic: no traversal / skipping)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

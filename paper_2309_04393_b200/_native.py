@@ -12,7 +12,7 @@ import os
 import torch  # noqa: F401  (loads the CUDA runtime libresoct.so links against)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libresoct.so")
+LIB_PATH = os.environ.get("RESOCT_LIB") or os.path.join(HERE, "libresoct.so")
 
 RO_MAX_LEVELS = 16
 RO_MAX_PT = 256

@@ -32,24 +32,35 @@ def _stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, defines=(), out=None) -> str:
+    """Compile csrc/*.cu into libresoct.so (or `out` with extra -D defines)."""
+    lib = out or LIB
+    if not force and out is None and not _stale():
         return LIB
-    objdir = os.path.join(HERE, "_obj")
+    tag = "_".join(d.replace("=", "") for d in defines) or "default"
+    objdir = os.path.join(HERE, "_obj", tag)
     os.makedirs(objdir, exist_ok=True)
     objs = []
     for src in SOURCES:
         obj = os.path.join(objdir, src.replace(".cu", ".o"))
-        cmd = [NVCC, *FLAGS, "-I", INCLUDE, "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-I", INCLUDE, "-c",
+               os.path.join(CSRC, src), "-o", obj]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         subprocess.run(cmd, check=True)
         objs.append(obj)
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
+    os.makedirs(os.path.dirname(lib), exist_ok=True)
     subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
                     "-o", tmp, *objs, "-lcudart"], check=True)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
+
+
+def build_variant(name: str, defines) -> str:
+    """Experiment builds (kernel variants) next to the package."""
+    return build(force=True, defines=tuple(defines),
+                 out=os.path.join(HERE, "_variants", f"libresoct_{name}.so"))
 
 
 if __name__ == "__main__":

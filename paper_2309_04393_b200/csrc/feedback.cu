@@ -1,11 +1,15 @@
 // feedback.cu -- kernel 3a: request ordering + budget, and the LRU touch.
 //
 // The ray caster leaves, per touched brick / metadata entry, the smallest
-// (pixel << 32 | event) key of any request for it (raycast.cu).  Sorting the
-// touched entries by that key reproduces the reference's single-threaded
-// first-seen append order (kernels.py:457-517, seen_brick / seen_meta); the
-// bricks-first budget is render.py:210-215.  Keys are reset in the same pass
-// so the next frame starts clean without an O(E) memset.
+// (pixel << 32 | event) key of any request for it (raycast.cu, RED.MIN).
+// Sorting the touched entries by that key reproduces the reference's
+// single-threaded first-seen append order (kernels.py:457-517, seen_brick /
+// seen_meta); the bricks-first budget is render.py:210-215.
+//
+// Touched entries are found by one streaming pass over the key arrays
+// (E u64 for bricks, N*m u64 for metadata: 0.6 MB + 9.6 MB at config 2),
+// which also resets them for the next frame -- cheaper than making every
+// request wait for an atomic's return value in the ray caster.
 #include <cub/cub.cuh>
 
 #include "internal.cuh"
@@ -14,16 +18,55 @@ namespace ro {
 
 namespace {
 
-__global__ void k_gather_keys(const int32_t *__restrict__ touched, int32_t n,
-                              unsigned long long *__restrict__ keys,
-                              unsigned long long *__restrict__ out_keys,
-                              int32_t *__restrict__ out_vals) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    int32_t e = touched[i];
-    out_keys[i] = keys[e];
-    out_vals[i] = e;
-    keys[e] = ~0ull;
+constexpr unsigned kScanBlocks = 148 * 4;
+
+// compact (key, entry) of every touched entry, reset the key; warp-aggregated
+// slot allocation
+__global__ void __launch_bounds__(256) k_compact(unsigned long long *__restrict__ keys,
+                                                 int64_t n,
+                                                 unsigned long long *__restrict__ out_keys,
+                                                 int32_t *__restrict__ out_vals,
+                                                 int32_t *__restrict__ count) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    // warp-uniform trip count (the shuffles need all 32 lanes)
+    for (int64_t wb = warp * 64; wb < n; wb += nwarps * 64) {
+        const int64_t base = wb + 2 * lane;
+        // two entries per lane: 16-byte loads
+        unsigned long long k0 = ~0ull, k1 = ~0ull;
+        if (base + 1 < n) {
+            const ulonglong2 v = *reinterpret_cast<const ulonglong2 *>(keys + base);
+            k0 = v.x;
+            k1 = v.y;
+        } else if (base < n) {
+            k0 = keys[base];
+        }
+        const bool t0 = k0 != ~0ull, t1 = k1 != ~0ull;
+        const int mine = (int)t0 + (int)t1;
+        int incl = mine;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        int basepos = 0;
+        if (lane == 31 && total) basepos = atomicAdd(count, total);
+        basepos = __shfl_sync(0xffffffffu, basepos, 31);
+        int pos = basepos + incl - mine;
+        if (t0) {
+            out_keys[pos] = k0;
+            out_vals[pos] = (int32_t)base;
+            keys[base] = ~0ull;
+            ++pos;
+        }
+        if (t1) {
+            out_keys[pos] = k1;
+            out_vals[pos] = (int32_t)(base + 1);
+            keys[base + 1] = ~0ull;
+        }
+    }
 }
 
 __global__ void k_emit_bricks(const DevLayout L,
@@ -60,36 +103,37 @@ __global__ void k_note_sampled(const uint8_t *__restrict__ required,
     }
 }
 
-// sort n (key, value) pairs held at ctx scratch and emit the first `keep`
-int sort_and_emit(ro_ctx *c, unsigned long long *key_arr, const int32_t *touched,
-                  int32_t n, int32_t keep, bool bricks, int64_t *out_keys,
-                  int64_t *out_ids, cudaStream_t s) {
-    if (n <= 0) return RO_OK;
-    void *p0, *p1, *p2, *p3, *tmp;
+inline unsigned scan_blocks(int64_t n) {
+    int64_t b = (n + 511) / 512;
+    if (b < 1) b = 1;
+    if (b > kScanBlocks) b = kScanBlocks;
+    return (unsigned)b;
+}
+
+// sort the n compacted (key, entry) pairs and emit the first `keep`
+int sort_and_emit(ro_ctx *c, unsigned long long *k_in, int32_t *v_in, int32_t n,
+                  int32_t keep, bool bricks, int64_t *out_keys, int64_t *out_ids,
+                  cudaStream_t s) {
+    if (n <= 0 || keep <= 0) return RO_OK;
+    void *p1, *p3, *tmp;
     int rc;
-    if ((rc = scratch(c, 0, sizeof(unsigned long long) * n, &p0))) return rc;
     if ((rc = scratch(c, 1, sizeof(unsigned long long) * n, &p1))) return rc;
-    if ((rc = scratch(c, 2, sizeof(int32_t) * n, &p2))) return rc;
     if ((rc = scratch(c, 3, sizeof(int32_t) * n, &p3))) return rc;
-    auto *k_in = (unsigned long long *)p0, *k_out = (unsigned long long *)p1;
-    auto *v_in = (int32_t *)p2, *v_out = (int32_t *)p3;
-    k_gather_keys<<<(n + 255) / 256, 256, 0, s>>>(touched, n, key_arr, k_in, v_in);
-    RO_CUDA(cudaGetLastError());
+    auto *k_out = (unsigned long long *)p1;
+    auto *v_out = (int32_t *)p3;
+    // keys are (pixel << 32 | event): only the bits up to the top pixel matter
     size_t tmp_bytes = 0;
-    RO_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k_in, k_out, v_in,
-                                            v_out, n, 0, 64, s));
+    RO_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k_in, k_out, v_in, v_out, n,
+                                            0, 64, s));
     if ((rc = scratch(c, 4, tmp_bytes, &tmp))) return rc;
-    RO_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, k_in, k_out, v_in,
-                                            v_out, n, 0, 64, s));
-    if (keep > 0) {
-        if (bricks)
-            k_emit_bricks<<<(keep + 255) / 256, 256, 0, s>>>(c->dl, k_out, v_out, keep,
-                                                              out_keys, out_ids);
-        else
-            k_emit_metas<<<(keep + 255) / 256, 256, 0, s>>>(k_out, v_out, keep,
-                                                             out_keys, out_ids);
-        RO_CUDA(cudaGetLastError());
-    }
+    RO_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, k_in, k_out, v_in, v_out, n, 0,
+                                            64, s));
+    if (bricks)
+        k_emit_bricks<<<(keep + 255) / 256, 256, 0, s>>>(c->dl, k_out, v_out, keep, out_keys,
+                                                          out_ids);
+    else
+        k_emit_metas<<<(keep + 255) / 256, 256, 0, s>>>(k_out, v_out, keep, out_keys, out_ids);
+    RO_CUDA(cudaGetLastError());
     return RO_OK;
 }
 
@@ -98,23 +142,31 @@ int sort_and_emit(ro_ctx *c, unsigned long long *key_arr, const int32_t *touched
 int feedback_collect(ro_ctx *c, int64_t budget, int32_t bricks_first,
                      const ro_feedback *fb, cudaStream_t s) {
     if (budget < 0) return fail(RO_EINVAL, "negative budget");
+    const int64_t n_meta = c->meta_key ? c->n_meta : 0;
+    void *p0, *p2;
+    int rc;
+    // compacted arrays: bricks at [0, E), metas at [E, E + n_meta)
+    if ((rc = scratch(c, 0, sizeof(unsigned long long) * (c->E + n_meta), &p0))) return rc;
+    if ((rc = scratch(c, 2, sizeof(int32_t) * (c->E + n_meta), &p2))) return rc;
+    auto *ck = (unsigned long long *)p0;
+    auto *cv = (int32_t *)p2;
+    RO_CUDA(cudaMemsetAsync(c->touched_n, 0, 2 * sizeof(int32_t), s));
+    k_compact<<<scan_blocks(c->E), 256, 0, s>>>(c->brick_key, c->E, ck, cv, c->touched_n);
+    if (n_meta)
+        k_compact<<<scan_blocks(n_meta), 256, 0, s>>>(c->meta_key, n_meta, ck + c->E,
+                                                      cv + c->E, c->touched_n + 1);
+    RO_CUDA(cudaGetLastError());
     int32_t *hn = reinterpret_cast<int32_t *>(c->pinned_small);
-    RO_CUDA(cudaMemcpyAsync(hn, c->touched_n, 2 * sizeof(int32_t),
-                            cudaMemcpyDeviceToHost, s));
+    RO_CUDA(cudaMemcpyAsync(hn, c->touched_n, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     RO_CUDA(cudaStreamSynchronize(s));
     const int32_t nb = hn[0], nm = hn[1];
     const int32_t kb = (int32_t)(nb < budget ? nb : budget);
-    int64_t rest = bricks_first ? budget - kb : budget;
+    const int64_t rest = bricks_first ? budget - kb : budget;
     const int32_t km = (int32_t)(nm < rest ? nm : rest);
-    int rc = sort_and_emit(c, c->brick_key, c->brick_touched, nb, kb, true,
-                           fb->brick_keys, fb->brick_ids, s);
+    rc = sort_and_emit(c, ck, cv, nb, kb, true, fb->brick_keys, fb->brick_ids, s);
     if (rc) return rc;
-    if (nm > 0) {
-        rc = sort_and_emit(c, c->meta_key, c->meta_touched, nm, km, false,
-                           fb->meta_keys, fb->meta_ids, s);
-        if (rc) return rc;
-    }
-    RO_CUDA(cudaMemsetAsync(c->touched_n, 0, 2 * sizeof(int32_t), s));
+    rc = sort_and_emit(c, ck + c->E, cv + c->E, nm, km, false, fb->meta_keys, fb->meta_ids, s);
+    if (rc) return rc;
     fb->counts[0] = nb;
     fb->counts[1] = nm;
     fb->counts[2] = kb;

@@ -5,27 +5,57 @@
 // with the skip loop (561-635), single-sample compositing (637-694) and the
 // skip audit (595-625, 644-655, 707-723).
 //
-// B200 design:
+// B200 design (see DESIGN.md §3):
 //  * one thread per pixel, each warp an 8x4 pixel packet so neighbouring
-//    rays walk the same octree nodes / bricks (L1 hits for words, page-table
+//    rays walk the same octree nodes / bricks (L1-resident words, page-table
 //    entries and trilinear taps); 128-thread CTAs;
 //  * rays are generated in-kernel from the camera basis (bit-exact with
 //    camera.py:32-51, no 50 MB/frame ray upload);
-//  * per-channel TF tables, emptiness thresholds and page-table offsets are
-//    staged in shared memory once per CTA;
-//  * each channel is composited the moment the shared cursor resolves it
-//    (same channel order and arithmetic as the reference's two-pass form),
-//    so no per-channel outcome arrays live in local memory;
+//  * channels are unrolled at compile time (NCH = 1, 2, 4, 8 with a runtime
+//    bound) so per-channel outcomes live in registers; per sample the work
+//    is three phases -- (A) the shared-cursor traversal, one 128-bit load
+//    per visited node holding all four channel slots' words, (B) every
+//    sampled channel's eight taps issued back to back, (C) trilinear + TF +
+//    front-to-back compositing in the reference's channel order;
+//  * division-free addressing: brick sizes are powers of two, so
+//    int(p*dim/b) == int(p*dim) >> log2(b) and node coordinates at depth d
+//    are the depth-D leaf coordinates shifted right, both bit-exact;
+//    u8 -> fp64 conversions use the 2^52 bias trick on the fp64 pipe
+//    instead of the (much narrower) conversion pipe;
 //  * request recording keeps the reference's first-seen order without a
 //    serial buffer: every request event carries key = (pixel << 32 | event
 //    index within the pixel) and an atomicMin per brick / metadata entry
 //    keeps the smallest key; the first toucher appends the entry to a
 //    compact list (feedback.cu sorts it);
-//  * fp64 throughout on the decision path, compiled with -fmad=false so
-//    every operation rounds like numba's unfused code.
-#include <cub/cub.cuh>
-
+//  * fp64 on the whole decision path, compiled with -fmad=false so every
+//    operation rounds like numba's unfused code.
 #include "internal.cuh"
+
+#ifndef RO_FUSED
+#define RO_FUSED 1
+#endif
+#ifndef RO_MINB
+#define RO_MINB 4
+#endif
+#ifndef RO_NOUNROLL
+#define RO_NOUNROLL 1
+#endif
+#if RO_NOUNROLL
+#define CH_UNROLL _Pragma("unroll 1")
+#else
+#define CH_UNROLL _Pragma("unroll")
+#endif
+#ifndef RO_MEMO
+#define RO_MEMO 0
+#endif
+#ifndef RO_RARE_NOINLINE
+#define RO_RARE_NOINLINE 0
+#endif
+#if RO_RARE_NOINLINE
+#define RARE __noinline__
+#else
+#define RARE __forceinline__
+#endif
 
 namespace ro {
 
@@ -35,18 +65,28 @@ constexpr int kBlock = 128;  // 4 warps, 16x8 pixels
 constexpr int kTileW = 16;
 constexpr int kTileH = 8;
 constexpr double kClampHi = 1.0 - 1e-9;
+constexpr double kTwo52 = 4503599627370496.0;
+
+// channel outcomes; K_SAMPLE_NOMEMO = sampled through a substitute found
+// after a position-dependent probe miss (never reused by the memo)
+enum : int {
+    K_ZERO = 0, K_CONST = 1, K_SAMPLE = 2, K_MISSU = 3, K_MISSP = 4, K_SAMPLE_NOMEMO = 5,
+    K_MISS = K_MISSP
+};
+
+__device__ __forceinline__ bool is_sample(int k) { return k == K_SAMPLE || k == K_SAMPLE_NOMEMO; }
 
 struct FrameSmem {
     double tf_x[RO_MAX_CH][RO_MAX_TF_POINTS];
     double tf_rgba[RO_MAX_CH][RO_MAX_TF_POINTS][4];
     uint16_t empty_below[RO_MAX_CH][256];
-    int64_t ptoff[RO_MAX_CH][RO_MAX_LEVELS];  // pt_offsets[slot*k + lev]
-    int64_t lvl_off[RO_MAX_LEVELS];
+    int32_t ptoff[RO_MAX_CH][RO_MAX_LEVELS];  // pt_offsets[slot*k + lev]
+    int32_t lvl_off[RO_MAX_LEVELS + 1];
     double lod_thr[RO_MAX_LEVELS + 1];
     double step_tab[RO_MAX_LEVELS];
+    double dimd[RO_MAX_LEVELS][3];
     int32_t maxlev[RO_MAX_LEVELS];
     int32_t dt_tab[RO_MAX_LEVELS];
-    int32_t dims[RO_MAX_LEVELS][3];
     int32_t grids[RO_MAX_LEVELS][3];
     int32_t slot[RO_MAX_CH], lo[RO_MAX_CH], hi[RO_MAX_CH], np[RO_MAX_CH];
     unsigned long long red[RO_NUM_COUNTERS];
@@ -74,6 +114,11 @@ __device__ __forceinline__ double lerp(double a, double b, double t) {
     return a + (b - a) * t;
 }
 
+// exact non-negative int -> double on the fp64 pipe
+__device__ __forceinline__ double i2d(int v) {
+    return __hiloint2double(0x43300000, v) - kTwo52;
+}
+
 // (1-alpha)^(2^j): the reference calls libm pow with ratio = step/base_step,
 // always an exact power of two.  Repeated squaring in double-double gives
 // the correctly rounded power (glibc pow is within 0.52 ulp, so the two
@@ -93,10 +138,11 @@ __device__ __forceinline__ double pow_pow2(double x, int j) {
 
 // raw LOD level (kernels.py:43-54 before the per-channel clamp); levels
 // above 15 clamp identically for every channel (hi <= k-1 <= 15).
-__device__ __forceinline__ int lod_raw(double t, double t0, const FrameSmem &S) {
-    double ratio = t / t0;
+__device__ __forceinline__ int lod_raw(double t, double t0, double inv_t0, bool t0_pow2,
+                                       const FrameSmem &S) {
+    const double ratio = t0_pow2 ? t * inv_t0 : t / t0;  // exact when t0 = 2^k
     if (ratio < 1.0) return 0;
-    int e = ilogb(ratio);
+    const int e = ilogb(ratio);
     if (e >= RO_MAX_LEVELS - 1) return RO_MAX_LEVELS - 1;
     int lev = e;
     if (ratio >= S.lod_thr[lev + 1]) lev += 1;
@@ -108,14 +154,6 @@ __device__ __forceinline__ int clampi(int v, int lo, int hi) {
     return v < lo ? lo : (v > hi ? hi : v);
 }
 
-// kernels.py:177-184
-__device__ __forceinline__ int brick_axis(double p, int dim, int b, int grid) {
-    int c = (int)(p * (double)dim / (double)b);
-    if (c < 0) c = 0;
-    if (c > grid - 1) c = grid - 1;
-    return c;
-}
-
 // kernels.py:119-133
 __device__ __forceinline__ void tf_eval(const FrameSmem &S, int ci, double v,
                                         double &r, double &g, double &b,
@@ -124,9 +162,9 @@ __device__ __forceinline__ void tf_eval(const FrameSmem &S, int ci, double v,
     const int n = S.np[ci];
     if (v < S.tf_x[ci][0] || v > S.tf_x[ci][n - 1]) return;
     for (int i = 0; i < n - 1; ++i) {
-        double x0 = S.tf_x[ci][i], x1 = S.tf_x[ci][i + 1];
+        const double x0 = S.tf_x[ci][i], x1 = S.tf_x[ci][i + 1];
         if (x0 <= v && v <= x1) {
-            double t = (x1 == x0) ? 0.0 : (v - x0) / (x1 - x0);
+            const double t = (x1 == x0) ? 0.0 : (v - x0) / (x1 - x0);
             r = lerp(S.tf_rgba[ci][i][0], S.tf_rgba[ci][i + 1][0], t);
             g = lerp(S.tf_rgba[ci][i][1], S.tf_rgba[ci][i + 1][1], t);
             b = lerp(S.tf_rgba[ci][i][2], S.tf_rgba[ci][i + 1][2], t);
@@ -134,35 +172,6 @@ __device__ __forceinline__ void tf_eval(const FrameSmem &S, int ci, double v,
             return;
         }
     }
-}
-
-// kernels.py:136-174
-__device__ __forceinline__ double trilinear(const uint8_t *__restrict__ brick,
-                                            double lx, double ly, double lz,
-                                            int bx, int by, int bz) {
-    double fx = lx - 0.5, fy = ly - 0.5, fz = lz - 0.5;
-    if (fx < 0.0) fx = 0.0;
-    if (fy < 0.0) fy = 0.0;
-    if (fz < 0.0) fz = 0.0;
-    if (fx > bx - 1.0) fx = bx - 1.0;
-    if (fy > by - 1.0) fy = by - 1.0;
-    if (fz > bz - 1.0) fz = bz - 1.0;
-    int x0 = (int)fx, y0 = (int)fy, z0 = (int)fz;
-    int x1 = x0 + 1 < bx ? x0 + 1 : bx - 1;
-    int y1 = y0 + 1 < by ? y0 + 1 : by - 1;
-    int z1 = z0 + 1 < bz ? z0 + 1 : bz - 1;
-    double tx = fx - x0, ty = fy - y0, tz = fz - z0;
-    const int r00 = (z0 * by + y0) * bx, r10 = (z0 * by + y1) * bx;
-    const int r01 = (z1 * by + y0) * bx, r11 = (z1 * by + y1) * bx;
-    double v000 = __ldg(brick + r00 + x0), v001 = __ldg(brick + r00 + x1);
-    double v010 = __ldg(brick + r10 + x0), v011 = __ldg(brick + r10 + x1);
-    double v100 = __ldg(brick + r01 + x0), v101 = __ldg(brick + r01 + x1);
-    double v110 = __ldg(brick + r11 + x0), v111 = __ldg(brick + r11 + x1);
-    double c00 = lerp(v000, v001, tx);
-    double c10 = lerp(v010, v011, tx);
-    double c01 = lerp(v100, v101, tx);
-    double c11 = lerp(v110, v111, tx);
-    return lerp(lerp(c00, c10, ty), lerp(c01, c11, ty), tz);
 }
 
 // kernels.py:97-116
@@ -196,19 +205,131 @@ __device__ __forceinline__ void axis_box(double o, double d, double &tmin,
 
 // first-seen request: keep the minimum (pixel, event) key per entry and list
 // each touched entry once.
-__device__ __forceinline__ void request(unsigned long long *keys,
-                                        int32_t *touched, int32_t *touched_n,
-                                        int64_t entry,
-                                        unsigned long long key) {
-    unsigned long long old = atomicMin(keys + entry, key);
-    if (old == ~0ull) {
-        int pos = atomicAdd(touched_n, 1);
-        touched[pos] = (int32_t)entry;
-    }
+// Fire-and-forget (RED.MIN): the lane never waits on the L2 round trip;
+// feedback.cu finds the touched entries by scanning the key arrays.
+RARE __device__ void request(unsigned long long *keys, int32_t *, int32_t *,
+                             int32_t entry, unsigned long long key) {
+    atomicMin(keys + entry, key);
 }
 
-template <int MODE, bool CHECK>
-__global__ void __launch_bounds__(kBlock)
+// Brick coordinates of one level at the current sample position:
+// P = fl(p * dim) (kernels.py:179 numerator), c = int(P / b) = int(P) >> lb.
+struct LevelPos {
+    int lev;
+    double P[3];
+    int cb[3];
+    int local;  // (cz*gy + cy)*gx + cx
+};
+
+__device__ __forceinline__ void level_pos(LevelPos &lp, int lev, double px, double py,
+                                          double pz, const FrameSmem &S, int lbx,
+                                          int lby, int lbz) {
+    lp.lev = lev;
+    const double p3[3] = {px, py, pz};
+    const int lb3[3] = {lbx, lby, lbz};
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        lp.P[a] = p3[a] * S.dimd[lev][a];
+        int c = ((int)lp.P[a]) >> lb3[a];
+        const int g = S.grids[lev][a];
+        lp.cb[a] = c > g - 1 ? g - 1 : c;
+    }
+    lp.local = (lp.cb[2] * S.grids[lev][1] + lp.cb[1]) * S.grids[lev][0] + lp.cb[0];
+}
+
+// kernels.py:518-549: nearest resident level in the node's mask, coarser
+// first on ties; returns (level, cache slot, brick local index, clean) or
+// level -1.  clean = no earlier candidate failed its page-table probe.
+RARE __device__ int4 substitute(const int32_t *__restrict__ pt, const FrameSmem &S, int ci,
+                                int lev, int k, uint32_t mask, double px, double py,
+                                double pz, int lbx, int lby, int lbz) {
+    int clean = 1;
+    for (int delta = 1; delta < k; ++delta) {
+#pragma unroll
+        for (int sgn = 0; sgn < 2; ++sgn) {
+            const int cand = sgn == 0 ? lev + delta : lev - delta;
+            if (cand < 0 || cand >= k || !((mask >> cand) & 1u)) continue;
+            LevelPos ap;
+            level_pos(ap, cand, px, py, pz, S, lbx, lby, lbz);
+            const int pv2 = __ldg(pt + S.ptoff[ci][cand] + ap.local);
+            if (pv2 >= 0) return make_int4(cand, pv2, ap.local, clean);
+            clean = 0;
+        }
+    }
+    return make_int4(-1, -1, -1, 0);
+}
+
+// trilinear tap addresses + weights inside one brick (kernels.py:136-174)
+struct Taps {
+    int r00, r10, r01, r11;  // row offsets of (y0,z0) (y1,z0) (y0,z1) (y1,z1)
+    int x0, x1;
+    double tx, ty, tz;
+};
+
+__device__ __forceinline__ void taps_of(Taps &tp, const LevelPos &lp, int bx, int by,
+                                        int bz) {
+    const int B[3] = {bx, by, bz};
+    int i0[3], i1[3];
+    double tw[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        // lx = P - c*B exactly; fx = lx - 0.5 exactly; clamped to [0, B-1]
+        double f = (lp.P[a] - i2d(lp.cb[a] * B[a])) - 0.5;
+        if (f < 0.0) f = 0.0;
+        if (f > B[a] - 1.0) f = B[a] - 1.0;
+        const int c0 = (int)f;
+        i0[a] = c0;
+        i1[a] = c0 + 1 < B[a] ? c0 + 1 : B[a] - 1;
+        tw[a] = f - i2d(c0);
+    }
+    tp.x0 = i0[0];
+    tp.x1 = i1[0];
+    tp.r00 = (i0[2] * by + i0[1]) * bx;
+    tp.r10 = (i0[2] * by + i1[1]) * bx;
+    tp.r01 = (i1[2] * by + i0[1]) * bx;
+    tp.r11 = (i1[2] * by + i1[1]) * bx;
+    tp.tx = tw[0];
+    tp.ty = tw[1];
+    tp.tz = tw[2];
+}
+
+__device__ __forceinline__ double trilerp(const int v[8], const Taps &tp) {
+    const double c00 = lerp(i2d(v[0]), i2d(v[1]), tp.tx);
+    const double c10 = lerp(i2d(v[2]), i2d(v[3]), tp.tx);
+    const double c01 = lerp(i2d(v[4]), i2d(v[5]), tp.tx);
+    const double c11 = lerp(i2d(v[6]), i2d(v[7]), tp.tx);
+    return lerp(lerp(c00, c10, tp.ty), lerp(c01, c11, tp.ty), tp.tz);
+}
+
+__device__ __forceinline__ void load_taps(int v[8], const uint8_t *__restrict__ b,
+                                          const Taps &tp) {
+    v[0] = __ldg(b + tp.r00 + tp.x0);
+    v[1] = __ldg(b + tp.r00 + tp.x1);
+    v[2] = __ldg(b + tp.r10 + tp.x0);
+    v[3] = __ldg(b + tp.r10 + tp.x1);
+    v[4] = __ldg(b + tp.r01 + tp.x0);
+    v[5] = __ldg(b + tp.r01 + tp.x1);
+    v[6] = __ldg(b + tp.r11 + tp.x0);
+    v[7] = __ldg(b + tp.r11 + tp.x1);
+}
+
+// audit value from the fully resident reference paging (kernels.py:707-723)
+__device__ double ref_value(const ro_frame &F, const FrameSmem &S, int ci, int lev,
+                            double qx, double qy, double qz, int bx, int by, int bz,
+                            int lbx, int lby, int lbz, int bvox) {
+    LevelPos lp;
+    level_pos(lp, lev, qx, qy, qz, S, lbx, lby, lbz);
+    const int rp = F.ref_pt[S.ptoff[ci][lev] + lp.local];
+    if (rp < 0) return -1.0;
+    Taps tp;
+    taps_of(tp, lp, bx, by, bz);
+    int v[8];
+    load_taps(v, F.ref_cache + (int64_t)rp * bvox, tp);
+    return trilerp(v, tp);
+}
+
+template <int MODE, bool CHECK, int NCH>
+__global__ void __launch_bounds__(kBlock, RO_MINB)
 k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A) {
     __shared__ FrameSmem S;
     extern __shared__ int32_t dyn[];  // per-thread channel state
@@ -219,27 +340,29 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
 
     // ---- stage frame tables ----
     for (int i = tid; i < n_ch * RO_MAX_TF_POINTS; i += kBlock) {
-        int c = i / RO_MAX_TF_POINTS, p = i % RO_MAX_TF_POINTS;
+        const int c = i / RO_MAX_TF_POINTS, p = i % RO_MAX_TF_POINTS;
         S.tf_x[c][p] = F.ch[c].tf_x[p];
         for (int q = 0; q < 4; ++q) S.tf_rgba[c][p][q] = F.ch[c].tf_rgba[p][q];
     }
     for (int i = tid; i < n_ch * 256; i += kBlock)
         S.empty_below[i / 256][i % 256] = F.ch[i / 256].empty_below[i % 256];
     for (int i = tid; i < n_ch * RO_MAX_LEVELS; i += kBlock) {
-        int c = i / RO_MAX_LEVELS, l = i % RO_MAX_LEVELS;
-        S.ptoff[c][l] = l < k ? A.L.pt_off[F.ch[c].slot * k + l] : 0;
+        const int c = i / RO_MAX_LEVELS, l = i % RO_MAX_LEVELS;
+        S.ptoff[c][l] = l < k ? (int32_t)A.L.pt_off[F.ch[c].slot * k + l] : 0;
+    }
+    if (tid <= RO_MAX_LEVELS) {
+        S.lvl_off[tid] = tid <= 10 ? (int32_t)level_offset(tid) : 0;
+        S.lod_thr[tid] = F.lod_threshold[tid];
     }
     if (tid < RO_MAX_LEVELS) {
-        S.lvl_off[tid] = level_offset(tid);
         S.step_tab[tid] = F.step_tab[tid];
         S.maxlev[tid] = F.maxlev_tab[tid];
         S.dt_tab[tid] = F.dt_tab[tid];
         for (int a = 0; a < 3; ++a) {
-            S.dims[tid][a] = A.L.dims[tid][a];
+            S.dimd[tid][a] = (double)A.L.dims[tid][a];
             S.grids[tid][a] = A.L.grids[tid][a];
         }
     }
-    if (tid <= RO_MAX_LEVELS) S.lod_thr[tid] = F.lod_threshold[tid];
     if (tid < RO_MAX_CH) {
         S.slot[tid] = F.ch[tid].slot;
         S.lo[tid] = F.ch[tid].lo;
@@ -268,15 +391,21 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
     const int gy = ((ly / tr) * F.n_parts + F.part) * tr + (ly % tr);
     const bool active = x < F.width && ly < A.local_rows && gy < F.height;
 
-    unsigned long long c_steps = 0, c_eval = 0, c_skip = 0, c_viol = 0,
-                       c_live = 0;
+    unsigned long long c_steps = 0, c_eval = 0, c_skip = 0, c_viol = 0, c_live = 0;
 
-    if (active) {
+    {  // every lane runs the warp-uniform sample loop below; `active` gates work
         const int bx = A.L.bx, by = A.L.by, bz = A.L.bz;
-        const int64_t bvox = (int64_t)bx * by * bz;
+        const int lbx = __ffs(bx) - 1, lby = __ffs(by) - 1, lbz = __ffs(bz) - 1;
+        const int bvox = bx * by * bz;
         const int D = A.L.depth;
+        const double sideD = (double)(1 << D);
+        const bool vec4 = (m == 4);
+        const double t0 = F.t0;
+        const bool t0_pow2 = (__double_as_longlong(t0) & 0x000FFFFFFFFFFFFFll) == 0;
+        const double inv_t0 = 1.0 / t0;
         const int64_t pix = (int64_t)gy * F.width + x;
         const int64_t lpix = (int64_t)ly * F.width + x;
+        const unsigned long long key_hi = (unsigned long long)pix << 32;
 
         // camera.py:32-51, same operation order as the numpy code
         const double u = (((double)x + 0.5) / (double)F.width * 2.0 - 1.0) *
@@ -306,8 +435,20 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
         int stall = 0;
         uint32_t ev = 0;  // request event index within this pixel
         int32_t pixreq = 0;
+        // per-channel outcome of the last traversal (reused on a memo hit)
+        int kind[NCH], lev_of[NCH], slin[NCH], dloc[NCH], sloc[NCH];
+        // traversal memo: key (raw LOD, start depth, deepest node) + brick checks
+        int m_raw = -1, m_d0 = -1, m_endd = 0, m_ix = 0, m_iy = 0, m_iz = 0, m_steps = 0;
+        bool m_allcz = false, m_anyc = false;
+        uint32_t m_zero = 0;
 
-        while (t < tfar && accA < F.early_alpha) {
+        // Warp-uniform sample loop: lanes whose ray ended idle until the whole
+        // packet is done, and the warp reconverges once per sample instead of
+        // drifting into per-lane serial paths.
+        bool alive = active && t < tfar && accA < F.early_alpha;
+        bool dead = false;
+        while (__any_sync(0xffffffffu, alive)) {
+          if (alive) do {
             double px = ox + t * dx, py = oy + t * dy, pz = oz + t * dz;
             if (px < 0.0) px = 0.0;
             if (py < 0.0) py = 0.0;
@@ -316,162 +457,196 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
             if (py > kClampHi) py = kClampHi;
             if (pz > kClampHi) pz = kClampHi;
 
-            const int raw = lod_raw(t, F.t0, S);
+            const int raw = lod_raw(t, t0, inv_t0, t0_pow2, S);
             double step = S.step_tab[raw];
             int jexp = S.maxlev[raw];
             const int dt_ = S.dt_tab[raw];
 
-            double sR = 0.0, sG = 0.0, sB = 0.0, trans = 1.0;
-            bool any_const = false;
-            uint32_t zero_mask = 0;
+            LevelPos lp;
+            lp.lev = -1;
             bool skippable = false;
             double skip_exit = -1.0;
             int end_depth = prev_depth;
+            uint32_t zero_mask = 0;
+            bool any_const = false;
 
-            // sample one resolved channel: trilinear + usage + composite input
-            auto sample = [&](int ci, int lev, int cbx, int cby, int cbz,
-                              int slot_lin, int64_t e) {
-                const double lx = px * S.dims[lev][0] - (double)(cbx * bx);
-                const double lyy = py * S.dims[lev][1] - (double)(cby * by);
-                const double lz = pz * S.dims[lev][2] - (double)(cbz * bz);
-                const double val = trilinear(A.cache + (int64_t)slot_lin * bvox,
-                                             lx, lyy, lz, bx, by, bz);
-                int32_t &pb = prev_brick[ci * kBlock + tid];
-                if ((int32_t)e != pb) {
-                    pb = (int32_t)e;
-                    pixreq += 1;
-                    A.required[e] = 1;
-                }
-                hist_t[(ci * k + lev) * kBlock + tid] += 1;
-                double r, g, b, a;
-                tf_eval(S, ci, val, r, g, b, a);
-                sR += r * a;
-                sG += g * a;
-                sB += b * a;
-                trans *= (1.0 - a);
-            };
-
+            // ------------------ phase A: resolve every channel ------------------
             if (MODE == RO_MODE_REFERENCE) {
-                for (int ci = 0; ci < n_ch; ++ci) {
-                    const int lev = clampi(raw, S.lo[ci], S.hi[ci]);
-                    const int cbx = brick_axis(px, S.dims[lev][0], bx, S.grids[lev][0]);
-                    const int cby = brick_axis(py, S.dims[lev][1], by, S.grids[lev][1]);
-                    const int cbz = brick_axis(pz, S.dims[lev][2], bz, S.grids[lev][2]);
-                    const int64_t e = S.ptoff[ci][lev] +
-                        ((int64_t)cbz * S.grids[lev][1] + cby) * S.grids[lev][0] + cbx;
-                    const int pv = __ldg(A.pt + e);
-                    if (pv >= 0) sample(ci, lev, cbx, cby, cbz, pv, e);
+CH_UNROLL
+                for (int ci = 0; ci < NCH; ++ci) {
+                    kind[ci] = K_MISS;
+                    if (ci < n_ch) {
+                        const int lev = clampi(raw, S.lo[ci], S.hi[ci]);
+                        if (lp.lev != lev) level_pos(lp, lev, px, py, pz, S, lbx, lby, lbz);
+                        const int pv = __ldg(A.pt + S.ptoff[ci][lev] + lp.local);
+                        if (pv >= 0) { kind[ci] = K_SAMPLE; lev_of[ci] = lev; slin[ci] = pv; }
+                    }
                 }
             } else {
                 // kernels.py:431-558 -- one cursor shared by all channels
+                const int qx = (int)(px * sideD), qy = (int)(py * sideD), qz = (int)(pz * sideD);
                 int d = prev_depth - 1;
                 if (d < 0) d = 0;
                 if (F.start_level < d) d = F.start_level;
                 if (d > dt_) d = dt_;
-                int ci = 0;
+                const int d0 = d;
                 bool all_cz = true;
                 int ix = 0, iy = 0, iz = 0;
-                while (ci < n_ch) {
-                    const int side = 1 << d;
-                    ix = (int)(px * (double)side);
-                    iy = (int)(py * (double)side);
-                    iz = (int)(pz * (double)side);
-                    const int64_t nidx = S.lvl_off[d] +
-                        ((int64_t)iz * side + iy) * side + ix;
-                    c_steps += 1;
-                    const int slot = S.slot[ci];
-                    const uint32_t w = __ldg(A.words + nidx * m + slot);
-                    const int mn = (w >> 16) & 0xFF, mx = (w >> 24) & 0xFF;
-                    const uint32_t mask = w & 0xFFFF;
-                    if (mn == 255 && mx == 0) {  // INVALID: metadata request
-                        const int64_t mid = nidx * m + slot;
-                        const unsigned long long key =
-                            ((unsigned long long)pix << 32) | ev++;
-                        int32_t &lm = last_mreq[ci * kBlock + tid];
-                        if ((int32_t)mid != lm) {
-                            lm = (int32_t)mid;
-                            request(A.meta_key, A.meta_touched, A.touched_n + 1,
-                                    mid, key);
-                        }
-                    } else {
-                        if (mx < (int)S.empty_below[ci][mn]) {  // K_ZERO
-                            zero_mask |= 1u << ci;
-                            ci += 1;
-                            continue;
-                        }
-                        if ((double)(mx - mn) <= F.eps_h) {  // K_CONST
-                            double r, g, b, a;
-                            tf_eval(S, ci, (double)mn, r, g, b, a);
-                            sR += r * a;
-                            sG += g * a;
-                            sB += b * a;
-                            trans *= (1.0 - a);
-                            any_const = true;
-                            ci += 1;
-                            continue;
-                        }
-                    }
-                    const int lev = clampi(raw, S.lo[ci], S.hi[ci]);
-                    if (mask == 0) {  // K_MISSU: request the desired brick
-                        const int cbx = brick_axis(px, S.dims[lev][0], bx, S.grids[lev][0]);
-                        const int cby = brick_axis(py, S.dims[lev][1], by, S.grids[lev][1]);
-                        const int cbz = brick_axis(pz, S.dims[lev][2], bz, S.grids[lev][2]);
-                        const int64_t gb = S.ptoff[ci][lev] +
-                            ((int64_t)cbz * S.grids[lev][1] + cby) * S.grids[lev][0] + cbx;
-                        const unsigned long long key =
-                            ((unsigned long long)pix << 32) | ev++;
-                        int32_t &lb = last_breq[ci * kBlock + tid];
-                        if ((int32_t)gb != lb) {
-                            lb = (int32_t)gb;
-                            request(A.brick_key, A.brick_touched, A.touched_n, gb, key);
-                        }
-                        ci += 1;
-                        continue;
-                    }
-                    if (d < dt_) {
-                        d += 1;
-                        continue;
-                    }
-                    // at traversal depth: probe the desired brick
-                    const int cbx = brick_axis(px, S.dims[lev][0], bx, S.grids[lev][0]);
-                    const int cby = brick_axis(py, S.dims[lev][1], by, S.grids[lev][1]);
-                    const int cbz = brick_axis(pz, S.dims[lev][2], bz, S.grids[lev][2]);
-                    const int64_t e = S.ptoff[ci][lev] +
-                        ((int64_t)cbz * S.grids[lev][1] + cby) * S.grids[lev][0] + cbx;
-                    const int pv = __ldg(A.pt + e);
-                    if (pv >= 0) {
-                        sample(ci, lev, cbx, cby, cbz, pv, e);
-                    } else {
-                        const unsigned long long key =
-                            ((unsigned long long)pix << 32) | ev++;
-                        int32_t &lb = last_breq[ci * kBlock + tid];
-                        if ((int32_t)e != lb) {
-                            lb = (int32_t)e;
-                            request(A.brick_key, A.brick_touched, A.touched_n, e, key);
-                        }
-                        // nearest resident level in this node, coarser first
-                        bool found = false;
-                        for (int delta = 1; delta < k && !found; ++delta) {
-                            for (int sgn = 0; sgn < 2; ++sgn) {
-                                const int cand = sgn == 0 ? lev + delta : lev - delta;
-                                if (cand < 0 || cand >= k) continue;
-                                if (!((mask >> cand) & 1u)) continue;
-                                const int abx = brick_axis(px, S.dims[cand][0], bx, S.grids[cand][0]);
-                                const int aby = brick_axis(py, S.dims[cand][1], by, S.grids[cand][1]);
-                                const int abz = brick_axis(pz, S.dims[cand][2], bz, S.grids[cand][2]);
-                                const int64_t e2 = S.ptoff[ci][cand] +
-                                    ((int64_t)abz * S.grids[cand][1] + aby) * S.grids[cand][0] + abx;
-                                const int pv2 = __ldg(A.pt + e2);
-                                if (pv2 >= 0) {
-                                    sample(ci, cand, abx, aby, abz, pv2, e2);
-                                    found = true;
-                                    break;
-                                }
+                // Memo: the traversal is a pure function of (raw LOD -> desired
+                // levels and dt, start depth d0, the nodes on the path -- all
+                // ancestors of the deepest node -- and, for channels that reached
+                // a brick probe, the probed bricks).  If those match the previous
+                // sample, its outcome, step count and requests repeat exactly (the
+                // requests are no-ops: this pixel already holds smaller keys).
+                bool hit = false;
+                if (RO_MEMO && m_raw == raw && m_d0 == d0) {
+                    const int sh = D - m_endd;
+                    if ((qx >> sh) == m_ix && (qy >> sh) == m_iy && (qz >> sh) == m_iz) {
+                        hit = true;
+#pragma unroll 1
+                        for (int ci = 0; ci < n_ch; ++ci) {
+                            if (kind[ci] < K_SAMPLE) continue;  // ZERO / CONST: node-only
+                            if (kind[ci] == K_MISSP || kind[ci] == K_SAMPLE_NOMEMO) { hit = false; break; }
+                            const int lev = clampi(raw, S.lo[ci], S.hi[ci]);
+                            if (lp.lev != lev) level_pos(lp, lev, px, py, pz, S, lbx, lby, lbz);
+                            if (lp.local != dloc[ci]) { hit = false; break; }
+                            if (kind[ci] == K_SAMPLE && lev_of[ci] != lev) {
+                                LevelPos ap;
+                                level_pos(ap, lev_of[ci], px, py, pz, S, lbx, lby, lbz);
+                                if (ap.local != sloc[ci]) { hit = false; break; }
                             }
                         }
                     }
-                    all_cz = false;
-                    ci += 1;
+                }
+                if (hit) {
+                    c_steps += m_steps;
+                    d = m_endd;
+                    ix = m_ix;
+                    iy = m_iy;
+                    iz = m_iz;
+                    all_cz = m_allcz;
+                    zero_mask = m_zero;
+                    any_const = m_anyc;
+                } else {
+                int steps = 0;
+                int cur_node = -1;
+                uint4 wv = make_uint4(0, 0, 0, 0);
+CH_UNROLL
+                for (int ci = 0; ci < NCH; ++ci) {
+                    kind[ci] = K_MISSU;
+                    if (ci >= n_ch) continue;
+                    const int slot = S.slot[ci];
+                    while (true) {
+                        const int sh = D - d;
+                        ix = qx >> sh;
+                        iy = qy >> sh;
+                        iz = qz >> sh;
+                        const int nidx = S.lvl_off[d] + (((iz << d) + iy) << d) + ix;
+                        steps += 1;
+                        uint32_t w;
+                        if (vec4) {
+                            if (nidx != cur_node) {
+                                wv = __ldg(reinterpret_cast<const uint4 *>(A.words) + nidx);
+                                cur_node = nidx;
+                            }
+                            w = slot == 0 ? wv.x : slot == 1 ? wv.y : slot == 2 ? wv.z : wv.w;
+                        } else {
+                            w = __ldg(A.words + nidx * m + slot);
+                        }
+                        const int mn = (w >> 16) & 0xFF, mx = (w >> 24) & 0xFF;
+                        const uint32_t mask = w & 0xFFFF;
+                        if (mn == 255 && mx == 0) {  // INVALID: metadata request
+                            const int32_t mid = nidx * m + slot;
+                            const unsigned long long key = key_hi | ev++;
+                            int32_t &lm = last_mreq[ci * kBlock + tid];
+                            if (mid != lm) {
+                                lm = mid;
+                                request(A.meta_key, A.meta_touched, A.touched_n + 1, mid, key);
+                            }
+                        } else {
+                            if (mx < (int)S.empty_below[ci][mn]) {  // K_ZERO
+                                kind[ci] = K_ZERO;
+                                zero_mask |= 1u << ci;
+                                break;
+                            }
+                            if ((double)(mx - mn) <= F.eps_h) {  // K_CONST
+                                kind[ci] = K_CONST;
+                                slin[ci] = mn;
+                                any_const = true;
+                                break;
+                            }
+                        }
+                        const int lev = clampi(raw, S.lo[ci], S.hi[ci]);
+                        if (mask == 0) {  // K_MISSU: request the desired brick
+                            if (lp.lev != lev) level_pos(lp, lev, px, py, pz, S, lbx, lby, lbz);
+                            dloc[ci] = lp.local;
+                            const int32_t gb = S.ptoff[ci][lev] + lp.local;
+                            const unsigned long long key = key_hi | ev++;
+                            int32_t &lb = last_breq[ci * kBlock + tid];
+                            if (gb != lb) {
+                                lb = gb;
+                                request(A.brick_key, A.brick_touched, A.touched_n, gb, key);
+                            }
+                            break;
+                        }
+                        if (d < dt_) {
+                            d += 1;
+                            continue;
+                        }
+                        // at traversal depth: probe the desired brick
+                        all_cz = false;
+                        if (lp.lev != lev) level_pos(lp, lev, px, py, pz, S, lbx, lby, lbz);
+                        dloc[ci] = lp.local;
+                        const int32_t e = S.ptoff[ci][lev] + lp.local;
+                        const int pv = __ldg(A.pt + e);
+                        if (pv >= 0) {
+                            kind[ci] = K_SAMPLE;
+                            lev_of[ci] = lev;
+                            slin[ci] = pv;
+                            sloc[ci] = lp.local;
+                            break;
+                        }
+                        {
+                            const unsigned long long key = key_hi | ev++;
+                            int32_t &lb = last_breq[ci * kBlock + tid];
+                            if (e != lb) {
+                                lb = e;
+                                request(A.brick_key, A.brick_touched, A.touched_n, e, key);
+                            }
+                        }
+                        // nearest resident level in this node, coarser first
+                        {
+                            const int4 sub = substitute(A.pt, S, ci, lev, k, mask, px, py, pz,
+                                                        lbx, lby, lbz);
+                            // memo-safe only if no earlier candidate missed on its
+                            // (position-dependent) page-table probe
+                            if (sub.x >= 0 && sub.w) {
+                                kind[ci] = K_SAMPLE;
+                                lev_of[ci] = sub.x;
+                                slin[ci] = sub.y;
+                                sloc[ci] = sub.z;
+                            } else if (sub.x >= 0) {
+                                kind[ci] = K_SAMPLE_NOMEMO;
+                                lev_of[ci] = sub.x;
+                                slin[ci] = sub.y;
+                            } else {
+                                kind[ci] = K_MISSP;
+                            }
+                        }
+                        break;
+                    }
+                }
+                c_steps += steps;
+                m_raw = raw;
+                m_d0 = d0;
+                m_endd = d;
+                m_ix = ix;
+                m_iy = iy;
+                m_iz = iz;
+                m_steps = steps;
+                m_allcz = all_cz;
+                m_zero = zero_mask;
+                m_anyc = any_const;
                 }
                 end_depth = d;
                 if (all_cz) {
@@ -483,7 +658,21 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                 }
             }
 
-            if (skippable) {  // kernels.py:561-635
+            if (skippable) {  // kernels.py:561-635 (only ZERO / CONST / MISSU)
+                double sR = 0.0, sG = 0.0, sB = 0.0, trans = 1.0;
+                if (any_const) {
+CH_UNROLL
+                    for (int ci = 0; ci < NCH; ++ci) {
+                        if (ci < n_ch && kind[ci] == K_CONST) {
+                            double r, g, b, a;
+                            tf_eval(S, ci, (double)slin[ci], r, g, b, a);
+                            sR += r * a;
+                            sG += g * a;
+                            sB += b * a;
+                            trans *= (1.0 - a);
+                        }
+                    }
+                }
                 const double limit = skip_exit < tfar ? skip_exit : tfar;
                 const double t_before = t;
                 const double alpha = 1.0 - trans;
@@ -509,36 +698,28 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                             if (qx > kClampHi) qx = kClampHi;
                             if (qy > kClampHi) qy = kClampHi;
                             if (qz > kClampHi) qz = kClampHi;
-                            const int raw2 = lod_raw(t, F.t0, S);
+                            const int raw2 = lod_raw(t, t0, inv_t0, t0_pow2, S);
                             for (int ci = 0; ci < n_ch; ++ci) {
                                 if (!((zero_mask >> ci) & 1u)) continue;
                                 const int lev = clampi(raw2, S.lo[ci], S.hi[ci]);
-                                const int cbx = brick_axis(qx, S.dims[lev][0], bx, S.grids[lev][0]);
-                                const int cby = brick_axis(qy, S.dims[lev][1], by, S.grids[lev][1]);
-                                const int cbz = brick_axis(qz, S.dims[lev][2], bz, S.grids[lev][2]);
-                                const int64_t e = S.ptoff[ci][lev] +
-                                    ((int64_t)cbz * S.grids[lev][1] + cby) * S.grids[lev][0] + cbx;
-                                const int rp = F.ref_pt[e];
-                                if (rp < 0) continue;
-                                const double rv = trilinear(
-                                    F.ref_cache + (int64_t)rp * bvox,
-                                    qx * S.dims[lev][0] - (double)(cbx * bx),
-                                    qy * S.dims[lev][1] - (double)(cby * by),
-                                    qz * S.dims[lev][2] - (double)(cbz * bz), bx, by, bz);
-                                double r, g, b, a;
-                                tf_eval(S, ci, rv, r, g, b, a);
-                                if (a > 0.0) c_viol += 1;
+                                const double rv = ref_value(F, S, ci, lev, qx, qy, qz, bx, by,
+                                                            bz, lbx, lby, lbz, bvox);
+                                if (rv >= 0.0) {
+                                    double r, g, b, a;
+                                    tf_eval(S, ci, rv, r, g, b, a);
+                                    if (a > 0.0) c_viol += 1;
+                                }
                             }
                         }
                     }
-                    const int raw2 = lod_raw(t, F.t0, S);
+                    const int raw2 = lod_raw(t, t0, inv_t0, t0_pow2, S);
                     step = S.step_tab[raw2];
                     jexp = S.maxlev[raw2];
                     t += step;
                 }
                 prev_depth = end_depth;
                 if (t == t_before) {
-                    if (++stall > D + 2) { c_live += 1; break; }
+                    if (++stall > D + 2) { c_live += 1; dead = true; break; }
                 } else {
                     stall = 0;
                 }
@@ -546,25 +727,105 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
             }
             stall = 0;
 
+#if RO_FUSED
+            // ---- phases B+C fused per channel (compiler interleaves channels) ----
+            double sR = 0.0, sG = 0.0, sB = 0.0, trans = 1.0;
+            {
+                Taps tp;
+                int tp_lev = -1;
+CH_UNROLL
+                for (int ci = 0; ci < NCH; ++ci) {
+                    if (ci < n_ch && (is_sample(kind[ci]) || kind[ci] == K_CONST)) {
+                        double val;
+                        if (is_sample(kind[ci])) {
+                            const int lev = lev_of[ci];
+                            if (lp.lev != lev) level_pos(lp, lev, px, py, pz, S, lbx, lby, lbz);
+                            if (tp_lev != lev) { taps_of(tp, lp, bx, by, bz); tp_lev = lev; }
+                            int tv[8];
+                            load_taps(tv, A.cache + (int64_t)slin[ci] * bvox, tp);
+                            const int32_t e = S.ptoff[ci][lev] + lp.local;
+                            int32_t &pb = prev_brick[ci * kBlock + tid];
+                            if (e != pb) {
+                                pb = e;
+                                pixreq += 1;
+                                A.required[e] = 1;
+                            }
+                            hist_t[(ci * k + lev) * kBlock + tid] += 1;
+                            val = trilerp(tv, tp);
+                        } else {
+                            val = (double)slin[ci];
+                        }
+                        double r, g, b, a;
+                        tf_eval(S, ci, val, r, g, b, a);
+                        sR += r * a;
+                        sG += g * a;
+                        sB += b * a;
+                        trans *= (1.0 - a);
+                    }
+                }
+            }
+#else
+            // ------------- phase B: taps of every sampled channel -------------
+            int taps[NCH][8];
+            Taps tp;
+            int tp_lev = -1;
+            {
+CH_UNROLL
+                for (int ci = 0; ci < NCH; ++ci) {
+                    if (ci < n_ch && is_sample(kind[ci])) {
+                        const int lev = lev_of[ci];
+                        if (lp.lev != lev) level_pos(lp, lev, px, py, pz, S, lbx, lby, lbz);
+                        if (tp_lev != lev) { taps_of(tp, lp, bx, by, bz); tp_lev = lev; }
+                        load_taps(taps[ci], A.cache + (int64_t)slin[ci] * bvox, tp);
+                        const int32_t e = S.ptoff[ci][lev] + lp.local;
+                        int32_t &pb = prev_brick[ci * kBlock + tid];
+                        if (e != pb) {
+                            pb = e;
+                            pixreq += 1;
+                            A.required[e] = 1;
+                        }
+                        hist_t[(ci * k + lev) * kBlock + tid] += 1;
+                    }
+                }
+            }
+
+            // ---- phase C: trilinear + TF + composite in channel order ----
+            double sR = 0.0, sG = 0.0, sB = 0.0, trans = 1.0;
+CH_UNROLL
+            for (int ci = 0; ci < NCH; ++ci) {
+                if (ci < n_ch && (is_sample(kind[ci]) || kind[ci] == K_CONST)) {
+                    double val;
+                    if (is_sample(kind[ci])) {
+                        const int lev = lev_of[ci];
+                        if (tp_lev != lev) {  // channels sampled at different levels
+                            if (lp.lev != lev) level_pos(lp, lev, px, py, pz, S, lbx, lby, lbz);
+                            taps_of(tp, lp, bx, by, bz);
+                            tp_lev = lev;
+                        }
+                        val = trilerp(taps[ci], tp);
+                    } else {
+                        val = (double)slin[ci];
+                    }
+                    double r, g, b, a;
+                    tf_eval(S, ci, val, r, g, b, a);
+                    sR += r * a;
+                    sG += g * a;
+                    sB += b * a;
+                    trans *= (1.0 - a);
+                }
+            }
+#endif
             if (CHECK && zero_mask) {  // kernels.py:644-655
                 for (int ci = 0; ci < n_ch; ++ci) {
                     if (!((zero_mask >> ci) & 1u)) continue;
                     const int lev = clampi(raw, S.lo[ci], S.hi[ci]);
-                    const int cbx = brick_axis(px, S.dims[lev][0], bx, S.grids[lev][0]);
-                    const int cby = brick_axis(py, S.dims[lev][1], by, S.grids[lev][1]);
-                    const int cbz = brick_axis(pz, S.dims[lev][2], bz, S.grids[lev][2]);
-                    const int64_t e = S.ptoff[ci][lev] +
-                        ((int64_t)cbz * S.grids[lev][1] + cby) * S.grids[lev][0] + cbx;
-                    const int rp = F.ref_pt[e];
-                    if (rp < 0) continue;
-                    const double rv = trilinear(
-                        F.ref_cache + (int64_t)rp * bvox,
-                        px * S.dims[lev][0] - (double)(cbx * bx),
-                        py * S.dims[lev][1] - (double)(cby * by),
-                        pz * S.dims[lev][2] - (double)(cbz * bz), bx, by, bz);
-                    double r, g, b, a;
-                    tf_eval(S, ci, rv, r, g, b, a);
-                    if (a > 0.0) c_viol += 1;
+                    const double rv = ref_value(F, S, ci, lev, px, py, pz, bx, by, bz, lbx,
+                                                lby, lbz, bvox);
+                    if (rv >= 0.0) {
+                        double r, g, b, a;
+                        tf_eval(S, ci, rv, r, g, b, a);
+                        if (a > 0.0) c_viol += 1;
+                    }
                 }
             }
             const double alpha = 1.0 - trans;
@@ -580,21 +841,25 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
             c_eval += 1;
             t += step;
             prev_depth = end_depth;
+          } while (0);
+          alive = alive && !dead && t < tfar && accA < F.early_alpha;
         }
-        float4 px4 = make_float4(__double2float_rn(accR), __double2float_rn(accG),
-                                 __double2float_rn(accB), __double2float_rn(accA));
-        reinterpret_cast<float4 *>(A.image)[lpix] = px4;
-        A.pix_required[lpix] = pixreq;
+        if (active) {
+            const float4 px4 = make_float4(__double2float_rn(accR), __double2float_rn(accG),
+                                           __double2float_rn(accB), __double2float_rn(accA));
+            reinterpret_cast<float4 *>(A.image)[lpix] = px4;
+            A.pix_required[lpix] = pixreq;
+        }
     }
 
     // ---- block reductions ----
     unsigned long long vals[5] = {c_steps, c_eval, c_skip, c_viol, c_live};
 #pragma unroll
     for (int i = 0; i < 5; ++i) {
-        unsigned long long v = vals[i];
+        unsigned long long vv = vals[i];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-        if (lane == 0 && v) atomicAdd(&S.red[i], v);
+        for (int o = 16; o > 0; o >>= 1) vv += __shfl_down_sync(0xffffffffu, vv, o);
+        if (lane == 0 && vv) atomicAdd(&S.red[i], vv);
     }
     __syncthreads();
     if (tid < 5 && S.red[tid]) atomicAdd(A.counters + tid, S.red[tid]);
@@ -605,17 +870,29 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
     }
 }
 
-template <int MODE, bool CHECK>
-cudaError_t launch(const ro_frame &F, const RayArgs &A, cudaStream_t s) {
-    dim3 grid((F.width + kTileW - 1) / kTileW,
-              (A.local_rows + kTileH - 1) / kTileH);
+template <int MODE, bool CHECK, int NCH>
+cudaError_t launch_n(const ro_frame &F, const RayArgs &A, cudaStream_t s) {
+    dim3 grid((F.width + kTileW - 1) / kTileW, (A.local_rows + kTileH - 1) / kTileH);
     size_t dyn = (size_t)F.n_ch * kBlock * 4 * 3 + (size_t)F.n_ch * A.L.k * kBlock * 4;
-    auto kern = k_raycast<MODE, CHECK>;
+    auto kern = k_raycast<MODE, CHECK, NCH>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)dyn);
     if (e != cudaSuccess) return e;
     kern<<<grid, kBlock, dyn, s>>>(F, A);
     return cudaGetLastError();
+}
+
+template <int MODE, bool CHECK>
+cudaError_t launch(const ro_frame &F, const RayArgs &A, cudaStream_t s) {
+#if RO_NOUNROLL
+    // channel loops are runtime loops: one instantiation covers every n_ch
+    return launch_n<MODE, CHECK, RO_MAX_CH>(F, A, s);
+#else
+    if (F.n_ch <= 1) return launch_n<MODE, CHECK, 1>(F, A, s);
+    if (F.n_ch <= 2) return launch_n<MODE, CHECK, 2>(F, A, s);
+    if (F.n_ch <= 4) return launch_n<MODE, CHECK, 4>(F, A, s);
+    return launch_n<MODE, CHECK, 8>(F, A, s);
+#endif
 }
 
 }  // namespace
@@ -628,6 +905,8 @@ int render(ro_ctx *c, const ro_frame *F, const ro_state *st,
         return fail(RO_EINVAL, "bad partition");
     if ((int64_t)F->width * F->height >= (int64_t(1) << 31))
         return fail(RO_EINVAL, "image too large");
+    if (!(F->t0 > 0.0) || !(F->base_step > 0.0)) return fail(RO_EINVAL, "t0 / base_step must be > 0");
+    if (c->layout.depth > 10) return fail(RO_EINVAL, "ray casting supports octree depth <= 10");
     for (int i = 0; i < F->n_ch; ++i) {
         const ro_channel &ch = F->ch[i];
         if (ch.slot < 0 || ch.slot >= c->layout.m) return fail(RO_EINVAL, "channel slot out of range");
@@ -640,9 +919,12 @@ int render(ro_ctx *c, const ro_frame *F, const ro_state *st,
         return fail(RO_EINVAL, "residency mode needs octree words");
     if (F->check_skips && (F->ref_pt == nullptr || F->ref_cache == nullptr))
         return fail(RO_EINVAL, "check_skips needs reference paging");
+    if (c->bvox >= (int64_t(1) << 24)) return fail(RO_EINVAL, "brick too large");
     if (F->mode == RO_MODE_RESIDENCY) {
         int rc = ensure_meta_keys(c);
         if (rc) return rc;
+        if (c->layout.m == 4 && (reinterpret_cast<uintptr_t>(st->words) & 15))
+            return fail(RO_EINVAL, "octree words must be 16-byte aligned");
     }
     RayArgs A;
     A.L = c->dl;

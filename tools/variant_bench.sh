@@ -1,0 +1,9 @@
+#!/bin/bash
+# Bench every experiment build in paper_2309_04393_b200/_variants/ (kernel only).
+mkdir -p gpurun_out
+for lib in paper_2309_04393_b200/_variants/libresoct_*.so; do
+  name=$(basename $lib .so)
+  RESOCT_LIB=$PWD/$lib timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e \
+     > gpurun_out/var_$name.log 2>&1
+  echo "$name $(grep -o '"kernel_ms": {[^}]*}' gpurun_out/var_$name.log)" >> gpurun_out/variants.txt
+done
