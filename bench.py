@@ -150,7 +150,12 @@ def run_reference(args):
     ref = OracleState(**scenarios.reference_state(scn))
     threads = os.cpu_count() or 1
     w, h = scn.render.image_dims
-    frac = args.cpu_fraction
+    # size each step so the whole run stays within ~2-3 minutes: calibrate on
+    # a small strided sample, then aim at args.cpu_budget_s over all steps
+    cal_fps, cal_dt, cal_rows, _ = cpu_frame_rate(ref, scn, _sample_rows(h, 0.01), threads)
+    sec_per_row = cal_dt / max(cal_rows, 1)
+    per_step = args.cpu_budget_s / max(args.steps + 0.25 * args.warmup, 1)
+    frac = min(1.0, max(4.0 / h, per_step / sec_per_row / h))
     for _ in range(args.warmup):
         cpu_frame_rate(ref, scn, _sample_rows(h, frac / 4), threads)
     rates, secs, rows_total = [], 0.0, 0
@@ -355,7 +360,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--image", type=int, nargs=2, default=[1920, 1080])
-    ap.add_argument("--cpu-fraction", type=float, default=0.02)
+    ap.add_argument("--cpu-fraction", type=float, default=0.25,
+                    help="share of the frame's rows the CPU-baseline leg renders")
+    ap.add_argument("--cpu-budget-s", type=float, default=120.0,
+                    help="--impl reference: CPU seconds to spread over the timed steps")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--mode", default="residency", choices=["residency", "reference"],
