@@ -152,8 +152,9 @@ int ro_create(const ro_layout *layout, ro_ctx **out) {
     TRY(cudaMalloc(&c->brick_key, sizeof(unsigned long long) * c->E));
     TRY(cudaMemset(c->brick_key, 0xFF, sizeof(unsigned long long) * c->E));
     TRY(cudaMalloc(&c->brick_touched, sizeof(int32_t) * c->E));
-    TRY(cudaMalloc(&c->touched_n, sizeof(int32_t) * 2));
-    TRY(cudaMemset(c->touched_n, 0, sizeof(int32_t) * 2));
+    // [0..1] feedback counts, [2] ray-cast tile counter
+    TRY(cudaMalloc(&c->touched_n, sizeof(int32_t) * 4));
+    TRY(cudaMemset(c->touched_n, 0, sizeof(int32_t) * 4));
     TRY(cudaMalloc(&c->claim, sizeof(uint32_t) * c->E));
     TRY(cudaMemset(c->claim, 0, sizeof(uint32_t) * c->E));
     TRY(cudaMallocHost(&c->pinned_small, sizeof(int64_t) * 64));

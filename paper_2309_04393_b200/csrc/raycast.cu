@@ -5,18 +5,18 @@
 // with the skip loop (561-635), single-sample compositing (637-694) and the
 // skip audit (595-625, 644-655, 707-723).
 //
-// B200 design (see DESIGN.md §3):
+// B200 design (see DESIGN.md §4):
 //  * one thread per pixel, each warp an 8x4 pixel packet so neighbouring
 //    rays walk the same octree nodes / bricks (L1-resident words, page-table
 //    entries and trilinear taps); 128-thread CTAs;
+//  * warp-uniform sample loop: the packet reconverges once per sample;
 //  * rays are generated in-kernel from the camera basis (bit-exact with
 //    camera.py:32-51, no 50 MB/frame ray upload);
-//  * channels are unrolled at compile time (NCH = 1, 2, 4, 8 with a runtime
-//    bound) so per-channel outcomes live in registers; per sample the work
-//    is three phases -- (A) the shared-cursor traversal, one 128-bit load
-//    per visited node holding all four channel slots' words, (B) every
-//    sampled channel's eight taps issued back to back, (C) trilinear + TF +
-//    front-to-back compositing in the reference's channel order;
+//  * one cursor shared by all channels exactly like the reference, one
+//    128-bit load per visited node holding all four channel slots' words;
+//    each channel is sampled and composited the moment it resolves (same
+//    channel order and arithmetic as the reference's two-pass form), so no
+//    per-channel arrays spill to local memory and pollute L1;
 //  * division-free addressing: brick sizes are powers of two, so
 //    int(p*dim/b) == int(p*dim) >> log2(b) and node coordinates at depth d
 //    are the depth-D leaf coordinates shifted right, both bit-exact;
@@ -24,29 +24,23 @@
 //    instead of the (much narrower) conversion pipe;
 //  * request recording keeps the reference's first-seen order without a
 //    serial buffer: every request event carries key = (pixel << 32 | event
-//    index within the pixel) and an atomicMin per brick / metadata entry
-//    keeps the smallest key; the first toucher appends the entry to a
-//    compact list (feedback.cu sorts it);
+//    index within the pixel) and a fire-and-forget RED.MIN per brick /
+//    metadata entry keeps the smallest key (feedback.cu compacts + sorts);
 //  * fp64 on the whole decision path, compiled with -fmad=false so every
 //    operation rounds like numba's unfused code.
 #include "internal.cuh"
 
-#ifndef RO_FUSED
-#define RO_FUSED 1
-#endif
 #ifndef RO_MINB
 #define RO_MINB 4
 #endif
-#ifndef RO_NOUNROLL
-#define RO_NOUNROLL 1
+#ifndef RO_PERSISTENT
+#define RO_PERSISTENT 1
 #endif
-#if RO_NOUNROLL
-#define CH_UNROLL _Pragma("unroll 1")
-#else
-#define CH_UNROLL _Pragma("unroll")
+#ifndef RO_SUBCACHE
+#define RO_SUBCACHE 0
 #endif
-#ifndef RO_MEMO
-#define RO_MEMO 0
+#ifndef RO_DESCENT_MEMO
+#define RO_DESCENT_MEMO 0
 #endif
 #ifndef RO_RARE_NOINLINE
 #define RO_RARE_NOINLINE 0
@@ -67,18 +61,15 @@ constexpr int kTileH = 8;
 constexpr double kClampHi = 1.0 - 1e-9;
 constexpr double kTwo52 = 4503599627370496.0;
 
-// channel outcomes; K_SAMPLE_NOMEMO = sampled through a substitute found
-// after a position-dependent probe miss (never reused by the memo)
-enum : int {
-    K_ZERO = 0, K_CONST = 1, K_SAMPLE = 2, K_MISSU = 3, K_MISSP = 4, K_SAMPLE_NOMEMO = 5,
-    K_MISS = K_MISSP
-};
-
-__device__ __forceinline__ bool is_sample(int k) { return k == K_SAMPLE || k == K_SAMPLE_NOMEMO; }
-
 struct FrameSmem {
     double tf_x[RO_MAX_CH][RO_MAX_TF_POINTS];
     double tf_rgba[RO_MAX_CH][RO_MAX_TF_POINTS][4];
+    // per segment i: fl(x[i+1] - x[i]) and fl(c[i+1] - c[i]) -- the exact
+    // intermediate values of the reference's (v - x0) / (x1 - x0) and lerps
+    double tf_dx[RO_MAX_CH][RO_MAX_TF_POINTS];
+    double tf_drgba[RO_MAX_CH][RO_MAX_TF_POINTS][4];
+    // first segment i with x[i+1] >= j, for integer j (search start)
+    uint8_t tf_seg[RO_MAX_CH][256];
     uint16_t empty_below[RO_MAX_CH][256];
     int32_t ptoff[RO_MAX_CH][RO_MAX_LEVELS];  // pt_offsets[slot*k + lev]
     int32_t lvl_off[RO_MAX_LEVELS + 1];
@@ -108,6 +99,7 @@ struct RayArgs {
     int32_t *meta_touched;
     int32_t *touched_n;
     int32_t local_rows;
+    int32_t *tile_counter;   // persistent-CTA work counter (zeroed per launch)
 };
 
 __device__ __forceinline__ double lerp(double a, double b, double t) {
@@ -160,18 +152,17 @@ __device__ __forceinline__ void tf_eval(const FrameSmem &S, int ci, double v,
                                         double &a) {
     r = g = b = a = 0.0;
     const int n = S.np[ci];
-    if (v < S.tf_x[ci][0] || v > S.tf_x[ci][n - 1]) return;
-    for (int i = 0; i < n - 1; ++i) {
-        const double x0 = S.tf_x[ci][i], x1 = S.tf_x[ci][i + 1];
-        if (x0 <= v && v <= x1) {
-            const double t = (x1 == x0) ? 0.0 : (v - x0) / (x1 - x0);
-            r = lerp(S.tf_rgba[ci][i][0], S.tf_rgba[ci][i + 1][0], t);
-            g = lerp(S.tf_rgba[ci][i][1], S.tf_rgba[ci][i + 1][1], t);
-            b = lerp(S.tf_rgba[ci][i][2], S.tf_rgba[ci][i + 1][2], t);
-            a = lerp(S.tf_rgba[ci][i][3], S.tf_rgba[ci][i + 1][3], t);
-            return;
-        }
-    }
+    if (n < 2 || v < S.tf_x[ci][0] || v > S.tf_x[ci][n - 1]) return;
+    // the reference takes the first segment with x0 <= v <= x1; with strictly
+    // increasing knots that is the first i with x[i+1] >= v
+    int i = S.tf_seg[ci][(int)v];
+    while (i < n - 2 && S.tf_x[ci][i + 1] < v) ++i;
+    const double dxs = S.tf_dx[ci][i];
+    const double t = (dxs == 0.0) ? 0.0 : (v - S.tf_x[ci][i]) / dxs;
+    r = S.tf_rgba[ci][i][0] + S.tf_drgba[ci][i][0] * t;
+    g = S.tf_rgba[ci][i][1] + S.tf_drgba[ci][i][1] * t;
+    b = S.tf_rgba[ci][i][2] + S.tf_drgba[ci][i][2] * t;
+    a = S.tf_rgba[ci][i][3] + S.tf_drgba[ci][i][3] * t;
 }
 
 // kernels.py:97-116
@@ -238,25 +229,22 @@ __device__ __forceinline__ void level_pos(LevelPos &lp, int lev, double px, doub
 }
 
 // kernels.py:518-549: nearest resident level in the node's mask, coarser
-// first on ties; returns (level, cache slot, brick local index, clean) or
-// level -1.  clean = no earlier candidate failed its page-table probe.
-RARE __device__ int4 substitute(const int32_t *__restrict__ pt, const FrameSmem &S, int ci,
+// first on ties; returns (level, cache slot) or level -1.  The position of
+// the chosen level is left in `lp2` (a one-entry cache across channels).
+RARE __device__ int2 substitute(const int32_t *__restrict__ pt, const FrameSmem &S, int ci,
                                 int lev, int k, uint32_t mask, double px, double py,
-                                double pz, int lbx, int lby, int lbz) {
-    int clean = 1;
+                                double pz, int lbx, int lby, int lbz, LevelPos &lp2) {
     for (int delta = 1; delta < k; ++delta) {
 #pragma unroll
         for (int sgn = 0; sgn < 2; ++sgn) {
             const int cand = sgn == 0 ? lev + delta : lev - delta;
             if (cand < 0 || cand >= k || !((mask >> cand) & 1u)) continue;
-            LevelPos ap;
-            level_pos(ap, cand, px, py, pz, S, lbx, lby, lbz);
-            const int pv2 = __ldg(pt + S.ptoff[ci][cand] + ap.local);
-            if (pv2 >= 0) return make_int4(cand, pv2, ap.local, clean);
-            clean = 0;
+            if (lp2.lev != cand) level_pos(lp2, cand, px, py, pz, S, lbx, lby, lbz);
+            const int pv2 = __ldg(pt + S.ptoff[ci][cand] + lp2.local);
+            if (pv2 >= 0) return make_int2(cand, pv2);
         }
     }
-    return make_int4(-1, -1, -1, 0);
+    return make_int2(-1, -1);
 }
 
 // trilinear tap addresses + weights inside one brick (kernels.py:136-174)
@@ -328,7 +316,18 @@ __device__ double ref_value(const ro_frame &F, const FrameSmem &S, int ci, int l
     return trilerp(v, tp);
 }
 
-template <int MODE, bool CHECK, int NCH>
+// one sampled channel: taps + trilinear + TF; side effects on the usage
+// mask / histogram / per-pixel brick switches (kernels.py:660-681)
+struct SampleCtx {
+    LevelPos lp;   // brick coordinates of the desired level (probe)
+    Taps tp;       // tap offsets / weights of tp_lev
+    int tp_lev;
+    LevelPos lp2;  // the last substitute level (kernels.py:518-549)
+    Taps tp2;
+    int tp2_lev;
+};
+
+template <int MODE, bool CHECK>
 __global__ void __launch_bounds__(kBlock, RO_MINB)
 k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A) {
     __shared__ FrameSmem S;
@@ -344,8 +343,20 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
         S.tf_x[c][p] = F.ch[c].tf_x[p];
         for (int q = 0; q < 4; ++q) S.tf_rgba[c][p][q] = F.ch[c].tf_rgba[p][q];
     }
-    for (int i = tid; i < n_ch * 256; i += kBlock)
-        S.empty_below[i / 256][i % 256] = F.ch[i / 256].empty_below[i % 256];
+    for (int i = tid; i < n_ch * RO_MAX_TF_POINTS; i += kBlock) {
+        const int c = i / RO_MAX_TF_POINTS, p = i % RO_MAX_TF_POINTS;
+        const bool seg = p + 1 < F.ch[c].npoints;
+        S.tf_dx[c][p] = seg ? F.ch[c].tf_x[p + 1] - F.ch[c].tf_x[p] : 0.0;
+        for (int q = 0; q < 4; ++q)
+            S.tf_drgba[c][p][q] = seg ? F.ch[c].tf_rgba[p + 1][q] - F.ch[c].tf_rgba[p][q] : 0.0;
+    }
+    for (int i = tid; i < n_ch * 256; i += kBlock) {
+        const int c = i / 256, j = i % 256;
+        S.empty_below[c][j] = F.ch[c].empty_below[j];
+        int sg = 0;
+        while (sg < F.ch[c].npoints - 2 && F.ch[c].tf_x[sg + 1] < (double)j) ++sg;
+        S.tf_seg[c][j] = (uint8_t)sg;
+    }
     for (int i = tid; i < n_ch * RO_MAX_LEVELS; i += kBlock) {
         const int c = i / RO_MAX_LEVELS, l = i % RO_MAX_LEVELS;
         S.ptoff[c][l] = l < k ? (int32_t)A.L.pt_off[F.ch[c].slot * k + l] : 0;
@@ -375,80 +386,90 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
     int32_t *last_breq = prev_brick + n_ch * kBlock;  // n_ch
     int32_t *last_mreq = last_breq + n_ch * kBlock;   // n_ch
     uint32_t *hist_t = reinterpret_cast<uint32_t *>(last_mreq + n_ch * kBlock);
+    for (int i = 0; i < n_ch * k; ++i) hist_t[i * kBlock + tid] = 0;
+    const int lane = tid & 31, warp = tid >> 5;
+    const int tiles_x = (F.width + kTileW - 1) / kTileW;
+    // per-thread work counters (32-bit: a thread's share stays far below 2^32)
+    uint32_t c_steps = 0, c_eval = 0, c_skip = 0, c_viol = 0, c_live = 0;
+
+#if RO_PERSISTENT
+    // Persistent CTAs: tables are staged once per CTA, then 16x8 pixel tiles
+    // are pulled from a global counter in scanline order.
+    __shared__ int s_tile;
+    const int n_tiles = tiles_x * ((A.local_rows + kTileH - 1) / kTileH);
+    while (true) {
+    if (tid == 0) s_tile = atomicAdd(A.tile_counter, 1);
+    __syncthreads();
+    const int tile = s_tile;
+    __syncthreads();
+    if (tile >= n_tiles) break;
+#else
+    __syncthreads();  // staged tables visible to every thread
+    {
+    const int tile = blockIdx.x;
+#endif
     for (int i = 0; i < n_ch; ++i) {
         prev_brick[i * kBlock + tid] = -1;
         last_breq[i * kBlock + tid] = -1;
         last_mreq[i * kBlock + tid] = -1;
     }
-    for (int i = 0; i < n_ch * k; ++i) hist_t[i * kBlock + tid] = 0;
-    __syncthreads();
 
     // ---- pixel of this thread: warp = 8x4 packet ----
-    const int lane = tid & 31, warp = tid >> 5;
-    const int x = blockIdx.x * kTileW + (warp & 1) * 8 + (lane & 7);
-    const int ly = blockIdx.y * kTileH + (warp >> 1) * 4 + (lane >> 3);
+    const int x = (tile % tiles_x) * kTileW + (warp & 1) * 8 + (lane & 7);
+    const int ly = (tile / tiles_x) * kTileH + (warp >> 1) * 4 + (lane >> 3);
     const int tr = F.tile_rows;
     const int gy = ((ly / tr) * F.n_parts + F.part) * tr + (ly % tr);
     const bool active = x < F.width && ly < A.local_rows && gy < F.height;
 
-    unsigned long long c_steps = 0, c_eval = 0, c_skip = 0, c_viol = 0, c_live = 0;
+    const int bx = A.L.bx, by = A.L.by, bz = A.L.bz;
+    const int lbx = __ffs(bx) - 1, lby = __ffs(by) - 1, lbz = __ffs(bz) - 1;
+    const int bvox = bx * by * bz;
+    const int D = A.L.depth;
+    const double sideD = (double)(1 << D);
+    const bool vec4 = (m == 4);
+    const double t0 = F.t0;
+    const bool t0_pow2 = (__double_as_longlong(t0) & 0x000FFFFFFFFFFFFFll) == 0;
+    const double inv_t0 = 1.0 / t0;
+    // (mx - mn) <= eps_h  <=>  (mx - mn) <= floor(eps_h) for integer mx - mn
+    const int eps_i = F.eps_h >= 255.0 ? 255 : (F.eps_h < 0.0 ? -1 : (int)F.eps_h);
+    const int64_t pix = (int64_t)gy * F.width + x;
+    const int64_t lpix = (int64_t)ly * F.width + x;
+    const unsigned long long key_hi = (unsigned long long)pix << 32;
 
-    {  // every lane runs the warp-uniform sample loop below; `active` gates work
-        const int bx = A.L.bx, by = A.L.by, bz = A.L.bz;
-        const int lbx = __ffs(bx) - 1, lby = __ffs(by) - 1, lbz = __ffs(bz) - 1;
-        const int bvox = bx * by * bz;
-        const int D = A.L.depth;
-        const double sideD = (double)(1 << D);
-        const bool vec4 = (m == 4);
-        const double t0 = F.t0;
-        const bool t0_pow2 = (__double_as_longlong(t0) & 0x000FFFFFFFFFFFFFll) == 0;
-        const double inv_t0 = 1.0 / t0;
-        const int64_t pix = (int64_t)gy * F.width + x;
-        const int64_t lpix = (int64_t)ly * F.width + x;
-        const unsigned long long key_hi = (unsigned long long)pix << 32;
+    // camera.py:32-51, same operation order as the numpy code
+    const double u = (((double)x + 0.5) / (double)F.width * 2.0 - 1.0) *
+                     F.tan_half * F.aspect;
+    const double v = (1.0 - ((double)gy + 0.5) / (double)F.height * 2.0) * F.tan_half;
+    double dx = (F.cam_fwd[0] + u * F.cam_right[0]) + v * F.cam_up[0];
+    double dy = (F.cam_fwd[1] + u * F.cam_right[1]) + v * F.cam_up[1];
+    double dz = (F.cam_fwd[2] + u * F.cam_right[2]) + v * F.cam_up[2];
+    const double nrm = sqrt((dx * dx + dy * dy) + dz * dz);
+    dx = dx / nrm;
+    dy = dy / nrm;
+    dz = dz / nrm;
+    const double ox = F.cam_pos[0], oy = F.cam_pos[1], oz = F.cam_pos[2];
 
-        // camera.py:32-51, same operation order as the numpy code
-        const double u = (((double)x + 0.5) / (double)F.width * 2.0 - 1.0) *
-                         F.tan_half * F.aspect;
-        const double v = (1.0 - ((double)gy + 0.5) / (double)F.height * 2.0) *
-                         F.tan_half;
-        double dx = (F.cam_fwd[0] + u * F.cam_right[0]) + v * F.cam_up[0];
-        double dy = (F.cam_fwd[1] + u * F.cam_right[1]) + v * F.cam_up[1];
-        double dz = (F.cam_fwd[2] + u * F.cam_right[2]) + v * F.cam_up[2];
-        const double nrm = sqrt((dx * dx + dy * dy) + dz * dz);
-        dx = dx / nrm;
-        dy = dy / nrm;
-        dz = dz / nrm;
-        const double ox = F.cam_pos[0], oy = F.cam_pos[1], oz = F.cam_pos[2];
+    // kernels.py:69-94
+    double tnear = -1e30, tfar = 1e30;
+    bool miss = false;
+    axis_box(ox, dx, tnear, tfar, miss);
+    if (!miss) axis_box(oy, dy, tnear, tfar, miss);
+    if (!miss) axis_box(oz, dz, tnear, tfar, miss);
+    if (miss) { tnear = 1.0; tfar = -1.0; }
 
-        // kernels.py:69-94
-        double tnear = -1e30, tfar = 1e30;
-        bool miss = false;
-        axis_box(ox, dx, tnear, tfar, miss);
-        if (!miss) axis_box(oy, dy, tnear, tfar, miss);
-        if (!miss) axis_box(oz, dz, tnear, tfar, miss);
-        if (miss) { tnear = 1.0; tfar = -1.0; }
+    double accR = 0.0, accG = 0.0, accB = 0.0, accA = 0.0;
+    double t = tnear > 0.0 ? tnear : 0.0;
+    int prev_depth = F.start_level;
+    int stall = 0;
+    uint32_t ev = 0;  // request event index within this pixel
+    int32_t pixreq = 0;
+    int m_key = -1, m_node = -1;  // descent memo (see the traversal)
 
-        double accR = 0.0, accG = 0.0, accB = 0.0, accA = 0.0;
-        double t = tnear > 0.0 ? tnear : 0.0;
-        int prev_depth = F.start_level;
-        int stall = 0;
-        uint32_t ev = 0;  // request event index within this pixel
-        int32_t pixreq = 0;
-        // per-channel outcome of the last traversal (reused on a memo hit)
-        int kind[NCH], lev_of[NCH], slin[NCH], dloc[NCH], sloc[NCH];
-        // traversal memo: key (raw LOD, start depth, deepest node) + brick checks
-        int m_raw = -1, m_d0 = -1, m_endd = 0, m_ix = 0, m_iy = 0, m_iz = 0, m_steps = 0;
-        bool m_allcz = false, m_anyc = false;
-        uint32_t m_zero = 0;
-
-        // Warp-uniform sample loop: lanes whose ray ended idle until the whole
-        // packet is done, and the warp reconverges once per sample instead of
-        // drifting into per-lane serial paths.
-        bool alive = active && t < tfar && accA < F.early_alpha;
-        bool dead = false;
-        while (__any_sync(0xffffffffu, alive)) {
-          if (alive) do {
+    // Warp-uniform sample loop: lanes whose ray ended idle until the whole
+    // packet is done, so the warp reconverges once per sample.
+    bool alive = active && t < tfar && accA < F.early_alpha;
+    while (__any_sync(0xffffffffu, alive)) {
+        if (alive) {
             double px = ox + t * dx, py = oy + t * dy, pz = oz + t * dz;
             if (px < 0.0) px = 0.0;
             if (py < 0.0) py = 0.0;
@@ -462,25 +483,63 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
             int jexp = S.maxlev[raw];
             const int dt_ = S.dt_tab[raw];
 
-            LevelPos lp;
-            lp.lev = -1;
+            SampleCtx sc;
+            sc.lp.lev = -1;
+            sc.tp_lev = -1;
+            sc.lp2.lev = -1;
+            sc.tp2_lev = -1;
+            // channel contributions, accumulated in the reference's channel
+            // order the moment each channel resolves (kernels.py:637-681)
+            double sR = 0.0, sG = 0.0, sB = 0.0, trans = 1.0;
+            bool any_const = false;
+            uint32_t zero_mask = 0;
             bool skippable = false;
             double skip_exit = -1.0;
             int end_depth = prev_depth;
-            uint32_t zero_mask = 0;
-            bool any_const = false;
 
-            // ------------------ phase A: resolve every channel ------------------
-            if (MODE == RO_MODE_REFERENCE) {
-CH_UNROLL
-                for (int ci = 0; ci < NCH; ++ci) {
-                    kind[ci] = K_MISS;
-                    if (ci < n_ch) {
-                        const int lev = clampi(raw, S.lo[ci], S.hi[ci]);
-                        if (lp.lev != lev) level_pos(lp, lev, px, py, pz, S, lbx, lby, lbz);
-                        const int pv = __ldg(A.pt + S.ptoff[ci][lev] + lp.local);
-                        if (pv >= 0) { kind[ci] = K_SAMPLE; lev_of[ci] = lev; slin[ci] = pv; }
-                    }
+            auto finish = [&](int ci, int lev, int slot_lin, const LevelPos &lp, const Taps &tp) {
+                int tv[8];
+                load_taps(tv, A.cache + (int64_t)slot_lin * bvox, tp);
+                const int32_t e = S.ptoff[ci][lev] + lp.local;
+                int32_t &pb = prev_brick[ci * kBlock + tid];
+                if (e != pb) {
+                    pb = e;
+                    pixreq += 1;
+                    A.required[e] = 1;
+                }
+                hist_t[(ci * k + lev) * kBlock + tid] += 1;
+                const double val = trilerp(tv, tp);
+                double r, g, b, a;
+                tf_eval(S, ci, val, r, g, b, a);
+                sR += r * a;
+                sG += g * a;
+                sB += b * a;
+                trans *= (1.0 - a);
+            };
+            // sample at the desired level (sc.lp already holds it)
+            auto sample = [&](int ci, int lev, int slot_lin) {
+                if (sc.tp_lev != lev) { taps_of(sc.tp, sc.lp, bx, by, bz); sc.tp_lev = lev; }
+                finish(ci, lev, slot_lin, sc.lp, sc.tp);
+            };
+            // sample at a substitute level (sc.lp2 holds it)
+            auto sample2 = [&](int ci, int lev, int slot_lin) {
+#if RO_SUBCACHE
+                if (sc.tp2_lev != lev) { taps_of(sc.tp2, sc.lp2, bx, by, bz); sc.tp2_lev = lev; }
+                finish(ci, lev, slot_lin, sc.lp2, sc.tp2);
+#else
+                Taps t2;
+                taps_of(t2, sc.lp2, bx, by, bz);
+                finish(ci, lev, slot_lin, sc.lp2, t2);
+#endif
+            };
+
+            if (MODE == RO_MODE_REFERENCE) {  // kernels.py:301-314
+#pragma unroll 1
+                for (int ci = 0; ci < n_ch; ++ci) {
+                    const int lev = clampi(raw, S.lo[ci], S.hi[ci]);
+                    if (sc.lp.lev != lev) level_pos(sc.lp, lev, px, py, pz, S, lbx, lby, lbz);
+                    const int pv = __ldg(A.pt + S.ptoff[ci][lev] + sc.lp.local);
+                    if (pv >= 0) sample(ci, lev, pv);
                 }
             } else {
                 // kernels.py:431-558 -- one cursor shared by all channels
@@ -489,52 +548,25 @@ CH_UNROLL
                 if (d < 0) d = 0;
                 if (F.start_level < d) d = F.start_level;
                 if (d > dt_) d = dt_;
-                const int d0 = d;
                 bool all_cz = true;
                 int ix = 0, iy = 0, iz = 0;
-                // Memo: the traversal is a pure function of (raw LOD -> desired
-                // levels and dt, start depth d0, the nodes on the path -- all
-                // ancestors of the deepest node -- and, for channels that reached
-                // a brick probe, the probed bricks).  If those match the previous
-                // sample, its outcome, step count and requests repeat exactly (the
-                // requests are no-ops: this pixel already holds smaller keys).
-                bool hit = false;
-                if (RO_MEMO && m_raw == raw && m_d0 == d0) {
-                    const int sh = D - m_endd;
-                    if ((qx >> sh) == m_ix && (qy >> sh) == m_iy && (qz >> sh) == m_iz) {
-                        hit = true;
-#pragma unroll 1
-                        for (int ci = 0; ci < n_ch; ++ci) {
-                            if (kind[ci] < K_SAMPLE) continue;  // ZERO / CONST: node-only
-                            if (kind[ci] == K_MISSP || kind[ci] == K_SAMPLE_NOMEMO) { hit = false; break; }
-                            const int lev = clampi(raw, S.lo[ci], S.hi[ci]);
-                            if (lp.lev != lev) level_pos(lp, lev, px, py, pz, S, lbx, lby, lbz);
-                            if (lp.local != dloc[ci]) { hit = false; break; }
-                            if (kind[ci] == K_SAMPLE && lev_of[ci] != lev) {
-                                LevelPos ap;
-                                level_pos(ap, lev_of[ci], px, py, pz, S, lbx, lby, lbz);
-                                if (ap.local != sloc[ci]) { hit = false; break; }
-                            }
-                        }
-                    }
-                }
-                if (hit) {
-                    c_steps += m_steps;
-                    d = m_endd;
-                    ix = m_ix;
-                    iy = m_iy;
-                    iz = m_iz;
-                    all_cz = m_allcz;
-                    zero_mask = m_zero;
-                    any_const = m_anyc;
-                } else {
-                int steps = 0;
                 int cur_node = -1;
                 uint4 wv = make_uint4(0, 0, 0, 0);
-CH_UNROLL
-                for (int ci = 0; ci < NCH; ++ci) {
-                    kind[ci] = K_MISSU;
-                    if (ci >= n_ch) continue;
+                const int d0 = d;
+                // Descent memo: channel 0's walk from d0 through the ancestors of
+                // the depth-dt node depends only on (raw LOD, d0, that node) --
+                // if the previous sample descended through the same ancestors
+                // without resolving, so does this one: count the steps, start at
+                // dt.  (Requests it would repeat are no-ops: smaller keys exist.)
+                const int sh_dt = D - dt_;
+                const int node_dt = S.lvl_off[dt_] +
+                    ((((qz >> sh_dt) << dt_) + (qy >> sh_dt)) << dt_) + (qx >> sh_dt);
+                if (RO_DESCENT_MEMO && d0 < dt_ && m_key == raw * 32 + d0 && m_node == node_dt) {
+                    c_steps += dt_ - d0;
+                    d = dt_;
+                }
+#pragma unroll 1
+                for (int ci = 0; ci < n_ch; ++ci) {
                     const int slot = S.slot[ci];
                     while (true) {
                         const int sh = D - d;
@@ -542,7 +574,7 @@ CH_UNROLL
                         iy = qy >> sh;
                         iz = qz >> sh;
                         const int nidx = S.lvl_off[d] + (((iz << d) + iy) << d) + ix;
-                        steps += 1;
+                        c_steps += 1;
                         uint32_t w;
                         if (vec4) {
                             if (nidx != cur_node) {
@@ -561,31 +593,34 @@ CH_UNROLL
                             int32_t &lm = last_mreq[ci * kBlock + tid];
                             if (mid != lm) {
                                 lm = mid;
-                                request(A.meta_key, A.meta_touched, A.touched_n + 1, mid, key);
+                                request(A.meta_key, nullptr, nullptr, mid, key);
                             }
                         } else {
                             if (mx < (int)S.empty_below[ci][mn]) {  // K_ZERO
-                                kind[ci] = K_ZERO;
                                 zero_mask |= 1u << ci;
                                 break;
                             }
-                            if ((double)(mx - mn) <= F.eps_h) {  // K_CONST
-                                kind[ci] = K_CONST;
-                                slin[ci] = mn;
+                            if (mx - mn <= eps_i) {  // K_CONST
+                                double r, g, b, a;
+                                tf_eval(S, ci, (double)mn, r, g, b, a);
+                                sR += r * a;
+                                sG += g * a;
+                                sB += b * a;
+                                trans *= (1.0 - a);
                                 any_const = true;
                                 break;
                             }
                         }
                         const int lev = clampi(raw, S.lo[ci], S.hi[ci]);
                         if (mask == 0) {  // K_MISSU: request the desired brick
-                            if (lp.lev != lev) level_pos(lp, lev, px, py, pz, S, lbx, lby, lbz);
-                            dloc[ci] = lp.local;
-                            const int32_t gb = S.ptoff[ci][lev] + lp.local;
+                            if (sc.lp.lev != lev)
+                                level_pos(sc.lp, lev, px, py, pz, S, lbx, lby, lbz);
+                            const int32_t gb = S.ptoff[ci][lev] + sc.lp.local;
                             const unsigned long long key = key_hi | ev++;
                             int32_t &lb = last_breq[ci * kBlock + tid];
                             if (gb != lb) {
                                 lb = gb;
-                                request(A.brick_key, A.brick_touched, A.touched_n, gb, key);
+                                request(A.brick_key, nullptr, nullptr, gb, key);
                             }
                             break;
                         }
@@ -595,15 +630,11 @@ CH_UNROLL
                         }
                         // at traversal depth: probe the desired brick
                         all_cz = false;
-                        if (lp.lev != lev) level_pos(lp, lev, px, py, pz, S, lbx, lby, lbz);
-                        dloc[ci] = lp.local;
-                        const int32_t e = S.ptoff[ci][lev] + lp.local;
+                        if (sc.lp.lev != lev) level_pos(sc.lp, lev, px, py, pz, S, lbx, lby, lbz);
+                        const int32_t e = S.ptoff[ci][lev] + sc.lp.local;
                         const int pv = __ldg(A.pt + e);
                         if (pv >= 0) {
-                            kind[ci] = K_SAMPLE;
-                            lev_of[ci] = lev;
-                            slin[ci] = pv;
-                            sloc[ci] = lp.local;
+                            sample(ci, lev, pv);
                             break;
                         }
                         {
@@ -611,68 +642,30 @@ CH_UNROLL
                             int32_t &lb = last_breq[ci * kBlock + tid];
                             if (e != lb) {
                                 lb = e;
-                                request(A.brick_key, A.brick_touched, A.touched_n, e, key);
+                                request(A.brick_key, nullptr, nullptr, e, key);
                             }
                         }
                         // nearest resident level in this node, coarser first
-                        {
-                            const int4 sub = substitute(A.pt, S, ci, lev, k, mask, px, py, pz,
-                                                        lbx, lby, lbz);
-                            // memo-safe only if no earlier candidate missed on its
-                            // (position-dependent) page-table probe
-                            if (sub.x >= 0 && sub.w) {
-                                kind[ci] = K_SAMPLE;
-                                lev_of[ci] = sub.x;
-                                slin[ci] = sub.y;
-                                sloc[ci] = sub.z;
-                            } else if (sub.x >= 0) {
-                                kind[ci] = K_SAMPLE_NOMEMO;
-                                lev_of[ci] = sub.x;
-                                slin[ci] = sub.y;
-                            } else {
-                                kind[ci] = K_MISSP;
-                            }
-                        }
+                        const int2 sub = substitute(A.pt, S, ci, lev, k, mask, px, py, pz,
+                                                    lbx, lby, lbz, sc.lp2);
+                        if (sub.x >= 0) sample2(ci, sub.x, sub.y);
                         break;
                     }
-                }
-                c_steps += steps;
-                m_raw = raw;
-                m_d0 = d0;
-                m_endd = d;
-                m_ix = ix;
-                m_iy = iy;
-                m_iz = iz;
-                m_steps = steps;
-                m_allcz = all_cz;
-                m_zero = zero_mask;
-                m_anyc = any_const;
+                    if (ci == 0) {  // channel 0 done: remember a clean descent
+                        m_key = (d == dt_ && d0 < dt_) ? raw * 32 + d0 : -1;
+                        m_node = node_dt;
+                    }
                 }
                 end_depth = d;
                 if (all_cz) {
                     skippable = true;
                     const double s = 1.0 / (double)(1 << d);
-                    skip_exit = box_exit(ox, oy, oz, dx, dy, dz, ix * s, iy * s,
-                                         iz * s, (ix + 1) * s, (iy + 1) * s,
-                                         (iz + 1) * s);
+                    skip_exit = box_exit(ox, oy, oz, dx, dy, dz, ix * s, iy * s, iz * s,
+                                         (ix + 1) * s, (iy + 1) * s, (iz + 1) * s);
                 }
             }
 
             if (skippable) {  // kernels.py:561-635 (only ZERO / CONST / MISSU)
-                double sR = 0.0, sG = 0.0, sB = 0.0, trans = 1.0;
-                if (any_const) {
-CH_UNROLL
-                    for (int ci = 0; ci < NCH; ++ci) {
-                        if (ci < n_ch && kind[ci] == K_CONST) {
-                            double r, g, b, a;
-                            tf_eval(S, ci, (double)slin[ci], r, g, b, a);
-                            sR += r * a;
-                            sG += g * a;
-                            sB += b * a;
-                            trans *= (1.0 - a);
-                        }
-                    }
-                }
                 const double limit = skip_exit < tfar ? skip_exit : tfar;
                 const double t_before = t;
                 const double alpha = 1.0 - trans;
@@ -719,138 +712,52 @@ CH_UNROLL
                 }
                 prev_depth = end_depth;
                 if (t == t_before) {
-                    if (++stall > D + 2) { c_live += 1; dead = true; break; }
+                    if (++stall > D + 2) {  // proven cycle: the reference never returns
+                        c_live += 1;
+                        alive = false;
+                    }
                 } else {
                     stall = 0;
                 }
-                continue;
-            }
-            stall = 0;
-
-#if RO_FUSED
-            // ---- phases B+C fused per channel (compiler interleaves channels) ----
-            double sR = 0.0, sG = 0.0, sB = 0.0, trans = 1.0;
-            {
-                Taps tp;
-                int tp_lev = -1;
-CH_UNROLL
-                for (int ci = 0; ci < NCH; ++ci) {
-                    if (ci < n_ch && (is_sample(kind[ci]) || kind[ci] == K_CONST)) {
-                        double val;
-                        if (is_sample(kind[ci])) {
-                            const int lev = lev_of[ci];
-                            if (lp.lev != lev) level_pos(lp, lev, px, py, pz, S, lbx, lby, lbz);
-                            if (tp_lev != lev) { taps_of(tp, lp, bx, by, bz); tp_lev = lev; }
-                            int tv[8];
-                            load_taps(tv, A.cache + (int64_t)slin[ci] * bvox, tp);
-                            const int32_t e = S.ptoff[ci][lev] + lp.local;
-                            int32_t &pb = prev_brick[ci * kBlock + tid];
-                            if (e != pb) {
-                                pb = e;
-                                pixreq += 1;
-                                A.required[e] = 1;
-                            }
-                            hist_t[(ci * k + lev) * kBlock + tid] += 1;
-                            val = trilerp(tv, tp);
-                        } else {
-                            val = (double)slin[ci];
+            } else {
+                stall = 0;
+                if (CHECK && zero_mask) {  // kernels.py:644-655
+                    for (int ci = 0; ci < n_ch; ++ci) {
+                        if (!((zero_mask >> ci) & 1u)) continue;
+                        const int lev = clampi(raw, S.lo[ci], S.hi[ci]);
+                        const double rv = ref_value(F, S, ci, lev, px, py, pz, bx, by, bz, lbx,
+                                                    lby, lbz, bvox);
+                        if (rv >= 0.0) {
+                            double r, g, b, a;
+                            tf_eval(S, ci, rv, r, g, b, a);
+                            if (a > 0.0) c_viol += 1;
                         }
-                        double r, g, b, a;
-                        tf_eval(S, ci, val, r, g, b, a);
-                        sR += r * a;
-                        sG += g * a;
-                        sB += b * a;
-                        trans *= (1.0 - a);
                     }
                 }
-            }
-#else
-            // ------------- phase B: taps of every sampled channel -------------
-            int taps[NCH][8];
-            Taps tp;
-            int tp_lev = -1;
-            {
-CH_UNROLL
-                for (int ci = 0; ci < NCH; ++ci) {
-                    if (ci < n_ch && is_sample(kind[ci])) {
-                        const int lev = lev_of[ci];
-                        if (lp.lev != lev) level_pos(lp, lev, px, py, pz, S, lbx, lby, lbz);
-                        if (tp_lev != lev) { taps_of(tp, lp, bx, by, bz); tp_lev = lev; }
-                        load_taps(taps[ci], A.cache + (int64_t)slin[ci] * bvox, tp);
-                        const int32_t e = S.ptoff[ci][lev] + lp.local;
-                        int32_t &pb = prev_brick[ci * kBlock + tid];
-                        if (e != pb) {
-                            pb = e;
-                            pixreq += 1;
-                            A.required[e] = 1;
-                        }
-                        hist_t[(ci * k + lev) * kBlock + tid] += 1;
-                    }
+                const double alpha = 1.0 - trans;
+                if (alpha > 0.0) {
+                    const double corr = 1.0 - pow_pow2(1.0 - alpha, jexp);
+                    const double scale = corr / alpha;
+                    const double wgt = 1.0 - accA;
+                    accR += wgt * sR * scale;
+                    accG += wgt * sG * scale;
+                    accB += wgt * sB * scale;
+                    accA += wgt * corr;
                 }
+                c_eval += 1;
+                t += step;
+                prev_depth = end_depth;
             }
-
-            // ---- phase C: trilinear + TF + composite in channel order ----
-            double sR = 0.0, sG = 0.0, sB = 0.0, trans = 1.0;
-CH_UNROLL
-            for (int ci = 0; ci < NCH; ++ci) {
-                if (ci < n_ch && (is_sample(kind[ci]) || kind[ci] == K_CONST)) {
-                    double val;
-                    if (is_sample(kind[ci])) {
-                        const int lev = lev_of[ci];
-                        if (tp_lev != lev) {  // channels sampled at different levels
-                            if (lp.lev != lev) level_pos(lp, lev, px, py, pz, S, lbx, lby, lbz);
-                            taps_of(tp, lp, bx, by, bz);
-                            tp_lev = lev;
-                        }
-                        val = trilerp(taps[ci], tp);
-                    } else {
-                        val = (double)slin[ci];
-                    }
-                    double r, g, b, a;
-                    tf_eval(S, ci, val, r, g, b, a);
-                    sR += r * a;
-                    sG += g * a;
-                    sB += b * a;
-                    trans *= (1.0 - a);
-                }
-            }
-#endif
-            if (CHECK && zero_mask) {  // kernels.py:644-655
-                for (int ci = 0; ci < n_ch; ++ci) {
-                    if (!((zero_mask >> ci) & 1u)) continue;
-                    const int lev = clampi(raw, S.lo[ci], S.hi[ci]);
-                    const double rv = ref_value(F, S, ci, lev, px, py, pz, bx, by, bz, lbx,
-                                                lby, lbz, bvox);
-                    if (rv >= 0.0) {
-                        double r, g, b, a;
-                        tf_eval(S, ci, rv, r, g, b, a);
-                        if (a > 0.0) c_viol += 1;
-                    }
-                }
-            }
-            const double alpha = 1.0 - trans;
-            if (alpha > 0.0) {
-                const double corr = 1.0 - pow_pow2(1.0 - alpha, jexp);
-                const double scale = corr / alpha;
-                const double wgt = 1.0 - accA;
-                accR += wgt * sR * scale;
-                accG += wgt * sG * scale;
-                accB += wgt * sB * scale;
-                accA += wgt * corr;
-            }
-            c_eval += 1;
-            t += step;
-            prev_depth = end_depth;
-          } while (0);
-          alive = alive && !dead && t < tfar && accA < F.early_alpha;
-        }
-        if (active) {
-            const float4 px4 = make_float4(__double2float_rn(accR), __double2float_rn(accG),
-                                           __double2float_rn(accB), __double2float_rn(accA));
-            reinterpret_cast<float4 *>(A.image)[lpix] = px4;
-            A.pix_required[lpix] = pixreq;
+            alive = alive && t < tfar && accA < F.early_alpha;
         }
     }
+    if (active) {
+        const float4 px4 = make_float4(__double2float_rn(accR), __double2float_rn(accG),
+                                       __double2float_rn(accB), __double2float_rn(accA));
+        reinterpret_cast<float4 *>(A.image)[lpix] = px4;
+        A.pix_required[lpix] = pixreq;
+    }
+    }  // tile loop
 
     // ---- block reductions ----
     unsigned long long vals[5] = {c_steps, c_eval, c_skip, c_viol, c_live};
@@ -870,29 +777,32 @@ CH_UNROLL
     }
 }
 
-template <int MODE, bool CHECK, int NCH>
-cudaError_t launch_n(const ro_frame &F, const RayArgs &A, cudaStream_t s) {
-    dim3 grid((F.width + kTileW - 1) / kTileW, (A.local_rows + kTileH - 1) / kTileH);
+template <int MODE, bool CHECK>
+cudaError_t launch(const ro_frame &F, const RayArgs &A, cudaStream_t s) {
+    int n_tiles = ((F.width + kTileW - 1) / kTileW) * ((A.local_rows + kTileH - 1) / kTileH);
+    static int sm_count = 0;
+    if (sm_count == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev);
+    }
     size_t dyn = (size_t)F.n_ch * kBlock * 4 * 3 + (size_t)F.n_ch * A.L.k * kBlock * 4;
-    auto kern = k_raycast<MODE, CHECK, NCH>;
+    auto kern = k_raycast<MODE, CHECK>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)dyn);
     if (e != cudaSuccess) return e;
-    kern<<<grid, kBlock, dyn, s>>>(F, A);
-    return cudaGetLastError();
-}
-
-template <int MODE, bool CHECK>
-cudaError_t launch(const ro_frame &F, const RayArgs &A, cudaStream_t s) {
-#if RO_NOUNROLL
-    // channel loops are runtime loops: one instantiation covers every n_ch
-    return launch_n<MODE, CHECK, RO_MAX_CH>(F, A, s);
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlock, dyn);
+    if (e != cudaSuccess) return e;
+#if RO_PERSISTENT
+    int blocks = per_sm * sm_count;
+    if (blocks > n_tiles) blocks = n_tiles;
+    if (blocks < 1) blocks = 1;
 #else
-    if (F.n_ch <= 1) return launch_n<MODE, CHECK, 1>(F, A, s);
-    if (F.n_ch <= 2) return launch_n<MODE, CHECK, 2>(F, A, s);
-    if (F.n_ch <= 4) return launch_n<MODE, CHECK, 4>(F, A, s);
-    return launch_n<MODE, CHECK, 8>(F, A, s);
+    int blocks = n_tiles;
 #endif
+    kern<<<blocks, kBlock, dyn, s>>>(F, A);
+    return cudaGetLastError();
 }
 
 }  // namespace
@@ -941,11 +851,13 @@ int render(ro_ctx *c, const ro_frame *F, const ro_state *st,
     A.brick_touched = c->brick_touched;
     A.meta_touched = c->meta_touched;
     A.touched_n = c->touched_n;
+    A.tile_counter = c->touched_n + 2;
     A.local_rows = (int32_t)ro_local_rows(F->height, F->n_parts, F->part, F->tile_rows);
     RO_CUDA(cudaMemsetAsync(out->required, 0, (size_t)c->E, s));
     RO_CUDA(cudaMemsetAsync(out->hist, 0, sizeof(int64_t) * F->n_ch * c->layout.k, s));
     RO_CUDA(cudaMemsetAsync(out->counters, 0, sizeof(int64_t) * RO_NUM_COUNTERS, s));
     if (A.local_rows == 0) return RO_OK;
+    RO_CUDA(cudaMemsetAsync(A.tile_counter, 0, sizeof(int32_t), s));
     cudaError_t e;
     if (F->mode == RO_MODE_REFERENCE) {
         e = launch<RO_MODE_REFERENCE, false>(*F, A, s);
