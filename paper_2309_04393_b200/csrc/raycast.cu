@@ -80,6 +80,8 @@ struct FrameSmem {
     int32_t dt_tab[RO_MAX_LEVELS];
     int32_t grids[RO_MAX_LEVELS][3];
     int32_t slot[RO_MAX_CH], lo[RO_MAX_CH], hi[RO_MAX_CH], np[RO_MAX_CH];
+    // largest integer value v with opacity(u) == 0 for every u <= v
+    int32_t zero_upto[RO_MAX_CH];
     unsigned long long red[RO_NUM_COUNTERS];
 };
 
@@ -379,6 +381,16 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
         S.lo[tid] = F.ch[tid].lo;
         S.hi[tid] = F.ch[tid].hi;
         S.np[tid] = F.ch[tid].npoints;
+        // leading zero-opacity range of the piecewise-linear TF (kernels.py:119-133):
+        // below x[0] the TF is transparent; a segment whose two knots have alpha 0
+        // evaluates to 0 + (0 - 0) * t = 0 exactly
+        const ro_channel &c = F.ch[tid];
+        int z = 255;
+        for (int i = 0; i + 1 < c.npoints; ++i) {
+            if (c.tf_rgba[i][3] > 0.0) { z = (int)ceil(c.tf_x[i]) - 1; break; }
+            if (c.tf_rgba[i + 1][3] > 0.0) { z = (int)floor(c.tf_x[i]); break; }
+        }
+        S.zero_upto[tid] = z;  // (a single-knot TF evaluates to 0 everywhere)
     }
     if (tid < RO_NUM_COUNTERS) S.red[tid] = 0;
     // per-thread arrays: [ci*kBlock + tid]
@@ -508,6 +520,13 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                     A.required[e] = 1;
                 }
                 hist_t[(ci * k + lev) * kBlock + tid] += 1;
+                // The trilinear value never exceeds the largest tap (every lerp
+                // is a rounded convex combination).  If that tap lies in the
+                // TF's leading zero-opacity range, r*a, g*a, b*a are +0 and
+                // (1 - a) is 1: the channel adds exactly nothing -- skip it.
+                const int mt = max(max(max(tv[0], tv[1]), max(tv[2], tv[3])),
+                                   max(max(tv[4], tv[5]), max(tv[6], tv[7])));
+                if (mt <= S.zero_upto[ci]) return;
                 const double val = trilerp(tv, tp);
                 double r, g, b, a;
                 tf_eval(S, ci, val, r, g, b, a);
