@@ -39,8 +39,8 @@
 #ifndef RO_SUBCACHE
 #define RO_SUBCACHE 0
 #endif
-#ifndef RO_DESCENT_MEMO
-#define RO_DESCENT_MEMO 0
+#ifndef RO_FAST_DESCENT
+#define RO_FAST_DESCENT 1
 #endif
 #ifndef RO_RARE_NOINLINE
 #define RO_RARE_NOINLINE 0
@@ -58,6 +58,7 @@ namespace {
 constexpr int kBlock = 128;  // 4 warps, 16x8 pixels
 constexpr int kTileW = 16;
 constexpr int kTileH = 8;
+constexpr int kFastDepth = 6;  // longest channel-0 descent handled in parallel
 constexpr double kClampHi = 1.0 - 1e-9;
 constexpr double kTwo52 = 4503599627370496.0;
 
@@ -475,7 +476,6 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
     int stall = 0;
     uint32_t ev = 0;  // request event index within this pixel
     int32_t pixreq = 0;
-    int m_key = -1, m_node = -1;  // descent memo (see the traversal)
 
     // Warp-uniform sample loop: lanes whose ray ended idle until the whole
     // packet is done, so the warp reconverges once per sample.
@@ -572,18 +572,44 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                 int cur_node = -1;
                 uint4 wv = make_uint4(0, 0, 0, 0);
                 const int d0 = d;
-                // Descent memo: channel 0's walk from d0 through the ancestors of
-                // the depth-dt node depends only on (raw LOD, d0, that node) --
-                // if the previous sample descended through the same ancestors
-                // without resolving, so does this one: count the steps, start at
-                // dt.  (Requests it would repeat are no-ops: smaller keys exist.)
-                const int sh_dt = D - dt_;
-                const int node_dt = S.lvl_off[dt_] +
-                    ((((qz >> sh_dt) << dt_) + (qy >> sh_dt)) << dt_) + (qx >> sh_dt);
-                if (RO_DESCENT_MEMO && d0 < dt_ && m_key == raw * 32 + d0 && m_node == node_dt) {
-                    c_steps += dt_ - d0;
-                    d = dt_;
+#if RO_FAST_DESCENT
+                // Channel 0 walks d0 -> dt through nodes known up front (the
+                // ancestors of the sample position).  Load its word at every depth
+                // at once and find the first node where it does anything but a
+                // plain descent (valid, not empty, not constant, some level
+                // resident); the generic loop below resumes exactly there.  Any
+                // INVALID ancestor (it would issue a metadata request) stops the
+                // fast walk at that node, so requests stay in program order.
+                if (dt_ - d0 >= 1 && dt_ - d0 <= kFastDepth) {
+                    const int slot0 = S.slot[0];
+                    uint32_t pw[kFastDepth];
+#pragma unroll
+                    for (int i = 0; i < kFastDepth; ++i) {
+                        const int dd = d0 + i;
+                        pw[i] = 0;
+                        if (dd < dt_) {
+                            const int sh = D - dd;
+                            const int nidx = S.lvl_off[dd] +
+                                ((((qz >> sh) << dd) + (qy >> sh)) << dd) + (qx >> sh);
+                            pw[i] = __ldg(A.words + nidx * m + slot0);
+                        }
+                    }
+                    int stop = dt_ - d0;
+#pragma unroll
+                    for (int i = kFastDepth - 1; i >= 0; --i) {
+                        if (d0 + i < dt_) {
+                            const uint32_t w = pw[i];
+                            const int mn = (w >> 16) & 0xFF, mx = (w >> 24) & 0xFF;
+                            const bool plain = !(mn == 255 && mx == 0) &&
+                                               mx >= (int)S.empty_below[0][mn] &&
+                                               mx - mn > eps_i && (w & 0xFFFFu) != 0;
+                            if (!plain) stop = i;
+                        }
+                    }
+                    c_steps += stop;
+                    d = d0 + stop;
                 }
+#endif
 #pragma unroll 1
                 for (int ci = 0; ci < n_ch; ++ci) {
                     const int slot = S.slot[ci];
@@ -669,10 +695,6 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                                                     lbx, lby, lbz, sc.lp2);
                         if (sub.x >= 0) sample2(ci, sub.x, sub.y);
                         break;
-                    }
-                    if (ci == 0) {  // channel 0 done: remember a clean descent
-                        m_key = (d == dt_ && d0 < dt_) ? raw * 32 + d0 : -1;
-                        m_node = node_dt;
                     }
                 }
                 end_depth = d;
