@@ -82,7 +82,10 @@ typedef struct ro_layout {
 typedef struct ro_state {
     uint32_t *words;         /* [N*m] octree words (mask|min<<16|max<<24); may be NULL */
     int32_t *pt;             /* [E]   packed page-table entries */
-    uint8_t *cache;          /* [S*bz*by*bx] brick cache */
+    uint8_t *cache;          /* [S*bz*by*bx] brick cache, allocated with one more
+                                brick of tail padding ((S+1)*bvox bytes): the ray
+                                caster may read -- never use -- bytes just past
+                                a brick's last tap */
     int64_t *slot_brick;     /* [S]   brick id per slot, -1 free */
     int64_t *slot_last_used; /* [S]   LRU frame stamp */
     int32_t *free_stack;     /* [S]   LIFO free list, top at free_count-1 */

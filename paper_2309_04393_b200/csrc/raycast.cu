@@ -84,6 +84,12 @@ struct FrameSmem {
     // largest integer value v with opacity(u) == 0 for every u <= v
     int32_t zero_upto[RO_MAX_CH];
     unsigned long long red[RO_NUM_COUNTERS];
+    // frame constants kept out of registers
+    double bm1[3];      // brick extent - 1, as fp64 (the reference's B - 1.0)
+    double side_d;      // 2^depth
+    double inv_t0;      // 1 / t0 (exact when t0 is a power of two)
+    int32_t t0_pow2;
+    int32_t eps_i;      // (mx - mn) <= eps_h  <=>  (mx - mn) <= eps_i
 };
 
 struct RayArgs {
@@ -252,33 +258,31 @@ RARE __device__ int2 substitute(const int32_t *__restrict__ pt, const FrameSmem 
 
 // trilinear tap addresses + weights inside one brick (kernels.py:136-174)
 struct Taps {
-    int r00, r10, r01, r11;  // row offsets of (y0,z0) (y1,z0) (y0,z1) (y1,z1)
-    int x0, x1;
+    int o;                // offset of tap (x0, y0, z0) inside the brick
     double tx, ty, tz;
 };
 
+// The upper taps are read unclamped at x0+1 / y0+1 / z0+1: the reference
+// clamps them to B-1 only when x0 = B-1, and then f = B-1 exactly, so the
+// weight is 0 and lerp(a, b, 0) = a + (b - a) * 0 = a for any finite b.  The
+// read may touch the next row / slice / brick -- the cache carries one brick
+// of tail padding (resoct.h) -- but never changes a result.
 __device__ __forceinline__ void taps_of(Taps &tp, const LevelPos &lp, int bx, int by,
-                                        int bz) {
+                                        int bz, const FrameSmem &S) {
     const int B[3] = {bx, by, bz};
-    int i0[3], i1[3];
+    int i0[3];
     double tw[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
         // lx = P - c*B exactly; fx = lx - 0.5 exactly; clamped to [0, B-1]
         double f = (lp.P[a] - i2d(lp.cb[a] * B[a])) - 0.5;
         if (f < 0.0) f = 0.0;
-        if (f > B[a] - 1.0) f = B[a] - 1.0;
+        if (f > S.bm1[a]) f = S.bm1[a];
         const int c0 = (int)f;
         i0[a] = c0;
-        i1[a] = c0 + 1 < B[a] ? c0 + 1 : B[a] - 1;
         tw[a] = f - i2d(c0);
     }
-    tp.x0 = i0[0];
-    tp.x1 = i1[0];
-    tp.r00 = (i0[2] * by + i0[1]) * bx;
-    tp.r10 = (i0[2] * by + i1[1]) * bx;
-    tp.r01 = (i1[2] * by + i0[1]) * bx;
-    tp.r11 = (i1[2] * by + i1[1]) * bx;
+    tp.o = (i0[2] * by + i0[1]) * bx + i0[0];
     tp.tx = tw[0];
     tp.ty = tw[1];
     tp.tz = tw[2];
@@ -292,16 +296,21 @@ __device__ __forceinline__ double trilerp(const int v[8], const Taps &tp) {
     return lerp(lerp(c00, c10, tp.ty), lerp(c01, c11, tp.ty), tp.tz);
 }
 
-__device__ __forceinline__ void load_taps(int v[8], const uint8_t *__restrict__ b,
-                                          const Taps &tp) {
-    v[0] = __ldg(b + tp.r00 + tp.x0);
-    v[1] = __ldg(b + tp.r00 + tp.x1);
-    v[2] = __ldg(b + tp.r10 + tp.x0);
-    v[3] = __ldg(b + tp.r10 + tp.x1);
-    v[4] = __ldg(b + tp.r01 + tp.x0);
-    v[5] = __ldg(b + tp.r01 + tp.x1);
-    v[6] = __ldg(b + tp.r11 + tp.x0);
-    v[7] = __ldg(b + tp.r11 + tp.x1);
+// BX/BY = compile-time brick extent (0: runtime) so the eight tap offsets
+// become load immediates off one base address
+template <int BX, int BY>
+__device__ __forceinline__ void load_taps(int v[8], const uint8_t *__restrict__ p, int bx,
+                                          int bxy) {
+    const int sx = BX ? BX : bx;
+    const int sxy = BX ? BX * BY : bxy;
+    v[0] = __ldg(p);
+    v[1] = __ldg(p + 1);
+    v[2] = __ldg(p + sx);
+    v[3] = __ldg(p + sx + 1);
+    v[4] = __ldg(p + sxy);
+    v[5] = __ldg(p + sxy + 1);
+    v[6] = __ldg(p + sxy + sx);
+    v[7] = __ldg(p + sxy + sx + 1);
 }
 
 // audit value from the fully resident reference paging (kernels.py:707-723)
@@ -313,9 +322,9 @@ __device__ double ref_value(const ro_frame &F, const FrameSmem &S, int ci, int l
     const int rp = F.ref_pt[S.ptoff[ci][lev] + lp.local];
     if (rp < 0) return -1.0;
     Taps tp;
-    taps_of(tp, lp, bx, by, bz);
+    taps_of(tp, lp, bx, by, bz, S);
     int v[8];
-    load_taps(v, F.ref_cache + (int64_t)rp * bvox, tp);
+    load_taps<0, 0>(v, F.ref_cache + (int64_t)rp * bvox + tp.o, bx, bx * by);
     return trilerp(v, tp);
 }
 
@@ -330,7 +339,7 @@ struct SampleCtx {
     int tp2_lev;
 };
 
-template <int MODE, bool CHECK>
+template <int MODE, bool CHECK, int BX, int BY>
 __global__ void __launch_bounds__(kBlock, RO_MINB)
 k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A) {
     __shared__ FrameSmem S;
@@ -394,6 +403,15 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
         S.zero_upto[tid] = z;  // (a single-knot TF evaluates to 0 everywhere)
     }
     if (tid < RO_NUM_COUNTERS) S.red[tid] = 0;
+    if (tid == 0) {
+        S.bm1[0] = A.L.bx - 1.0;
+        S.bm1[1] = A.L.by - 1.0;
+        S.bm1[2] = A.L.bz - 1.0;
+        S.side_d = (double)(1 << A.L.depth);
+        S.inv_t0 = 1.0 / F.t0;
+        S.t0_pow2 = (__double_as_longlong(F.t0) & 0x000FFFFFFFFFFFFFll) == 0;
+        S.eps_i = F.eps_h >= 255.0 ? 255 : (F.eps_h < 0.0 ? -1 : (int)F.eps_h);
+    }
     // per-thread arrays: [ci*kBlock + tid]
     int32_t *prev_brick = dyn;                        // n_ch
     int32_t *last_breq = prev_brick + n_ch * kBlock;  // n_ch
@@ -438,13 +456,9 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
     const int lbx = __ffs(bx) - 1, lby = __ffs(by) - 1, lbz = __ffs(bz) - 1;
     const int bvox = bx * by * bz;
     const int D = A.L.depth;
-    const double sideD = (double)(1 << D);
     const bool vec4 = (m == 4);
     const double t0 = F.t0;
-    const bool t0_pow2 = (__double_as_longlong(t0) & 0x000FFFFFFFFFFFFFll) == 0;
-    const double inv_t0 = 1.0 / t0;
     // (mx - mn) <= eps_h  <=>  (mx - mn) <= floor(eps_h) for integer mx - mn
-    const int eps_i = F.eps_h >= 255.0 ? 255 : (F.eps_h < 0.0 ? -1 : (int)F.eps_h);
     const int64_t pix = (int64_t)gy * F.width + x;
     const int64_t lpix = (int64_t)ly * F.width + x;
     const unsigned long long key_hi = (unsigned long long)pix << 32;
@@ -490,7 +504,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
             if (py > kClampHi) py = kClampHi;
             if (pz > kClampHi) pz = kClampHi;
 
-            const int raw = lod_raw(t, t0, inv_t0, t0_pow2, S);
+            const int raw = lod_raw(t, t0, S.inv_t0, S.t0_pow2, S);
             double step = S.step_tab[raw];
             int jexp = S.maxlev[raw];
             const int dt_ = S.dt_tab[raw];
@@ -511,7 +525,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
 
             auto finish = [&](int ci, int lev, int slot_lin, const LevelPos &lp, const Taps &tp) {
                 int tv[8];
-                load_taps(tv, A.cache + (int64_t)slot_lin * bvox, tp);
+                load_taps<BX, BY>(tv, A.cache + (int64_t)slot_lin * bvox + tp.o, bx, bx * by);
                 const int32_t e = S.ptoff[ci][lev] + lp.local;
                 int32_t &pb = prev_brick[ci * kBlock + tid];
                 if (e != pb) {
@@ -537,17 +551,17 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
             };
             // sample at the desired level (sc.lp already holds it)
             auto sample = [&](int ci, int lev, int slot_lin) {
-                if (sc.tp_lev != lev) { taps_of(sc.tp, sc.lp, bx, by, bz); sc.tp_lev = lev; }
+                if (sc.tp_lev != lev) { taps_of(sc.tp, sc.lp, bx, by, bz, S); sc.tp_lev = lev; }
                 finish(ci, lev, slot_lin, sc.lp, sc.tp);
             };
             // sample at a substitute level (sc.lp2 holds it)
             auto sample2 = [&](int ci, int lev, int slot_lin) {
 #if RO_SUBCACHE
-                if (sc.tp2_lev != lev) { taps_of(sc.tp2, sc.lp2, bx, by, bz); sc.tp2_lev = lev; }
+                if (sc.tp2_lev != lev) { taps_of(sc.tp2, sc.lp2, bx, by, bz, S); sc.tp2_lev = lev; }
                 finish(ci, lev, slot_lin, sc.lp2, sc.tp2);
 #else
                 Taps t2;
-                taps_of(t2, sc.lp2, bx, by, bz);
+                taps_of(t2, sc.lp2, bx, by, bz, S);
                 finish(ci, lev, slot_lin, sc.lp2, t2);
 #endif
             };
@@ -562,7 +576,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                 }
             } else {
                 // kernels.py:431-558 -- one cursor shared by all channels
-                const int qx = (int)(px * sideD), qy = (int)(py * sideD), qz = (int)(pz * sideD);
+                const int qx = (int)(px * S.side_d), qy = (int)(py * S.side_d), qz = (int)(pz * S.side_d);
                 int d = prev_depth - 1;
                 if (d < 0) d = 0;
                 if (F.start_level < d) d = F.start_level;
@@ -602,7 +616,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                             const int mn = (w >> 16) & 0xFF, mx = (w >> 24) & 0xFF;
                             const bool plain = !(mn == 255 && mx == 0) &&
                                                mx >= (int)S.empty_below[0][mn] &&
-                                               mx - mn > eps_i && (w & 0xFFFFu) != 0;
+                                               mx - mn > S.eps_i && (w & 0xFFFFu) != 0;
                             if (!plain) stop = i;
                         }
                     }
@@ -645,7 +659,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                                 zero_mask |= 1u << ci;
                                 break;
                             }
-                            if (mx - mn <= eps_i) {  // K_CONST
+                            if (mx - mn <= S.eps_i) {  // K_CONST
                                 double r, g, b, a;
                                 tf_eval(S, ci, (double)mn, r, g, b, a);
                                 sR += r * a;
@@ -732,7 +746,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                             if (qx > kClampHi) qx = kClampHi;
                             if (qy > kClampHi) qy = kClampHi;
                             if (qz > kClampHi) qz = kClampHi;
-                            const int raw2 = lod_raw(t, t0, inv_t0, t0_pow2, S);
+                            const int raw2 = lod_raw(t, t0, S.inv_t0, S.t0_pow2, S);
                             for (int ci = 0; ci < n_ch; ++ci) {
                                 if (!((zero_mask >> ci) & 1u)) continue;
                                 const int lev = clampi(raw2, S.lo[ci], S.hi[ci]);
@@ -746,7 +760,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                             }
                         }
                     }
-                    const int raw2 = lod_raw(t, t0, inv_t0, t0_pow2, S);
+                    const int raw2 = lod_raw(t, t0, S.inv_t0, S.t0_pow2, S);
                     step = S.step_tab[raw2];
                     jexp = S.maxlev[raw2];
                     t += step;
@@ -818,8 +832,8 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
     }
 }
 
-template <int MODE, bool CHECK>
-cudaError_t launch(const ro_frame &F, const RayArgs &A, cudaStream_t s) {
+template <int MODE, bool CHECK, int BX, int BY>
+cudaError_t launch_b(const ro_frame &F, const RayArgs &A, cudaStream_t s) {
     int n_tiles = ((F.width + kTileW - 1) / kTileW) * ((A.local_rows + kTileH - 1) / kTileH);
     static int sm_count = 0;
     if (sm_count == 0) {
@@ -828,7 +842,7 @@ cudaError_t launch(const ro_frame &F, const RayArgs &A, cudaStream_t s) {
         cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev);
     }
     size_t dyn = (size_t)F.n_ch * kBlock * 4 * 3 + (size_t)F.n_ch * A.L.k * kBlock * 4;
-    auto kern = k_raycast<MODE, CHECK>;
+    auto kern = k_raycast<MODE, CHECK, BX, BY>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)dyn);
     if (e != cudaSuccess) return e;
@@ -844,6 +858,14 @@ cudaError_t launch(const ro_frame &F, const RayArgs &A, cudaStream_t s) {
 #endif
     kern<<<blocks, kBlock, dyn, s>>>(F, A);
     return cudaGetLastError();
+}
+
+// brick sizes with compile-time tap offsets; anything else uses runtime ones
+template <int MODE, bool CHECK>
+cudaError_t launch(const ro_frame &F, const RayArgs &A, cudaStream_t s) {
+    if (A.L.bx == 32 && A.L.by == 32) return launch_b<MODE, CHECK, 32, 32>(F, A, s);
+    if (A.L.bx == 16 && A.L.by == 16) return launch_b<MODE, CHECK, 16, 16>(F, A, s);
+    return launch_b<MODE, CHECK, 0, 0>(F, A, s);
 }
 
 }  // namespace

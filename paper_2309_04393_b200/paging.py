@@ -115,8 +115,11 @@ class MultiChannelPaging:
         dev = self.device
         self.pt = torch.full((self.total_entries,), N.RO_PT_UNMAPPED,
                              dtype=torch.int32, device=dev)
-        self.cache_dev = torch.zeros((self.num_slots, sz, sy, sx), dtype=torch.uint8,
-                                     device=dev)
+        # one brick of tail padding: the ray caster may read (never use) the
+        # byte after a brick's last tap (resoct.h, ro_state.cache)
+        self._cache_storage = torch.zeros((self.num_slots + 1, sz, sy, sx),
+                                          dtype=torch.uint8, device=dev)
+        self.cache_dev = self._cache_storage[:self.num_slots]
         self.slot_brick_dev = torch.full((self.num_slots,), -1, dtype=torch.int64,
                                          device=dev)
         self.slot_last_used_dev = torch.zeros(self.num_slots, dtype=torch.int64,
