@@ -44,14 +44,56 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons during the timed region."""
+    """SM clocks + throttle reasons sampled DURING the timed region: an NVML
+    polling thread (every ~2 ms), falling back to `nvidia-smi -lms`."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown",
+               0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap"}
 
     def __init__(self, gpu: int):
         self.gpu = gpu
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = None
+        self._thread = None
         self.proc = None
         self.path = f"/tmp/bench_clocks_{os.getpid()}.csv"
 
+    def _handle(self):
+        import pynvml
+        pynvml.nvmlInit()
+        try:
+            pr = torch.cuda.get_device_properties(self.gpu)
+            bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+            return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(bus.encode())
+        except Exception:
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+
     def start(self):
+        import threading
+        try:
+            nv, h = self._handle()
+            self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+        except Exception:
+            return self._start_smi()
+        self._stop = threading.Event()
+
+        def run():
+            while not self._stop.is_set():
+                try:
+                    self.samples.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
+                    bits = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    for b, name in self.REASONS.items():
+                        if bits & b:
+                            self.reasons.add(name)
+                except Exception:
+                    pass
+                time.sleep(0.002)
+        self._thread = threading.Thread(target=run, daemon=True)
+        self._thread.start()
+
+    def _start_smi(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu),
@@ -64,8 +106,14 @@ class ClockSampler:
             self.proc = None
 
     def stop(self) -> dict:
+        if self._thread is not None:
+            self._stop.set()
+            self._thread.join(timeout=5)
+            return {"sm_mhz": float(np.median(self.samples)) if self.samples else None,
+                    "sm_max_mhz": self.max_mhz, "samples": len(self.samples),
+                    "reasons": sorted(self.reasons), "source": "nvml"}
         if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"]}
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
@@ -87,7 +135,17 @@ class ClockSampler:
                     reasons.add(n)
         return {"sm_mhz": float(np.median(sm)) if sm else None,
                 "sm_max_mhz": max(smax) if smax else None,
-                "samples": len(sm), "reasons": sorted(reasons)}
+                "samples": len(sm), "reasons": sorted(reasons), "source": "nvidia-smi"}
+
+
+def _ncu_traffic(world):
+    """dram read+write bytes per ray-cast launch from the committed ncu
+    capture (profiles/ncu_raycast_summary.json), scaled to this part."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_raycast_summary.json")) as f:
+            return json.load(f)["dram_bytes_per_launch"] / world
+    except Exception:
+        return None
 
 
 def _dist_init():
@@ -338,7 +396,8 @@ def run_ours(args):
                            "pixels": P, "livelocked_rays": int(counters[4])},
             "kernel_ms": {"raycast": kern_ms, "feedback": fb_ms},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak,
-                         "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                         "unit": "GB/s", "frac": achieved / peak, "traffic": _ncu_traffic(world),
+                         "traffic_source": "profiles/ncu_raycast_summary.json (ncu --set full)",
                          "peak_kind": peak_kind,
                          "algorithmic_bytes_per_launch": part_bytes,
                          "model": "13*F + 4*S + 16*P bytes (SURVEY 8d), /ray-cast kernel time"},
