@@ -392,3 +392,44 @@ def test_gpu_cycif_small_scenario_matches_oracle():
     assert np.array_equal(out.required_mask, want.required_mask)
     assert np.array_equal(out.level_histogram, want.level_histogram)
     torch.cuda.synchronize()
+
+
+def test_gpu_config3_mixed_bias_swap_session_matches_oracle():
+    """Config 3 (scaled): 8-channel sparse volume, m = 4 slots with mixed
+    level ranges, cold session with budget pressure, a mid-sequence swap of
+    all four slots to the other four channels, run on; every frame's image,
+    ordered requests, usage mask and the full state equal the oracle."""
+    from oracle.session import OracleSession, state_hashes
+    from paper_2309_04393_b200 import (ChannelSettings, EngineConfig, LocalTransport,
+                                       RenderConfig, Session, grayscale_ramp_tf, orbit_pose)
+    from paper_2309_04393_b200 import volume as V
+    from oracle import raycast as orc
+    store = V.VolumeStore(V.sparse_multichannel(64, channels=8), (16, 16, 16), 3, (2, 2, 2))
+    ranges = [(0, 2), (1, 2), (2, 2), (0, 1)]
+    tfs = [grayscale_ramp_tf(40.0), grayscale_ramp_tf(30.0, 0.6),
+           grayscale_ramp_tf(50.0), grayscale_ramp_tf(20.0, 0.8)]
+    chans = [ChannelSettings(slot=s, tf=tfs[s], level_range=ranges[s]) for s in range(4)]
+    rconf = RenderConfig(image_dims=(56, 48), base_step=1 / 64, max_requests_per_frame=40)
+    econf = EngineConfig(octree_depth=3, cache_slots=(5, 5, 4), channel_slots=4)
+    sess = Session(LocalTransport(store), econf, rconf, chans)
+    och = [orc.OracleChannel(slot=c.slot, points=c.tf.points, level_range=c.level_range)
+           for c in chans]
+    ora = OracleSession(store, 4, 3, (5, 5, 4), och,
+                        dict(image_dims=(56, 48), base_step=1 / 64, budget=40),
+                        sess.engine.metadata_pad)
+    pose = orbit_pose(2.6, radius=2.0)
+    cam = cam_tuple(pose)
+    for i in range(16):
+        if i == 8:
+            for s in range(4):
+                sess.swap_channel(s, 4 + s)
+                ora.swap_channel(s, 4 + s)
+        r = sess.step_frame(pose)
+        o = ora.step_frame(cam)
+        assert np.array_equal(r.output.image, o.image), i
+        assert r.output.brick_requests == o.brick_requests, i
+        assert r.output.metadata_requests == o.metadata_requests, i
+        assert np.array_equal(r.output.required_mask, o.required_mask), i
+        d = diff_hashes(device_state_hashes(sess.engine), state_hashes(ora.st))
+        assert not d, (i, d)
+    sess.close()
