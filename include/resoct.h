@@ -8,8 +8,9 @@
  * resoctree/.
  *
  *   ro_render            kernels.py:209-704  raycast_frame (MODE_RESIDENCY /
- *                        MODE_REFERENCE, check_skips audit), driven by
- *                        render.py:125-208 (_run) and camera.py:32-51
+ *                        MODE_REFERENCE / MODE_PAGETABLE / MODE_CLASSIC,
+ *                        check_skips audit), driven by render.py:125-208
+ *                        (_run), render.py:236-262 and camera.py:32-51
  *   ro_feedback_collect  render.py:210-215  bricks-first request budget over
  *                        the first-seen request lists of kernels.py:457-517
  *   ro_note_sampled      engine.py:72-81    Engine.note_sampled
@@ -57,6 +58,8 @@ extern "C" {
 
 #define RO_MODE_RESIDENCY 0
 #define RO_MODE_REFERENCE 1
+#define RO_MODE_PAGETABLE 2  /* page-table-only baseline, kernels.py:316-357 */
+#define RO_MODE_CLASSIC 3    /* classic one-node-one-brick octree, kernels.py:359-429 */
 
 /* packed page-table entry: >= 0 cache slot (MAPPED), else: */
 #define RO_PT_UNMAPPED (-1)
@@ -120,9 +123,14 @@ typedef struct ro_frame {
     int32_t dt_tab[RO_MAX_LEVELS];       /* traversal_depth(step_tab[raw]) */
     /* sort-first partition: rows are cut in blocks of tile_rows; block b is
        rendered by part (b % n_parts).  Outputs are local (compacted rows). */
-    int32_t n_parts, part, tile_rows, _pad0;
+    int32_t n_parts, part, tile_rows;
+    int32_t cls_depth;            /* RO_MODE_CLASSIC: classic octree depth = k-1 */
     const int32_t *ref_pt;        /* audit paging (check_skips), device */
     const uint8_t *ref_cache;
+    /* RO_MODE_CLASSIC: per-node min / max u8[n_nodes*m] of the classic octree
+       (render.py:271-315 ClassicMetadata.min_arr / max_arr), device */
+    const uint8_t *cls_min;
+    const uint8_t *cls_max;
     ro_channel ch[RO_MAX_CH];
 } ro_frame;
 

@@ -25,6 +25,8 @@ from .build import build, lib_path
 INF = float("inf")
 MODE_RESIDENCY = 0
 MODE_REFERENCE = 1
+MODE_PAGETABLE = 2
+MODE_CLASSIC = 3
 
 _P = C.c_void_p
 
@@ -44,6 +46,8 @@ class _Frame(C.Structure):
         ("pt_offsets", _P), ("pt_status", _P), ("pt_slot", _P), ("cache", _P),
         ("check_skips", C.c_int64), ("ref_status", _P), ("ref_slot", _P),
         ("ref_cache", _P),
+        ("cls_min", _P), ("cls_max", _P), ("cls_depth", C.c_int64),
+        ("cls_lvl_off", _P),
         ("image", _P), ("brick_req", _P), ("brick_req_n", _P),
         ("meta_req", _P), ("meta_req_n", _P), ("req_cap", C.c_int64),
         ("seen_brick", _P), ("seen_meta", _P), ("required", _P),
@@ -192,10 +196,11 @@ def _ptr(a):
 def render(state: OracleState, channels, camera, image_dims, base_step,
            t0=1.0, early_alpha=0.99, budget=256, start_level=2,
            mode=MODE_RESIDENCY, reference_state: OracleState | None = None,
-           rows=None, threads=1, rays=None) -> OracleOutput:
+           rows=None, threads=1, rays=None, classic=None) -> OracleOutput:
     """One oracle frame.
 
-    camera: (position, target, up, fov_deg).  ``rows`` = (row_begin,
+    camera: (position, target, up, fov_deg).  ``classic`` = (min u8[n, m],
+    max u8[n, m], depth) for MODE_CLASSIC (render.py:271-315).  ``rows`` = (row_begin,
     row_end) renders only those scanlines (the other pixels stay zero);
     ``threads`` > 1 uses the band-parallel driver (identical results).
     """
@@ -261,6 +266,15 @@ def render(state: OracleState, channels, camera, image_dims, base_step,
                np.ascontiguousarray(reference_state.cache, dtype=np.uint8))
     else:
         ref = (None, None, None)
+    if mode == MODE_CLASSIC:
+        cmin = np.ascontiguousarray(classic[0], dtype=np.uint8)
+        cmax = np.ascontiguousarray(classic[1], dtype=np.uint8)
+        cdepth = int(classic[2])
+    else:
+        cmin = cmax = np.zeros((1, m), dtype=np.uint8)
+        cdepth = 0
+    cls_off = np.array([((1 << (3 * d)) - 1) // 7 for d in range(cdepth + 1)],
+                       dtype=np.int64)
     r0, r1 = (0, h) if rows is None else rows
     fr = _Frame(
         mode=mode, npix=npix, origins=_ptr(origins), dirs=_ptr(dirs),
@@ -275,6 +289,8 @@ def render(state: OracleState, channels, camera, image_dims, base_step,
         pt_status=_ptr(pt_status), pt_slot=_ptr(pt_slot), cache=_ptr(cache),
         check_skips=1 if reference_state is not None else 0,
         ref_status=_ptr(ref[0]), ref_slot=_ptr(ref[1]), ref_cache=_ptr(ref[2]),
+        cls_min=_ptr(cmin), cls_max=_ptr(cmax), cls_depth=cdepth,
+        cls_lvl_off=_ptr(cls_off),
         image=_ptr(image), brick_req=_ptr(brick_req), brick_req_n=_ptr(brick_n),
         meta_req=_ptr(meta_req), meta_req_n=_ptr(meta_n), req_cap=cap,
         seen_brick=_ptr(seen_brick), seen_meta=_ptr(seen_meta),

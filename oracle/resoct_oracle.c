@@ -3,7 +3,8 @@
  *
  * A plain-C restatement of the reference ray-cast frame kernel
  *   /root/reference/pkg/src/resoctree/kernels.py:209-704 (raycast_frame)
- * for MODE_RESIDENCY (kernels.py:431-558) and MODE_REFERENCE (301-314),
+ * for MODE_RESIDENCY (kernels.py:431-558), MODE_REFERENCE (301-314) and
+ * the two baseline methods MODE_PAGETABLE (316-357) / MODE_CLASSIC (359-429),
  * including the skip loop (561-635), single-sample compositing (637-694)
  * and the skip audit (`check_skips`, 595-625 / 644-655 / 707-723).
  *
@@ -34,8 +35,11 @@
 #define K_MISSU 3
 #define K_MISSP 4
 #define ST_MAPPED 1
+#define ST_EMPTY 2
 #define MODE_RESIDENCY 0
 #define MODE_REFERENCE 1
+#define MODE_PAGETABLE 2
+#define MODE_CLASSIC 3
 #define MAXC 64
 
 static const double CLAMP_HI = 1.0 - 1e-9;
@@ -66,6 +70,10 @@ typedef struct oracle_frame {
     const int8_t *ref_status;
     const int32_t *ref_slot;
     const uint8_t *ref_cache;
+    /* classic-octree baseline metadata (render.py:271-315), MODE_CLASSIC only */
+    const uint8_t *cls_min, *cls_max; /* [n_nodes*m] */
+    int64_t cls_depth;
+    const int64_t *cls_lvl_off;       /* [cls_depth+1] */
     /* outputs */
     float *image;             /* [npix*4] */
     int64_t *brick_req, *brick_req_n;
@@ -290,6 +298,104 @@ int oracle_raycast(const oracle_frame *f) {
                     } else {
                         out_kind[ci] = K_MISSP;
                     }
+                }
+            } else if (f->mode == MODE_PAGETABLE) { /* kernels.py:316-357 */
+                int all_empty = 1;
+                skip_exit = 1e30;
+                for (int64_t ci = 0; ci < n_ch; ++ci) {
+                    int64_t lev = desired[ci];
+                    int64_t cbx = brick_axis(px, f->dims[lev * 3 + 0], bx, f->grids[lev * 3 + 0]);
+                    int64_t cby = brick_axis(py, f->dims[lev * 3 + 1], by, f->grids[lev * 3 + 1]);
+                    int64_t cbz = brick_axis(pz, f->dims[lev * 3 + 2], bz, f->grids[lev * 3 + 2]);
+                    int64_t slot = f->ch_slot[ci];
+                    int64_t e = entry_index(f, slot, lev, cbx, cby, cbz);
+                    int st = f->pt_status[e];
+                    if (st == ST_MAPPED) {
+                        out_kind[ci] = K_SAMPLE;
+                        out_slot[ci] = f->pt_slot[e];
+                        out_level[ci] = lev;
+                        all_empty = 0;
+                    } else if (st == ST_EMPTY) {
+                        out_kind[ci] = K_ZERO;
+                        double dxl = (double)f->dims[lev * 3 + 0], dyl = (double)f->dims[lev * 3 + 1],
+                               dzl = (double)f->dims[lev * 3 + 2];
+                        double ex = box_exit(ox, oy, oz, dx, dy, dz,
+                                             (double)(cbx * bx) / dxl, (double)(cby * by) / dyl,
+                                             (double)(cbz * bz) / dzl,
+                                             (double)((cbx + 1) * bx) / dxl,
+                                             (double)((cby + 1) * by) / dyl,
+                                             (double)((cbz + 1) * bz) / dzl);
+                        if (ex < skip_exit) skip_exit = ex;
+                    } else {
+                        out_kind[ci] = K_MISSP;
+                        if (f->seen_brick[e] == 0) {
+                            f->seen_brick[e] = 1;
+                            push_req(f->brick_req, f->brick_req_n, f->req_cap,
+                                     brick_id(slot, k, lev, cbx, cby, cbz));
+                        }
+                        all_empty = 0;
+                    }
+                }
+                skippable = all_empty;
+            } else if (f->mode == MODE_CLASSIC) { /* kernels.py:359-429 */
+                int all_empty = 1;
+                int64_t deep_d = -1, dix = 0, diy = 0, diz = 0;
+                for (int64_t ci = 0; ci < n_ch; ++ci) {
+                    int64_t lev = desired[ci];
+                    int64_t slot = f->ch_slot[ci];
+                    int64_t d_target = f->cls_depth - lev;
+                    if (d_target < 0) d_target = 0;
+                    int64_t d = 0, last_slot = -1, last_lev = -1;
+                    while (1) {
+                        steps_total += 1;
+                        int64_t side = (int64_t)1 << d;
+                        int64_t ix = (int64_t)(px * (double)side);
+                        int64_t iy = (int64_t)(py * (double)side);
+                        int64_t iz = (int64_t)(pz * (double)side);
+                        int64_t nidx = f->cls_lvl_off[d] + (iz * side + iy) * side + ix;
+                        int64_t mn = f->cls_min[nidx * m + slot], mx = f->cls_max[nidx * m + slot];
+                        if (is_empty_meta(f, ci, mn, mx)) {
+                            out_kind[ci] = K_ZERO;
+                            if (d > deep_d) { deep_d = d; dix = ix; diy = iy; diz = iz; }
+                            break;
+                        }
+                        int64_t lev_d = f->cls_depth - d;
+                        int64_t e = entry_index(f, slot, lev_d, ix, iy, iz);
+                        f->required[e] = 1;
+                        if (f->pt_status[e] != ST_MAPPED) {
+                            if (f->seen_brick[e] == 0) {
+                                f->seen_brick[e] = 1;
+                                push_req(f->brick_req, f->brick_req_n, f->req_cap,
+                                         brick_id(slot, k, lev_d, ix, iy, iz));
+                            }
+                            /* descent blocked: deepest resident ancestor */
+                            if (last_slot >= 0) {
+                                out_kind[ci] = K_SAMPLE;
+                                out_slot[ci] = last_slot;
+                                out_level[ci] = last_lev;
+                            } else {
+                                out_kind[ci] = K_MISSP;
+                            }
+                            all_empty = 0;
+                            break;
+                        }
+                        last_slot = f->pt_slot[e];
+                        last_lev = lev_d;
+                        if (d == d_target) {
+                            out_kind[ci] = K_SAMPLE;
+                            out_slot[ci] = last_slot;
+                            out_level[ci] = last_lev;
+                            all_empty = 0;
+                            break;
+                        }
+                        d += 1;
+                    }
+                }
+                if (all_empty && deep_d >= 0) {
+                    skippable = 1;
+                    double s = 1.0 / (double)((int64_t)1 << deep_d);
+                    skip_exit = box_exit(ox, oy, oz, dx, dy, dz, dix * s, diy * s, diz * s,
+                                         (dix + 1) * s, (diy + 1) * s, (diz + 1) * s);
                 }
             } else { /* MODE_RESIDENCY, kernels.py:431-558 */
                 int64_t d = prev_depth - 1;

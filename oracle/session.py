@@ -131,3 +131,59 @@ def prepare_full(store, slots_to_channels, m, depth, cache_slots, pad,
             masks = st.words[base:base + side ** 3, slot] & np.uint32(0xFFFF)
             st.words[base:base + side ** 3, slot] = masks | w.ravel()
     return st
+
+
+def prepare_paging(store, slots_to_channels, m, depth, cache_slots, keep=None,
+                   zero_as_empty=False):
+    """Paging-only prefill in (slot, level, z, y, x) order at frame 0.
+
+    ``zero_as_empty`` restates bench.py:74-95 (prepare_pagetable_engine):
+    all-zero payloads are entered EMPTY instead of taking a cache slot.
+    ``keep(slot, level, x, y, z)`` (optional) selects the bricks inserted,
+    for partially resident baselines; the octree is left untouched."""
+    man = store.manifest
+    k = len(man.levels)
+    st = OracleResidency(m, k, man.brick_size, [l.dims for l in man.levels],
+                         [l.brick_grid_dims for l in man.levels], cache_slots, depth)
+    for slot in sorted(slots_to_channels):
+        ch = slots_to_channels[slot]
+        for lev in range(k):
+            gx, gy, gz = man.levels[lev].brick_grid_dims
+            for z in range(gz):
+                for y in range(gy):
+                    for x in range(gx):
+                        payload = store.brick(ch, lev, (x, y, z))
+                        bid = ((slot * k + lev) << 24) | (z << 16) | (y << 8) | x
+                        if zero_as_empty and int(payload.max()) == 0:
+                            st.mark_empty(bid)
+                        elif keep is None or keep(slot, lev, x, y, z):
+                            st.insert_brick(bid, payload, 0)
+    return st
+
+
+def classic_metadata(level0_volumes, m, k):
+    """Per-node min / max of the classic one-node-one-brick octree
+    (render.py:271-315, ClassicMetadata.build_from_volume): node depth d
+    holds the exact min / max of its (dims / 2^d)-voxel block of the level-0
+    volume, depth = k - 1.  Unfilled slots keep (min 0, max 255).
+    Returns (min u8[n, m], max u8[n, m], depth)."""
+    depth = k - 1
+    n_nodes = ((1 << (3 * k)) - 1) // 7
+    mins = np.zeros((n_nodes, m), dtype=np.uint8)
+    maxs = np.full((n_nodes, m), 255, dtype=np.uint8)
+    for slot, vol in level0_volumes.items():
+        g = 1 << depth
+        nz, ny, nx = vol.shape
+        blocks = vol.reshape(g, nz // g, g, ny // g, g, nx // g)
+        lo = blocks.min(axis=(1, 3, 5))
+        hi = blocks.max(axis=(1, 3, 5))
+        for d in range(depth, -1, -1):
+            base = ((1 << (3 * d)) - 1) // 7
+            side = 1 << d
+            mins[base:base + side ** 3, slot] = lo.reshape(-1)
+            maxs[base:base + side ** 3, slot] = hi.reshape(-1)
+            if d:
+                h = side // 2
+                lo = lo.reshape(h, 2, h, 2, h, 2).min(axis=(1, 3, 5))
+                hi = hi.reshape(h, 2, h, 2, h, 2).max(axis=(1, 3, 5))
+    return mins, maxs, depth

@@ -21,6 +21,8 @@ RO_MAX_TF_POINTS = 16
 RO_NUM_COUNTERS = 8
 RO_MODE_RESIDENCY = 0
 RO_MODE_REFERENCE = 1
+RO_MODE_PAGETABLE = 2
+RO_MODE_CLASSIC = 3
 RO_PT_UNMAPPED = -1
 RO_PT_EMPTY = -2
 
@@ -68,7 +70,8 @@ class Frame(C.Structure):
                 ("maxlev_tab", _i32 * RO_MAX_LEVELS),
                 ("dt_tab", _i32 * RO_MAX_LEVELS),
                 ("n_parts", _i32), ("part", _i32), ("tile_rows", _i32),
-                ("_pad0", _i32), ("ref_pt", _p), ("ref_cache", _p),
+                ("cls_depth", _i32), ("ref_pt", _p), ("ref_cache", _p),
+                ("cls_min", _p), ("cls_max", _p),
                 ("ch", Channel * RO_MAX_CH)]
 
 

@@ -1,8 +1,9 @@
 // raycast.cu -- kernel 1: the per-pixel residency-octree ray caster.
 //
 // Restates /root/reference/pkg/src/resoctree/kernels.py:209-704
-// (raycast_frame) for MODE_RESIDENCY (431-558) and MODE_REFERENCE (301-314)
-// with the skip loop (561-635), single-sample compositing (637-694) and the
+// (raycast_frame) for MODE_RESIDENCY (431-558), MODE_REFERENCE (301-314) and
+// the paper's two baseline methods, MODE_PAGETABLE (316-357) and MODE_CLASSIC
+// (359-429), with the skip loop (561-635), single-sample compositing (637-694) and the
 // skip audit (595-625, 644-655, 707-723).
 //
 // B200 design:
@@ -566,7 +567,107 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
 #endif
             };
 
-            if (MODE == RO_MODE_REFERENCE) {  // kernels.py:301-314
+            // sample channel ci from `slot_lin` at level `lev` (any level)
+            auto sample_at = [&](int ci, int lev, int slot_lin) {
+                if (sc.lp.lev != lev) level_pos(sc.lp, lev, px, py, pz, S, lbx, lby, lbz);
+                sample(ci, lev, slot_lin);
+            };
+
+            if (MODE == RO_MODE_PAGETABLE) {  // kernels.py:316-357
+                // desired-level probe per channel; EMPTY entries are skippable
+                // up to the exit of their brick box
+                bool all_empty = true;
+                skip_exit = 1e30;
+#pragma unroll 1
+                for (int ci = 0; ci < n_ch; ++ci) {
+                    const int lev = clampi(raw, S.lo[ci], S.hi[ci]);
+                    if (sc.lp.lev != lev) level_pos(sc.lp, lev, px, py, pz, S, lbx, lby, lbz);
+                    const int32_t e = S.ptoff[ci][lev] + sc.lp.local;
+                    const int pv = __ldg(A.pt + e);
+                    if (pv >= 0) {
+                        all_empty = false;
+                        sample(ci, lev, pv);
+                    } else if (pv == RO_PT_EMPTY) {
+                        zero_mask |= 1u << ci;
+                        // c*B / float(dim): integer numerator, one IEEE division
+                        const double ex = box_exit(
+                            ox, oy, oz, dx, dy, dz, i2d(sc.lp.cb[0] * bx) / S.dimd[lev][0],
+                            i2d(sc.lp.cb[1] * by) / S.dimd[lev][1],
+                            i2d(sc.lp.cb[2] * bz) / S.dimd[lev][2],
+                            i2d((sc.lp.cb[0] + 1) * bx) / S.dimd[lev][0],
+                            i2d((sc.lp.cb[1] + 1) * by) / S.dimd[lev][1],
+                            i2d((sc.lp.cb[2] + 1) * bz) / S.dimd[lev][2]);
+                        if (ex < skip_exit) skip_exit = ex;
+                    } else {
+                        all_empty = false;
+                        const unsigned long long key = key_hi | ev++;
+                        int32_t &lb = last_breq[ci * kBlock + tid];
+                        if (e != lb) {
+                            lb = e;
+                            request(A.brick_key, nullptr, nullptr, e, key);
+                        }
+                    }
+                }
+                skippable = all_empty;
+            } else if (MODE == RO_MODE_CLASSIC) {  // kernels.py:359-429
+                // per channel, a root-to-target descent of the classic octree
+                // (node depth d <-> level cls_depth - d, one brick per node)
+                const int CD = F.cls_depth;
+                const double cside = (double)(1 << CD);
+                const int qx = (int)(px * cside), qy = (int)(py * cside), qz = (int)(pz * cside);
+                bool all_empty = true;
+                int deep_d = -1, dix = 0, diy = 0, diz = 0;
+#pragma unroll 1
+                for (int ci = 0; ci < n_ch; ++ci) {
+                    const int slot = S.slot[ci];
+                    const int lev = clampi(raw, S.lo[ci], S.hi[ci]);
+                    const int d_target = CD - lev > 0 ? CD - lev : 0;
+                    int last_slot = -1, last_lev = -1;
+                    for (int d = 0;; ++d) {
+                        c_steps += 1;
+                        const int sh = CD - d;
+                        const int ix = qx >> sh, iy = qy >> sh, iz = qz >> sh;
+                        const int local = (((iz << d) + iy) << d) + ix;
+                        const int nidx = S.lvl_off[d] + local;
+                        const int mn = __ldg(F.cls_min + nidx * m + slot);
+                        const int mx = __ldg(F.cls_max + nidx * m + slot);
+                        if (mx < (int)S.empty_below[ci][mn]) {  // K_ZERO
+                            zero_mask |= 1u << ci;
+                            if (d > deep_d) { deep_d = d; dix = ix; diy = iy; diz = iz; }
+                            break;
+                        }
+                        const int lev_d = CD - d;
+                        const int32_t e = S.ptoff[ci][lev_d] + local;  // grid 2^d per axis
+                        A.required[e] = 1;
+                        const int pv = __ldg(A.pt + e);
+                        if (pv < 0) {
+                            const unsigned long long key = key_hi | ev++;
+                            int32_t &lb = last_breq[ci * kBlock + tid];
+                            if (e != lb) {
+                                lb = e;
+                                request(A.brick_key, nullptr, nullptr, e, key);
+                            }
+                            // descent blocked: deepest resident ancestor
+                            if (last_slot >= 0) sample_at(ci, last_lev, last_slot);
+                            all_empty = false;
+                            break;
+                        }
+                        last_slot = pv;
+                        last_lev = lev_d;
+                        if (d == d_target) {
+                            sample_at(ci, lev_d, pv);
+                            all_empty = false;
+                            break;
+                        }
+                    }
+                }
+                if (all_empty && deep_d >= 0) {
+                    skippable = true;
+                    const double s = 1.0 / (double)(1 << deep_d);
+                    skip_exit = box_exit(ox, oy, oz, dx, dy, dz, dix * s, diy * s, diz * s,
+                                         (dix + 1) * s, (diy + 1) * s, (diz + 1) * s);
+                }
+            } else if (MODE == RO_MODE_REFERENCE) {  // kernels.py:301-314
 #pragma unroll 1
                 for (int ci = 0; ci < n_ch; ++ci) {
                     const int lev = clampi(raw, S.lo[ci], S.hi[ci]);
@@ -890,8 +991,24 @@ int render(ro_ctx *c, const ro_frame *F, const ro_state *st,
     }
     if (F->mode == RO_MODE_RESIDENCY && st->words == nullptr)
         return fail(RO_EINVAL, "residency mode needs octree words");
+    if (F->mode < RO_MODE_RESIDENCY || F->mode > RO_MODE_CLASSIC)
+        return fail(RO_EINVAL, "unknown render mode");
     if (F->check_skips && (F->ref_pt == nullptr || F->ref_cache == nullptr))
         return fail(RO_EINVAL, "check_skips needs reference paging");
+    if (F->check_skips && F->mode != RO_MODE_RESIDENCY)
+        return fail(RO_EINVAL, "the skip audit runs in residency mode only");
+    if (F->mode == RO_MODE_CLASSIC) {
+        // render.py:282-295: node depth d owns exactly one brick of level k-1-d
+        const int k = c->layout.k;
+        if (F->cls_min == nullptr || F->cls_max == nullptr)
+            return fail(RO_EINVAL, "classic mode needs classic min / max metadata");
+        if (F->cls_depth != k - 1 || k - 1 > 8)
+            return fail(RO_EINVAL, "classic octree depth must be k-1 <= 8");
+        for (int l = 0; l < k; ++l)
+            for (int a = 0; a < 3; ++a)
+                if (c->layout.level_grids[l][a] != (1 << (k - 1 - l)))
+                    return fail(RO_EINVAL, "classic octree needs power-of-two brick grids");
+    }
     if (c->bvox >= (int64_t(1) << 24)) return fail(RO_EINVAL, "brick too large");
     if (F->mode == RO_MODE_RESIDENCY) {
         int rc = ensure_meta_keys(c);
@@ -924,6 +1041,10 @@ int render(ro_ctx *c, const ro_frame *F, const ro_state *st,
     cudaError_t e;
     if (F->mode == RO_MODE_REFERENCE) {
         e = launch<RO_MODE_REFERENCE, false>(*F, A, s);
+    } else if (F->mode == RO_MODE_PAGETABLE) {
+        e = launch<RO_MODE_PAGETABLE, false>(*F, A, s);
+    } else if (F->mode == RO_MODE_CLASSIC) {
+        e = launch<RO_MODE_CLASSIC, false>(*F, A, s);
     } else if (F->check_skips) {
         e = launch<RO_MODE_RESIDENCY, true>(*F, A, s);
     } else {

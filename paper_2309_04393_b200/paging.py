@@ -346,9 +346,16 @@ class MultiChannelPaging:
         self.slot_last_used_dev[lin] = frame
 
     def mark_empty(self, brick_id):
-        ids = self._ids_array([brick_id])
+        """paging.py:228-234: release the brick's slot if mapped, enter EMPTY."""
+        self.mark_empty_many([brick_id])
+
+    def mark_empty_many(self, brick_ids):
+        """mark_empty over an ordered id list (one launch)."""
+        ids = self._ids_array(brick_ids)
+        if len(ids) == 0:
+            return
         st = self.state(with_words=False)
-        N.check(N.lib().ro_mark_empty(self.ctx, C.byref(st), ids.ctypes.data, 1,
+        N.check(N.lib().ro_mark_empty(self.ctx, C.byref(st), ids.ctypes.data, len(ids),
                                       N.stream_ptr()))
 
     def evict_bricks(self, brick_ids, update_octree: bool = False):

@@ -1,7 +1,7 @@
 """Render entry points: the drop-in for render.py of the reference.
 
-``render_frame`` / ``render_reference`` keep the reference signatures
-(``render.py:236-250``) and return the same ``FrameOutput`` (numpy image,
+``render_frame`` / ``render_reference`` / ``render_pagetable_only`` /
+``render_classic_octree`` keep the reference signatures (``render.py:236-262``) and return the same ``FrameOutput`` (numpy image,
 ordered brick / metadata request lists, usage mask, level histogram,
 per-pixel brick switches, stats).  Underneath, one call is:
 
@@ -31,6 +31,8 @@ from .transfer import TransferFunction
 
 MODE_RESIDENCY = N.RO_MODE_RESIDENCY
 MODE_REFERENCE = N.RO_MODE_REFERENCE
+MODE_PAGETABLE = N.RO_MODE_PAGETABLE
+MODE_CLASSIC = N.RO_MODE_CLASSIC
 
 
 class RenderError(ValueError):
@@ -148,7 +150,7 @@ def choose_traversal_depth(step, max_depth) -> int:
 def _pack_frame(mode, paging: MultiChannelPaging, channels, camera: Camera,
                 config: RenderConfig, depth: int, eps_h: float,
                 reference_paging: MultiChannelPaging | None = None,
-                partition=(1, 0, 8)) -> N.Frame:
+                partition=(1, 0, 8), classic: "ClassicMetadata | None" = None) -> N.Frame:
     if not channels:
         raise RenderError("need at least one active channel")
     if len(channels) > N.RO_MAX_CH:
@@ -208,6 +210,10 @@ def _pack_frame(mode, paging: MultiChannelPaging, channels, camera: Camera,
         F.check_skips = 1
         F.ref_pt = reference_paging.pt.data_ptr()
         F.ref_cache = reference_paging.cache_dev.data_ptr()
+    if classic is not None:
+        F.cls_depth = classic.depth
+        F.cls_min = classic.min_arr.data_ptr()
+        F.cls_max = classic.max_arr.data_ptr()
     return F
 
 
@@ -263,7 +269,7 @@ class FramePass:
 
     def __init__(self, mode, paging: MultiChannelPaging, octree: ResidencyOctree | None,
                  channels, camera: Camera, config: RenderConfig, reference_paging=None,
-                 partition=(1, 0, 8), bricks_first: bool = True):
+                 partition=(1, 0, 8), bricks_first: bool = True, classic=None):
         N.require_cuda()
         if mode == MODE_RESIDENCY:
             if octree is None:
@@ -271,11 +277,20 @@ class FramePass:
             depth, eps_h = octree.config.depth, octree.config.homogeneity_eps
         else:
             depth, eps_h = 0, config.homogeneity_eps
+        if mode == MODE_CLASSIC:
+            if classic is None:
+                raise RenderError("classic mode needs ClassicMetadata")
+            cp = classic.paging
+            if (cp is not paging and (cp.config.m != paging.config.m
+                                      or not np.array_equal(cp.level_grids,
+                                                            paging.level_grids))):
+                raise RenderError("classic metadata built for another volume layout")
         self.paging = paging
         self.config = config
         self.bricks_first = bricks_first
+        self.classic = classic  # keeps the metadata buffers alive
         self.frame = _pack_frame(mode, paging, channels, camera, config, depth, eps_h,
-                                 reference_paging, partition)
+                                 reference_paging, partition, classic)
         w, h = config.image_dims
         self.local_rows = N.lib().ro_local_rows(h, *partition)
         self.buf = _buffers(paging, len(channels), self.local_rows * w,
@@ -296,13 +311,14 @@ class FramePass:
 def render_frame_device(mode, paging: MultiChannelPaging, octree: ResidencyOctree | None,
                         channels, camera: Camera, config: RenderConfig,
                         reference_paging=None, partition=(1, 0, 8),
-                        bricks_first: bool = True, collect: bool = True) -> DeviceFrame:
+                        bricks_first: bool = True, collect: bool = True,
+                        classic=None) -> DeviceFrame:
     """One ray-cast pass + feedback ordering, results left on the device.
 
     Not re-entrant per paging: the returned buffers are reused by the next
     call with the same shape."""
     fp = FramePass(mode, paging, octree, channels, camera, config, reference_paging,
-                   partition, bricks_first)
+                   partition, bricks_first, classic)
     fp.render()
     if collect:
         fp.collect()
@@ -310,10 +326,10 @@ def render_frame_device(mode, paging: MultiChannelPaging, octree: ResidencyOctre
 
 
 def _run(mode, paging, channels, camera, config, octree=None,
-         reference_paging=None) -> FrameOutput:
+         reference_paging=None, classic=None) -> FrameOutput:
     start = time.perf_counter()
     buf = render_frame_device(mode, paging, octree, channels, camera, config,
-                              reference_paging)
+                              reference_paging, classic=classic)
     m = paging.config.m
     nb, nm = buf.n_bricks, buf.n_metas
     # device -> pinned host (torch's caching host allocator recycles blocks)
@@ -367,3 +383,77 @@ def render_reference(paging: MultiChannelPaging, channels, camera: Camera,
     """In-core oracle mode (render.py:246-250): every sample translated and
     evaluated, no skipping or substitution."""
     return _run(MODE_REFERENCE, paging, channels, camera, config)
+
+
+def render_pagetable_only(paging: MultiChannelPaging, channels, camera: Camera,
+                          config: RenderConfig) -> FrameOutput:
+    """Page-table-only baseline (render.py:253-256, kernels.py:316-357):
+    desired-level translation per sample; EMPTY entries skip to their brick
+    exit, unmapped ones are requested."""
+    return _run(MODE_PAGETABLE, paging, channels, camera, config)
+
+
+def render_classic_octree(paging: MultiChannelPaging, classic: "ClassicMetadata",
+                          channels, camera: Camera, config: RenderConfig) -> FrameOutput:
+    """Classic-octree baseline (render.py:259-262, kernels.py:359-429): one
+    root-to-target descent per channel per sample over per-node min / max,
+    falling back to the deepest resident ancestor when a brick is missing."""
+    return _run(MODE_CLASSIC, paging, channels, camera, config, classic=classic)
+
+
+# ---------------------------------------------------------------------------
+# classic-octree baseline metadata
+# ---------------------------------------------------------------------------
+
+class ClassicMetadata:
+    """Per-node min / max of the classic one-node-one-brick octree
+    (render.py:271-315), kept in HBM as u8[n_nodes, m] (``min_arr`` /
+    ``max_arr``, unfilled slots = (0, 255)).
+
+    Node depth d corresponds to resolution level (depth - d); every level's
+    brick grid must be 2^(depth - level) bricks per axis, so each node owns
+    exactly one brick.  ``build_from_volume`` reduces a slot's level-0 volume
+    bottom-up on the device (exact block min / max, no dilation)."""
+
+    def __init__(self, paging: MultiChannelPaging):
+        k = paging.config.k
+        self.depth = k - 1
+        for lev in range(k):
+            g = [int(v) for v in paging.level_grids[lev]]
+            want = 1 << (self.depth - lev)
+            if not g[0] == g[1] == g[2] == want:
+                raise RenderError("classic octree needs power-of-two brick grids "
+                                  f"(level {lev} grid {tuple(g)}, expected {want}^3)")
+        if self.depth > 8:
+            raise RenderError("classic octree depth > 8 (brick coordinates are 8-bit)")
+        self.paging = paging
+        m = paging.config.m
+        n_nodes = ((1 << (3 * k)) - 1) // 7
+        dev = paging.device
+        self.min_arr = torch.zeros((n_nodes, m), dtype=torch.uint8, device=dev)
+        self.max_arr = torch.full((n_nodes, m), 255, dtype=torch.uint8, device=dev)
+        self.lvl_off = np.array([((1 << (3 * d)) - 1) // 7 for d in range(k)],
+                                dtype=np.int64)
+
+    def build_from_volume(self, slot: int, volume):
+        """Fill a slot's metadata column from its full-resolution volume
+        (z, y, x), numpy or torch."""
+        if not 0 <= slot < self.paging.config.m:
+            raise RenderError(f"channel slot {slot} out of range")
+        vol = torch.as_tensor(volume).to(self.min_arr.device)
+        g = 1 << self.depth
+        nz, ny, nx = vol.shape
+        if nz % g or ny % g or nx % g:
+            raise RenderError("volume dims must divide the leaf node grid")
+        blocks = vol.reshape(g, nz // g, g, ny // g, g, nx // g)
+        lo = torch.amin(blocks, dim=(1, 3, 5))
+        hi = torch.amax(blocks, dim=(1, 3, 5))
+        for d in range(self.depth, -1, -1):
+            off = int(self.lvl_off[d])
+            n = 1 << (3 * d)
+            self.min_arr[off:off + n, slot] = lo.reshape(-1).to(torch.uint8)
+            self.max_arr[off:off + n, slot] = hi.reshape(-1).to(torch.uint8)
+            if d:
+                h = (1 << d) // 2
+                lo = torch.amin(lo.reshape(h, 2, h, 2, h, 2), dim=(1, 3, 5))
+                hi = torch.amax(hi.reshape(h, 2, h, 2, h, 2), dim=(1, 3, 5))

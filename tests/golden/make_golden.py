@@ -2,7 +2,7 @@
 
 Run in the build container (the only place /root/reference exists):
 
-    NUMBA_CACHE_DIR=/tmp/nbcache python tests/golden/make_golden.py
+    NUMBA_CACHE_DIR=/tmp/nbcache python tests/golden/make_golden.py [names...]
 
 It imports ``resoctree`` from /root/reference/pkg/src, drives the
 reference's own Session / Engine / render_frame / render_reference on small
@@ -27,11 +27,13 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REF)
 
 from resoctree import bench, datasets  # noqa: E402
-from resoctree.camera import orbit_pose  # noqa: E402
+from resoctree.camera import orbit_path, orbit_pose  # noqa: E402
 from resoctree.engine import Engine, EngineConfig  # noqa: E402
 from resoctree.ingest import build_hierarchy  # noqa: E402
-from resoctree.render import (ChannelSettings, RenderConfig,  # noqa: E402
-                              render_frame, render_reference)
+from resoctree.render import (ChannelSettings, ClassicMetadata,  # noqa: E402
+                              RenderConfig, render_classic_octree,
+                              render_frame, render_pagetable_only,
+                              render_reference)
 from resoctree.service import DatasetStore, LocalTransport  # noqa: E402
 from resoctree.session import Session  # noqa: E402
 from resoctree.transfer import TransferFunction, grayscale_ramp_tf  # noqa: E402
@@ -287,12 +289,171 @@ def lru_replay():
     return meta, {}
 
 
+def _keep(slot, lev, x, y, z, k):
+    """Deterministic partial-residency rule of the baselines fixture: the
+    coarsest level always, otherwise 3 of 4 bricks."""
+    return lev == k - 1 or (x * 7 + y * 13 + z * 29 + lev * 3 + slot * 5) % 4 != 0
+
+
+def paging_hashes(p) -> dict:
+    return {"pt_status": h(p.pt_status), "pt_slot": h(p.pt_slot),
+            "slot_brick": h(p.slot_brick), "slot_last_used": h(p.slot_last_used),
+            "cache": h(p.cache), "free": h(np.array(p._free, dtype=np.int64))}
+
+
+def baselines_sparse256x4(tmp):
+    """The paper's three-way comparison (bench.py:98-145, acceptance criteria
+    4-5, test_acceptance.py:177-198): residency, classic-octree and
+    page-table-only renders of the trend scene (sparse 256^3 x 4 channels,
+    32^3 bricks, D=5, 96^2, step 1/128), fully resident and partially
+    resident (deterministic keep rule: requests, EMPTY entries, blocked
+    classic descents)."""
+    root = os.path.join(tmp, "sparse256x4")
+    build_hierarchy(datasets.sparse_multichannel(256, channels=4), (32, 32, 32),
+                    4, (2, 2, 2), root, name="sparse4")
+    store = DatasetStore(root)
+    k = len(store.manifest.levels)
+    tf = grayscale_ramp_tf(threshold=40.0)
+    chans = [ChannelSettings(slot=s, tf=tf) for s in range(4)]
+    slots = {s: s for s in range(4)}
+    econf = bench.full_engine_config(store, 4, depth=5)
+    rconf = RenderConfig(image_dims=(96, 96), base_step=1.0 / 128.0,
+                         max_requests_per_frame=2048, traversal_start_level=2)
+    eng = bench.prepare_engine(store, slots, econf)
+    eng_pt = bench.prepare_pagetable_engine(store, slots, econf)
+    classic = ClassicMetadata(eng.paging)
+    for s, ch in slots.items():
+        classic.build_from_volume(s, store.level_array(ch, 0))
+    # partial residency: one paging for classic, one for page-table-only
+    part = Engine(store.manifest, econf)
+    part_pt = Engine(store.manifest, econf)
+    for s, ch in slots.items():
+        for lev in range(k):
+            gx, gy, gz = (int(v) for v in part.paging.level_grids[lev])
+            for z in range(gz):
+                for y in range(gy):
+                    for x in range(gx):
+                        payload = store.brick(ch, lev, (x, y, z))
+                        bid = part.paging.encode(s, lev, (x, y, z))
+                        keep = _keep(s, lev, x, y, z, k)
+                        if keep:
+                            part.paging.insert_brick(bid, payload, 0)
+                        if payload.max() == 0:
+                            part_pt.paging.mark_empty(bid)
+                        elif keep:
+                            part_pt.paging.insert_brick(bid, payload, 0)
+    cams = orbit_path(36)
+    frames = (0, 9, 18, 27)
+    rec = {}
+    for i in frames:
+        cam = cams[i]
+        frame_record(f"res{i}_", render_frame(eng.paging, eng.octree, chans, cam,
+                                              rconf), rec)
+        frame_record(f"cls{i}_", render_classic_octree(eng.paging, classic, chans,
+                                                       cam, rconf), rec)
+        frame_record(f"pt{i}_", render_pagetable_only(eng_pt.paging, chans, cam,
+                                                      rconf), rec)
+        frame_record(f"pcls{i}_", render_classic_octree(part.paging, classic, chans,
+                                                        cam, rconf), rec)
+        frame_record(f"ppt{i}_", render_pagetable_only(part_pt.paging, chans, cam,
+                                                       rconf), rec)
+    rec["classic_min"] = classic.min_arr
+    rec["classic_max"] = classic.max_arr
+    meta = {
+        "volume": {"kind": "sparse_multichannel", "n": 256, "channels": 4,
+                   "seed": 11, "brick": [32, 32, 32], "levels": 4},
+        "pyramid_sha": pyramid_hash(store, range(4)),
+        "engine": {"depth": 5, "cache_slots": list(econf.cache_slots), "m": 4,
+                   "pad": eng.metadata_pad},
+        "state": state_hashes(eng),
+        "pagetable_state": paging_hashes(eng_pt.paging),
+        "partial_state": paging_hashes(part.paging),
+        "partial_pagetable_state": paging_hashes(part_pt.paging),
+        "render": {"image_dims": [96, 96], "base_step": 1.0 / 128.0,
+                   "budget": 2048, "start_level": 2, "t0": 1.0,
+                   "early_alpha": 0.99},
+        "channels": [{"slot": c.slot, "tf": tf_points(c.tf),
+                      "level_range": [0, 15]} for c in chans],
+        "orbit": {"num_frames": 36, "frames": list(frames)},
+    }
+    return meta, rec
+
+
+def baselines_vessel256():
+    """Baselines on the vessel volume (zero background: EMPTY page-table
+    entries and brick-exit skips in page-table-only mode, empty classic
+    nodes), fully and partially resident, m=1, D=5, 128^2, step 1/128."""
+    tmp = tempfile.mkdtemp()
+    root = os.path.join(tmp, "vessel256")
+    build_hierarchy([datasets.vessel_volume(256)], (32, 32, 32), 4, (2, 2, 2),
+                    root, name="vessel")
+    store = DatasetStore(root)
+    k = len(store.manifest.levels)
+    econf = bench.full_engine_config(store, 1, depth=5)
+    eng = bench.prepare_engine(store, {0: 0}, econf)
+    eng_pt = bench.prepare_pagetable_engine(store, {0: 0}, econf)
+    classic = ClassicMetadata(eng.paging)
+    classic.build_from_volume(0, store.level_array(0, 0))
+    part = Engine(store.manifest, econf)
+    part_pt = Engine(store.manifest, econf)
+    for lev in range(k):
+        gx, gy, gz = (int(v) for v in part.paging.level_grids[lev])
+        for z in range(gz):
+            for y in range(gy):
+                for x in range(gx):
+                    payload = store.brick(0, lev, (x, y, z))
+                    bid = part.paging.encode(0, lev, (x, y, z))
+                    keep = _keep(0, lev, x, y, z, k)
+                    if keep:
+                        part.paging.insert_brick(bid, payload, 0)
+                    if payload.max() == 0:
+                        part_pt.paging.mark_empty(bid)
+                    elif keep:
+                        part_pt.paging.insert_brick(bid, payload, 0)
+    rconf = RenderConfig(image_dims=(128, 128), base_step=1.0 / 128.0,
+                         max_requests_per_frame=512, traversal_start_level=2)
+    tf = grayscale_ramp_tf(threshold=40.0)
+    chans = [ChannelSettings(slot=0, tf=tf)]
+    angles = (0.0, 2.4, 4.1)
+    rec = {}
+    for i, a in enumerate(angles):
+        cam = orbit_pose(a)
+        frame_record(f"cls{i}_", render_classic_octree(eng.paging, classic, chans,
+                                                       cam, rconf), rec)
+        frame_record(f"pt{i}_", render_pagetable_only(eng_pt.paging, chans, cam,
+                                                      rconf), rec)
+        frame_record(f"pcls{i}_", render_classic_octree(part.paging, classic, chans,
+                                                        cam, rconf), rec)
+        frame_record(f"ppt{i}_", render_pagetable_only(part_pt.paging, chans, cam,
+                                                       rconf), rec)
+    meta = {
+        "volume": {"kind": "vessel", "n": 256, "seed": 7,
+                   "brick": [32, 32, 32], "levels": 4},
+        "engine": {"depth": 5, "cache_slots": list(econf.cache_slots), "m": 1},
+        "pagetable_state": paging_hashes(eng_pt.paging),
+        "partial_state": paging_hashes(part.paging),
+        "partial_pagetable_state": paging_hashes(part_pt.paging),
+        "empty_entries": int((eng_pt.paging.pt_status == 2).sum()),
+        "render": {"image_dims": [128, 128], "base_step": 1.0 / 128.0,
+                   "budget": 512, "start_level": 2, "t0": 1.0,
+                   "early_alpha": 0.99},
+        "channels": [{"slot": 0, "tf": tf_points(tf), "level_range": [0, 15]}],
+        "angles": list(angles),
+    }
+    return meta, rec
+
+
 def main():
     tmp = tempfile.mkdtemp()
+    only = set(sys.argv[1:])
     for name, fn in (("session_mc64", lambda: session_mc64(tmp)),
                      ("vessel256_full", vessel256_full),
                      ("skip_audit_shell64", lambda: skip_audit_shell64(tmp)),
-                     ("lru_replay", lru_replay)):
+                     ("lru_replay", lru_replay),
+                     ("baselines_sparse256x4", lambda: baselines_sparse256x4(tmp)),
+                     ("baselines_vessel256", baselines_vessel256)):
+        if only and name not in only:
+            continue
         print("generating", name, flush=True)
         meta, rec = fn()
         with open(os.path.join(HERE, name + ".json"), "w") as f:

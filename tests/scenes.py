@@ -19,6 +19,9 @@ def store(kind: str) -> V.VolumeStore:
         return V.VolumeStore([V.shell_volume(64)], (16, 16, 16), 3, (2, 2, 2))
     if kind == "vessel256":
         return V.VolumeStore([V.vessel_volume(256)], (32, 32, 32), 4, (2, 2, 2))
+    if kind == "sparse256x4":
+        return V.VolumeStore(V.sparse_multichannel(256, channels=4), (32, 32, 32), 4,
+                             (2, 2, 2))
     raise KeyError(kind)
 
 
@@ -38,6 +41,29 @@ def full_cache_slots(st, m):
     while side ** 3 < total:
         side += 1
     return (side, side, side)
+
+
+def keep_partial(slot, lev, x, y, z, k=4):
+    """Partial-residency rule of the baselines fixtures (make_golden.py
+    _keep): the coarsest level always, otherwise 3 of 4 bricks."""
+    return lev == k - 1 or (x * 7 + y * 13 + z * 29 + lev * 3 + slot * 5) % 4 != 0
+
+
+def paging_hashes(st) -> dict:
+    """make_golden.paging_hashes over an oracle state."""
+    from oracle.session import state_hashes
+    d = state_hashes(st)
+    d.pop("words")
+    return d
+
+
+def oracle_render_state(st, with_words=False):
+    from oracle import raycast as orc
+    return orc.OracleState(m=st.m, k=st.k, brick_size=st.brick_size,
+                           level_dims=st.level_dims, level_grids=st.level_grids,
+                           pt_offsets=st.pt_offsets, pt_status=st.pt_status,
+                           pt_slot=st.pt_slot, cache=st.cache,
+                           words=st.words if with_words else None, depth=st.depth)
 
 
 def tf_points(js):

@@ -433,3 +433,85 @@ def test_gpu_config3_mixed_bias_swap_session_matches_oracle():
         d = diff_hashes(device_state_hashes(sess.engine), state_hashes(ora.st))
         assert not d, (i, d)
     sess.close()
+
+
+def _baseline_engines(kind, m, meta):
+    """Product-side states of a baselines fixture (methods.py), each pinned to
+    the reference's state hashes."""
+    from paper_2309_04393_b200 import methods
+    st = scenes.store(kind)
+    slots = {s: s for s in range(m)}
+    econf = methods.full_engine_config(st, m, depth=meta["engine"]["depth"])
+    assert list(econf.cache_slots) == meta["engine"]["cache_slots"]
+    k = len(st.manifest.levels)
+    keep = lambda s, l, x, y, z: scenes.keep_partial(s, l, x, y, z, k)  # noqa: E731
+    eng = methods.prepare_engine(st, slots, econf)
+    if "state" in meta:
+        assert not diff_hashes(device_state_hashes(eng), meta["state"])
+    pt = methods.prepare_pagetable_engine(st, slots, econf)
+    assert not diff_hashes(device_state_hashes(pt.paging), meta["pagetable_state"])
+    part = methods.prepare_partial_engine(st, slots, econf, keep)
+    assert not diff_hashes(device_state_hashes(part.paging), meta["partial_state"])
+    ppt = methods.prepare_pagetable_engine(st, slots, econf, keep=keep)
+    assert not diff_hashes(device_state_hashes(ppt.paging),
+                           meta["partial_pagetable_state"])
+    classic = methods.build_classic(eng, st, slots)
+    return eng, pt, part, ppt, classic
+
+
+def test_gpu_baselines_sparse256x4_match_reference():
+    """The paper's three-way comparison (bench.py:98-145): residency,
+    classic-octree and page-table-only modes of the CUDA kernel, fully and
+    partially resident, bit-identical to the reference's outputs."""
+    from paper_2309_04393_b200 import (orbit_path, render_classic_octree, render_frame,
+                                       render_pagetable_only)
+    meta, rec = load_golden("baselines_sparse256x4")
+    eng, pt, part, ppt, classic = _baseline_engines("sparse256x4", 4, meta)
+    assert np.array_equal(classic.min_arr.cpu().numpy(), rec["classic_min"])
+    assert np.array_equal(classic.max_arr.cpu().numpy(), rec["classic_max"])
+    chans = scenes.product_channels(meta["channels"])
+    cfg = scenes.render_config(meta["render"])
+    cams = orbit_path(meta["orbit"]["num_frames"])
+    for i in meta["orbit"]["frames"]:
+        cam = cams[i]
+        outs = {"res": render_frame(eng.paging, eng.octree, chans, cam, cfg),
+                "cls": render_classic_octree(eng.paging, classic, chans, cam, cfg),
+                "pt": render_pagetable_only(pt.paging, chans, cam, cfg),
+                "pcls": render_classic_octree(part.paging, classic, chans, cam, cfg),
+                "ppt": render_pagetable_only(ppt.paging, chans, cam, cfg)}
+        for pre, out in outs.items():
+            bad = _check(rec, f"{pre}{i}_", out)
+            assert not bad, (i, pre, bad)
+
+
+def test_gpu_baselines_vessel256_match_reference():
+    """Baselines with all-zero bricks: EMPTY entries (brick-exit skips) and
+    empty classic nodes (node-exit skips), fully and partially resident."""
+    from paper_2309_04393_b200 import (orbit_pose, render_classic_octree,
+                                       render_pagetable_only)
+    meta, rec = load_golden("baselines_vessel256")
+    eng, pt, part, ppt, classic = _baseline_engines("vessel256", 1, meta)
+    chans = scenes.product_channels(meta["channels"])
+    cfg = scenes.render_config(meta["render"])
+    for i, a in enumerate(meta["angles"]):
+        cam = orbit_pose(a)
+        outs = {"cls": render_classic_octree(eng.paging, classic, chans, cam, cfg),
+                "pt": render_pagetable_only(pt.paging, chans, cam, cfg),
+                "pcls": render_classic_octree(part.paging, classic, chans, cam, cfg),
+                "ppt": render_pagetable_only(ppt.paging, chans, cam, cfg)}
+        for pre, out in outs.items():
+            bad = _check(rec, f"{pre}{i}_", out)
+            assert not bad, (i, pre, bad)
+
+
+def test_gpu_baselines_errors():
+    """ClassicMetadata / render_classic_octree validation (render.py:282-295)."""
+    from paper_2309_04393_b200 import (ClassicMetadata, Engine, EngineConfig,
+                                       RenderError)
+    from paper_2309_04393_b200.volume import VolumeManifest, plan_levels
+    man = VolumeManifest(name="t", channel_count=1, dtype_original="u8",
+                         brick_size=(16, 16, 16),
+                         levels=plan_levels((64, 48, 40), (16, 16, 16), 3, (2, 2, 2)))
+    eng = Engine(man, EngineConfig(octree_depth=3, cache_slots=(2, 2, 2), channel_slots=1))
+    with pytest.raises(RenderError):
+        ClassicMetadata(eng.paging)

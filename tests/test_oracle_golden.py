@@ -183,3 +183,97 @@ def test_oracle_row_bands_merge_to_full_frame(oracle_lib, threads):
     assert full.all_metadata_requests == par.all_metadata_requests
     assert np.array_equal(full.required_mask, par.required_mask)
     assert np.array_equal(full.counters, par.counters)
+
+
+def _baseline_states(store, m, meta):
+    """Full, page-table-only and partial states of a baselines fixture, each
+    pinned to the reference's own state hashes."""
+    from oracle.session import prepare_full, prepare_paging, state_hashes
+    from paper_2309_04393_b200.volume import box_minmax_grid
+    e = meta["engine"]
+    slots = {s: s for s in range(m)}
+    k = len(store.manifest.levels)
+    keep = lambda s, l, x, y, z: scenes.keep_partial(s, l, x, y, z, k)  # noqa: E731
+    out = {}
+    if "state" in meta:
+        full = prepare_full(store, slots, m, e["depth"], e["cache_slots"], e["pad"],
+                            box_minmax_grid)
+        assert state_hashes(full) == meta["state"]
+        out["full"] = full
+    pt = prepare_paging(store, slots, m, e["depth"], e["cache_slots"], zero_as_empty=True)
+    assert scenes.paging_hashes(pt) == meta["pagetable_state"]
+    part = prepare_paging(store, slots, m, e["depth"], e["cache_slots"], keep=keep)
+    assert scenes.paging_hashes(part) == meta["partial_state"]
+    ppt = prepare_paging(store, slots, m, e["depth"], e["cache_slots"], keep=keep,
+                         zero_as_empty=True)
+    assert scenes.paging_hashes(ppt) == meta["partial_pagetable_state"]
+    out.update(pt=pt, part=part, ppt=ppt)
+    return out
+
+
+def test_oracle_baselines_sparse256x4_match_reference(oracle_lib):
+    """The paper's three-way comparison (bench.py:98-145): residency,
+    classic-octree (kernels.py:359-429) and page-table-only (316-357) renders
+    of the trend scene, fully and partially resident, bit-identical to the
+    reference; the classic metadata pyramid equals ClassicMetadata's."""
+    from oracle import raycast as orc
+    from oracle.session import classic_metadata
+    from paper_2309_04393_b200.camera import orbit_path
+    meta, rec = load_golden("baselines_sparse256x4")
+    store = scenes.store("sparse256x4")
+    assert scenes.pyramid_sha(store, range(4)) == meta["pyramid_sha"]
+    sts = _baseline_states(store, 4, meta)
+    k = len(store.manifest.levels)
+    cls = classic_metadata({s: store.level_array(s, 0) for s in range(4)}, 4, k)
+    assert np.array_equal(cls[0], rec["classic_min"])
+    assert np.array_equal(cls[1], rec["classic_max"])
+    chans = scenes.oracle_channels(meta["channels"])
+    kw = scenes.render_kw(meta["render"])
+    cams = orbit_path(meta["orbit"]["num_frames"])
+    runs = (("res", "full", orc.MODE_RESIDENCY), ("cls", "full", orc.MODE_CLASSIC),
+            ("pt", "pt", orc.MODE_PAGETABLE), ("pcls", "part", orc.MODE_CLASSIC),
+            ("ppt", "ppt", orc.MODE_PAGETABLE))
+    for i in meta["orbit"]["frames"]:
+        c = cams[i]
+        cam = (c.position, c.target, c.up, c.fov_deg)
+        for pre, which, mode in runs:
+            st = scenes.oracle_render_state(sts[which], with_words=(mode == orc.MODE_RESIDENCY))
+            out = orc.render(st, chans, cam, mode=mode, threads=4, classic=cls, **kw)
+            bad = scenes.check_frame(rec, f"{pre}{i}_", out.image, out.brick_requests,
+                                     out.metadata_requests, out.required_mask,
+                                     out.level_histogram, out.pixel_required, out.counters)
+            assert not bad, (i, pre, bad)
+
+
+def test_oracle_baselines_vessel256_match_reference(oracle_lib):
+    """Baselines on a volume with all-zero bricks: EMPTY page-table entries
+    skip to their brick exit, empty classic nodes skip to their node exit."""
+    from oracle import raycast as orc
+    from oracle.session import classic_metadata, prepare_paging
+    from paper_2309_04393_b200.camera import orbit_pose
+    meta, rec = load_golden("baselines_vessel256")
+    store = scenes.store("vessel256")
+    sts = _baseline_states(store, 1, meta)
+    assert int((sts["pt"].pt_status == 2).sum()) == meta["empty_entries"] > 0
+    k = len(store.manifest.levels)
+    cls = classic_metadata({0: store.level_array(0, 0)}, 1, k)
+    e = meta["engine"]  # classic renders use a fully resident paging
+    full = prepare_paging(store, {0: 0}, 1, e["depth"], e["cache_slots"])
+    chans = scenes.oracle_channels(meta["channels"])
+    kw = scenes.render_kw(meta["render"])
+    runs = (("cls", full, orc.MODE_CLASSIC), ("pt", sts["pt"], orc.MODE_PAGETABLE),
+            ("pcls", sts["part"], orc.MODE_CLASSIC), ("ppt", sts["ppt"], orc.MODE_PAGETABLE))
+    skipped = 0
+    for i, a in enumerate(meta["angles"]):
+        p = orbit_pose(a)
+        cam = (p.position, p.target, p.up, p.fov_deg)
+        for pre, st, mode in runs:
+            out = orc.render(scenes.oracle_render_state(st), chans, cam, mode=mode,
+                             threads=4, classic=cls, **kw)
+            bad = scenes.check_frame(rec, f"{pre}{i}_", out.image, out.brick_requests,
+                                     out.metadata_requests, out.required_mask,
+                                     out.level_histogram, out.pixel_required, out.counters)
+            assert not bad, (i, pre, bad)
+            if mode == orc.MODE_PAGETABLE:
+                skipped += int(out.counters[2])
+    assert skipped > 0  # the EMPTY brick-exit skip was exercised
