@@ -349,7 +349,10 @@ def run_ours(args):
             e2e = {"value": 1.0 / e2e_s, "unit": "frames/s",
                    "h2d_bytes_per_step": ctypes.sizeof(N.Frame),
                    "d2h_bytes_per_step": int(d2h),
-                   "note": "render_frame(): kernel params in, numpy image/mask/requests out"}
+                   "note": ("render_frame(): frame params in; image + per-pixel counts stored by "
+                             "the kernel into pinned host memory over PCIe (zero-copy), "
+                             "usage mask / histogram / counters / requests copied after; "
+                             "numpy outputs")}
         # ---- kernel launches in one step (profiler, untimed) ----
         launches = None
         try:

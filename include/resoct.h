@@ -134,6 +134,10 @@ typedef struct ro_frame {
     ro_channel ch[RO_MAX_CH];
 } ro_frame;
 
+/* image and pix_required may be device memory or pinned host memory
+   (cudaHostAlloc / cudaHostRegister, UVA-mapped): the ray caster then
+   stores the frame straight over PCIe while it runs (zero-copy readback).
+   Pageable host memory is rejected. */
 typedef struct ro_outputs {
     float *image;          /* [local_rows*width*4] f32 RGBA */
     uint8_t *required;     /* [E] usage mask (zeroed by ro_render) */

@@ -1016,14 +1016,27 @@ int render(ro_ctx *c, const ro_frame *F, const ro_state *st,
         if (c->layout.m == 4 && (reinterpret_cast<uintptr_t>(st->words) & 15))
             return fail(RO_EINVAL, "octree words must be 16-byte aligned");
     }
+    // device views of the two per-pixel outputs (pinned host memory is
+    // written through its UVA mapping)
+    void *dev_out[2] = {out->image, out->pix_required};
+    for (void *&p : dev_out) {
+        cudaPointerAttributes pa;
+        if (p == nullptr) return fail(RO_EINVAL, "null image / pix_required output");
+        if (cudaPointerGetAttributes(&pa, p) != cudaSuccess ||
+            pa.type == cudaMemoryTypeUnregistered || pa.devicePointer == nullptr) {
+            cudaGetLastError();
+            return fail(RO_EINVAL, "image / pix_required must be device or pinned host memory");
+        }
+        p = pa.devicePointer;
+    }
     RayArgs A;
     A.L = c->dl;
     A.words = st->words;
     A.pt = st->pt;
     A.cache = st->cache;
-    A.image = out->image;
+    A.image = static_cast<float *>(dev_out[0]);
     A.required = out->required;
-    A.pix_required = out->pix_required;
+    A.pix_required = static_cast<int32_t *>(dev_out[1]);
     A.hist = reinterpret_cast<unsigned long long *>(out->hist);
     A.counters = reinterpret_cast<unsigned long long *>(out->counters);
     A.brick_key = c->brick_key;

@@ -16,6 +16,7 @@ Session uses it so the usage mask feeds ``note_sampled`` on the device.
 from __future__ import annotations
 
 import ctypes as C
+import functools
 import math
 import time
 from dataclasses import dataclass, field
@@ -147,6 +148,25 @@ def choose_traversal_depth(step, max_depth) -> int:
     return traversal_depth(step, max_depth)
 
 
+@functools.lru_cache(maxsize=256)
+def _channel_block(slot: int, lo: int, hi: int, tf: TransferFunction) -> N.Channel:
+    """ro_channel of one visible channel (render.py:101-122 packing), built
+    once per (slot, level range, transfer function)."""
+    ch = N.Channel()
+    ch.slot, ch.lo, ch.hi = slot, lo, hi
+    ch.npoints = len(tf.points)
+    xs = np.zeros(N.RO_MAX_TF_POINTS, dtype=np.float64)
+    rgba = np.zeros((N.RO_MAX_TF_POINTS, 4), dtype=np.float64)
+    for j, (x, c) in enumerate(tf.points):
+        xs[j] = float(x)
+        rgba[j] = [float(v) for v in c]
+    C.memmove(ch.tf_x, xs.ctypes.data, xs.nbytes)
+    C.memmove(ch.tf_rgba, rgba.ctypes.data, rgba.nbytes)
+    eb = np.ascontiguousarray(tf.empty_below(), dtype=np.uint16)
+    C.memmove(ch.empty_below, eb.ctypes.data, eb.nbytes)
+    return ch
+
+
 def _pack_frame(mode, paging: MultiChannelPaging, channels, camera: Camera,
                 config: RenderConfig, depth: int, eps_h: float,
                 reference_paging: MultiChannelPaging | None = None,
@@ -183,19 +203,9 @@ def _pack_frame(mode, paging: MultiChannelPaging, channels, camera: Camera,
         hi = max(0, min(c.level_range[1], k - 1))
         los.append(lo)
         his.append(hi)
-        ch = F.ch[i]
-        ch.slot, ch.lo, ch.hi = c.slot, lo, hi
-        pts = c.tf.points
-        if len(pts) > N.RO_MAX_TF_POINTS:
+        if len(c.tf.points) > N.RO_MAX_TF_POINTS:
             raise RenderError(f"transfer function with > {N.RO_MAX_TF_POINTS} points")
-        ch.npoints = len(pts)
-        for j, (x, rgba) in enumerate(pts):
-            ch.tf_x[j] = float(x)
-            for q in range(4):
-                ch.tf_rgba[j][q] = float(rgba[q])
-        eb = c.tf.empty_below()
-        for j in range(256):
-            ch.empty_below[j] = int(eb[j])
+        F.ch[i] = _channel_block(c.slot, lo, hi, c.tf)
     for raw in range(N.RO_MAX_LEVELS):
         maxlev = 0
         for lo, hi in zip(los, his):
@@ -297,9 +307,10 @@ class FramePass:
                             config.max_requests_per_frame)
         self.state = paging.state(with_words=(mode == MODE_RESIDENCY))
 
-    def render(self):
+    def render(self, outputs: N.Outputs | None = None):
+        out = outputs if outputs is not None else self.buf.outputs
         N.check(N.lib().ro_render(self.paging.ctx, C.byref(self.frame), C.byref(self.state),
-                                  C.byref(self.buf.outputs), N.stream_ptr()))
+                                  C.byref(out), N.stream_ptr()))
 
     def collect(self):
         N.check(N.lib().ro_feedback_collect(self.paging.ctx,
@@ -325,28 +336,54 @@ def render_frame_device(mode, paging: MultiChannelPaging, octree: ResidencyOctre
     return fp.buf
 
 
+_COPY_STREAMS = {}
+
+
+def _copy_stream(device) -> torch.cuda.Stream:
+    s = _COPY_STREAMS.get(device)
+    if s is None:
+        s = _COPY_STREAMS[device] = torch.cuda.Stream(device=device)
+    return s
+
+
 def _run(mode, paging, channels, camera, config, octree=None,
          reference_paging=None, classic=None) -> FrameOutput:
     start = time.perf_counter()
-    buf = render_frame_device(mode, paging, octree, channels, camera, config,
-                              reference_paging, classic=classic)
-    m = paging.config.m
-    nb, nm = buf.n_bricks, buf.n_metas
-    # device -> pinned host (torch's caching host allocator recycles blocks)
+    fp = FramePass(mode, paging, octree, channels, camera, config, reference_paging,
+                   classic=classic)
+    buf = fp.buf
+    # Zero-copy image: the ray caster stores each pixel's RGBA and brick
+    # count straight into pinned host memory (UVA-mapped), so the 20 B/pixel
+    # device->host transfer rides PCIe while the kernel runs instead of
+    # after it.  Usage mask, histogram and counters stay in HBM (scattered
+    # writes / atomics) and are copied once the kernel is done.
     pin = dict(pin_memory=True)
     img = torch.empty(buf.image.shape, dtype=torch.float32, **pin)
-    req = torch.empty(buf.required.shape, dtype=torch.uint8, **pin)
     pixr = torch.empty(buf.pix_required.shape, dtype=torch.int32, **pin)
-    small = torch.empty(buf.hist.numel() + N.RO_NUM_COUNTERS + 4 * buf.fb.shape[1],
-                        dtype=torch.int64, **pin)
-    img.copy_(buf.image, non_blocking=True)
-    req.copy_(buf.required, non_blocking=True)
-    pixr.copy_(buf.pix_required, non_blocking=True)
+    req = torch.empty(buf.required.shape, dtype=torch.uint8, **pin)
     nh = buf.hist.numel()
-    small[:nh].copy_(buf.hist.reshape(-1), non_blocking=True)
-    small[nh:nh + N.RO_NUM_COUNTERS].copy_(buf.counters, non_blocking=True)
+    small = torch.empty(nh + N.RO_NUM_COUNTERS + 4 * buf.fb.shape[1], dtype=torch.int64,
+                        **pin)
+    fp.render(N.Outputs(img.data_ptr(), buf.required.data_ptr(), pixr.data_ptr(),
+                        buf.hist.data_ptr(), buf.counters.data_ptr()))
+    # the usage mask / histogram / counters are final once the ray caster
+    # ends: copy them on a side stream while request ordering (kernel 3a)
+    # runs on the main stream
+    main = torch.cuda.current_stream()
+    side = _copy_stream(main.device)
+    done = torch.cuda.Event()
+    done.record(main)
+    with torch.cuda.stream(side):
+        side.wait_event(done)
+        req.copy_(buf.required, non_blocking=True)
+        small[:nh].copy_(buf.hist.reshape(-1), non_blocking=True)
+        small[nh:nh + N.RO_NUM_COUNTERS].copy_(buf.counters, non_blocking=True)
+    fp.collect()  # synchronises the main stream (the kernel's host stores included)
+    m = paging.config.m
+    nb, nm = buf.n_bricks, buf.n_metas
     small[nh + N.RO_NUM_COUNTERS:].copy_(buf.fb.reshape(-1), non_blocking=True)
-    torch.cuda.current_stream().synchronize()
+    main.synchronize()
+    side.synchronize()
     elapsed_ms = (time.perf_counter() - start) * 1000.0
     sm = small.numpy()
     hist = sm[:nh].reshape(buf.hist.shape).copy()
