@@ -37,6 +37,15 @@
 #ifndef RO_PERSISTENT
 #define RO_PERSISTENT 1
 #endif
+#ifndef RO_WARPS
+#define RO_WARPS 4
+#endif
+#ifndef RO_TILE_W
+#define RO_TILE_W 16
+#endif
+#ifndef RO_TILE_H
+#define RO_TILE_H 8
+#endif
 #ifndef RO_SUBCACHE
 #define RO_SUBCACHE 0
 #endif
@@ -56,9 +65,12 @@ namespace ro {
 
 namespace {
 
-constexpr int kBlock = 128;  // 4 warps, 16x8 pixels
-constexpr int kTileW = 16;
-constexpr int kTileH = 8;
+constexpr int kWarps = RO_WARPS;
+constexpr int kBlock = 32 * kWarps;  // default 4 warps on a 16x8 pixel tile
+constexpr int kTileW = RO_TILE_W;
+constexpr int kTileH = RO_TILE_H;
+constexpr int kPPT = (kTileW / 8) * (kTileH / 4);  // 8x4 packets per tile
+static_assert(kTileW % 8 == 0 && kTileH % 4 == 0 && kPPT % kWarps == 0, "tile shape");
 constexpr int kFastDepth = 6;  // longest channel-0 descent handled in parallel
 constexpr double kClampHi = 1.0 - 1e-9;
 constexpr double kTwo52 = 4503599627370496.0;
@@ -341,7 +353,7 @@ struct SampleCtx {
 };
 
 template <int MODE, bool CHECK, int BX, int BY>
-__global__ void __launch_bounds__(kBlock, RO_MINB)
+__global__ void __launch_bounds__(kBlock, RO_MINB * 4 / kWarps)
 k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A) {
     __shared__ FrameSmem S;
     extern __shared__ int32_t dyn[];  // per-thread channel state
@@ -419,7 +431,8 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
     int32_t *last_mreq = last_breq + n_ch * kBlock;   // n_ch
     uint32_t *hist_t = reinterpret_cast<uint32_t *>(last_mreq + n_ch * kBlock);
     for (int i = 0; i < n_ch * k; ++i) hist_t[i * kBlock + tid] = 0;
-    const int lane = tid & 31, warp = tid >> 5;
+    const int lane = tid & 31;
+    [[maybe_unused]] const int warp = tid >> 5;
     const int tiles_x = (F.width + kTileW - 1) / kTileW;
     // per-thread work counters (32-bit: a thread's share stays far below 2^32)
     uint32_t c_steps = 0, c_eval = 0, c_skip = 0, c_viol = 0, c_live = 0;
@@ -440,6 +453,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
     {
     const int tile = blockIdx.x;
 #endif
+    for (int wsub = warp; wsub < kPPT; wsub += kWarps) {
     for (int i = 0; i < n_ch; ++i) {
         prev_brick[i * kBlock + tid] = -1;
         last_breq[i * kBlock + tid] = -1;
@@ -447,8 +461,8 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
     }
 
     // ---- pixel of this thread: warp = 8x4 packet ----
-    const int x = (tile % tiles_x) * kTileW + (warp & 1) * 8 + (lane & 7);
-    const int ly = (tile / tiles_x) * kTileH + (warp >> 1) * 4 + (lane >> 3);
+    const int x = (tile % tiles_x) * kTileW + (wsub % (kTileW / 8)) * 8 + (lane & 7);
+    const int ly = (tile / tiles_x) * kTileH + (wsub / (kTileW / 8)) * 4 + (lane >> 3);
     const int tr = F.tile_rows;
     const int gy = ((ly / tr) * F.n_parts + F.part) * tr + (ly % tr);
     const bool active = x < F.width && ly < A.local_rows && gy < F.height;
@@ -913,6 +927,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
         reinterpret_cast<float4 *>(A.image)[lpix] = px4;
         A.pix_required[lpix] = pixreq;
     }
+    }  // packets of the tile
     }  // tile loop
 
     // ---- block reductions ----
