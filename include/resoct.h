@@ -30,6 +30,12 @@
  *                        for a list of changed bricks (incremental pass)
  *   ro_rebuild_masks     octree.py:355-395  masks from the resident set
  *                        (ground truth + OR closure), for verification
+ *   ro_apply_bricks_lz4  service.py:225-232 fetch + ingest.py:114-117
+ *                        decompress_brick + Engine.apply_brick: LZ4 frames
+ *                        decoded on the GPU into the cache
+ *   ro_lz4_decode        lz4io.py:69-110 decompress (batched, device)
+ *   ro_normalize_to_u8 / ro_downsample_box / ro_extract_bricks
+ *                        ingest.py:27-95 (device pyramid + bricks)
  *
  * Errors: every call returns 0 on success or a negative RO_E* code; the
  * message is available from ro_last_error() (thread-local).  Asynchronous
@@ -187,6 +193,50 @@ int ro_apply_bricks(ro_ctx *ctx, const ro_state *state, const int64_t *ids,
                     int64_t n, const void *payloads, int32_t payload_on_device,
                     int64_t frame, int32_t update_octree, int32_t *slots_out,
                     int64_t *evicted_out, void *stream);
+
+/* ---- brick ingest on the GPU ----
+   Bricks travel as standard LZ4 frames (lz4io.py:1-110 over liblz4 1.9.4's
+   frame API; ingest.py:114-117 decompress_brick, called by every fetch:
+   service.py:71-76, 225-232). */
+
+/* ro_apply_bricks with LZ4-framed payloads: frame i is
+   frames[frame_offsets[i] - frame_offsets[0] .. frame_offsets[i+1] - frame_offsets[0]).
+   ids / frame_offsets: HOST arrays (n and n+1); frames on the host
+   (frames_on_device=0, then indexed from frames + frame_offsets[0]) or the
+   device.  Frames are decoded on the device by one warp each straight into
+   brick payloads and inserted in order; if any frame is corrupt or does not
+   decode to exactly one brick, nothing is inserted and RO_EINVAL names the
+   first bad one.  Synchronises the stream. */
+int ro_apply_bricks_lz4(ro_ctx *ctx, const ro_state *state, const int64_t *ids,
+                        int64_t n, const uint8_t *frames,
+                        const int64_t *frame_offsets, int32_t frames_on_device,
+                        int64_t frame, int32_t update_octree, int32_t *slots_out,
+                        int64_t *evicted_out, void *stream);
+
+/* Batched LZ4 frame decode, all DEVICE arrays: frame i = src[off[i]-off[0] ..
+   off[i+1]-off[0]) -> dst + i*dst_stride (at most dst_stride bytes).
+   status[i] = 0, or <0: -1 not an LZ4 frame, -2 bad descriptor / header
+   checksum, -3 block too large, -4 truncated, -5 corrupt block, -6 size
+   differs from expected_size (<0: any size), -7 checksum mismatch, -8
+   trailing bytes.  Asynchronous. */
+int ro_lz4_decode(ro_ctx *ctx, const uint8_t *src, const int64_t *src_offsets,
+                  int64_t n, uint8_t *dst, int64_t dst_stride,
+                  int64_t expected_size, int32_t *status, void *stream);
+
+/* ingest.py:27-35 normalize_to_u8 over n device elements of dtype 1 u8,
+   2 u16, 3 u32, 4 f32 (min -> 0, max -> 255, round half up). */
+int ro_normalize_to_u8(ro_ctx *ctx, const void *src, int32_t dtype, int64_t n,
+                       uint8_t *dst, void *stream);
+/* ingest.py:38-61 downsample_box of a device level [dz][dy][dx], factors in
+   {1, 2}, odd extents edge-replicated: dst [ceil(dz/fz)][ceil(dy/fy)][ceil(dx/fx)]. */
+int ro_downsample_box(const uint8_t *src, int32_t dx, int32_t dy, int32_t dz,
+                      int32_t fx, int32_t fy, int32_t fz, uint8_t *dst,
+                      void *stream);
+/* ingest.py:75-95 extract_brick for every brick of a device level, in
+   (z, y, x) grid order: dst [gz*gy*gx][bz][by][bx], edge-replicated. */
+int ro_extract_bricks(const uint8_t *level, int32_t dx, int32_t dy, int32_t dz,
+                      int32_t bx, int32_t by, int32_t bz, uint8_t *dst,
+                      void *stream);
 
 int ro_evict_bricks(ro_ctx *ctx, const ro_state *state, const int64_t *ids,
                     int64_t n, int32_t update_octree, void *stream);

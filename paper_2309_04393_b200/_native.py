@@ -105,6 +105,12 @@ _SIGS = {
     "ro_octree_update": ([_p, C.POINTER(State), _p, _i64, _p], _i32),
     "ro_rebuild_masks": ([_p, C.POINTER(State), _p], _i32),
     "ro_sync": ([_p, _p], _i32),
+    "ro_apply_bricks_lz4": ([_p, C.POINTER(State), _p, _i64, _p, _p, _i32, _i64, _i32, _p,
+                             _p, _p], _i32),
+    "ro_lz4_decode": ([_p, _p, _p, _i64, _p, _i64, _i64, _p, _p], _i32),
+    "ro_normalize_to_u8": ([_p, _p, _i32, _i64, _p, _p], _i32),
+    "ro_downsample_box": ([_p, _i32, _i32, _i32, _i32, _i32, _i32, _p, _p], _i32),
+    "ro_extract_bricks": ([_p, _i32, _i32, _i32, _i32, _i32, _i32, _p, _p], _i32),
 }
 
 EXPORTED = tuple(_SIGS)

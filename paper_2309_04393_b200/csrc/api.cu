@@ -66,6 +66,20 @@ int rebuild_masks(ro_ctx *c, const ro_state *st, cudaStream_t s);
 int octree_update_host(ro_ctx *c, const ro_state *st, const int64_t *ids_h, int64_t n,
                        cudaStream_t s);
 
+int lz4_decode(ro_ctx *c, const uint8_t *src, const int64_t *off, int64_t n, uint8_t *dst,
+               int64_t stride, int64_t expected, int32_t *status, int32_t *first_bad,
+               cudaStream_t s);
+int apply_bricks_lz4(ro_ctx *c, const ro_state *st, const int64_t *ids_h, int64_t n,
+                     const uint8_t *frames, const int64_t *off_h, int32_t on_device,
+                     int64_t frame, int32_t update_octree, int32_t *slots_out,
+                     int64_t *evicted_out, cudaStream_t s);
+int normalize_to_u8(ro_ctx *c, const void *src, int32_t dtype, int64_t n, uint8_t *dst,
+                    cudaStream_t s);
+int downsample_box(const uint8_t *src, int32_t dx, int32_t dy, int32_t dz, int32_t fx,
+                   int32_t fy, int32_t fz, uint8_t *dst, cudaStream_t s);
+int extract_bricks(const uint8_t *level, int32_t dx, int32_t dy, int32_t dz, int32_t bx,
+                   int32_t by, int32_t bz, uint8_t *dst, cudaStream_t s);
+
 static int check_state(const ro_ctx *c, const ro_state *st) {
     if (!c) return fail(RO_EINVAL, "null context");
     if (!st || !st->pt || !st->slot_brick || !st->slot_last_used || !st->free_stack ||
@@ -222,6 +236,46 @@ int ro_apply_bricks(ro_ctx *c, const ro_state *st, const int64_t *ids, int64_t n
     if (payloads && !st->cache) return fail(RO_EINVAL, "null cache");
     return apply_bricks(c, st, ids, n, payloads, payload_on_device, frame, update_octree,
                         slots_out, evicted_out, (cudaStream_t)stream);
+}
+
+int ro_apply_bricks_lz4(ro_ctx *c, const ro_state *st, const int64_t *ids, int64_t n,
+                        const uint8_t *frames, const int64_t *frame_offsets,
+                        int32_t frames_on_device, int64_t frame, int32_t update_octree,
+                        int32_t *slots_out, int64_t *evicted_out, void *stream) {
+    int rc = check_state(c, st);
+    if (rc) return rc;
+    if (!st->cache) return fail(RO_EINVAL, "null cache");
+    return apply_bricks_lz4(c, st, ids, n, frames, frame_offsets, frames_on_device, frame,
+                            update_octree, slots_out, evicted_out, (cudaStream_t)stream);
+}
+
+int ro_lz4_decode(ro_ctx *c, const uint8_t *src, const int64_t *src_offsets, int64_t n,
+                  uint8_t *dst, int64_t dst_stride, int64_t expected_size, int32_t *status,
+                  void *stream) {
+    if (!c) return fail(RO_EINVAL, "null context");
+    if (n > 0 && (!src || !src_offsets || !dst || !status)) return fail(RO_EINVAL, "null array");
+    if (dst_stride < 1) return fail(RO_EINVAL, "dst_stride must be >= 1");
+    return lz4_decode(c, src, src_offsets, n, dst, dst_stride, expected_size, status, nullptr,
+                      (cudaStream_t)stream);
+}
+
+int ro_normalize_to_u8(ro_ctx *c, const void *src, int32_t dtype, int64_t n, uint8_t *dst,
+                       void *stream) {
+    if (!c) return fail(RO_EINVAL, "null context");
+    if (n > 0 && (!src || !dst)) return fail(RO_EINVAL, "null array");
+    return normalize_to_u8(c, src, dtype, n, dst, (cudaStream_t)stream);
+}
+
+int ro_downsample_box(const uint8_t *src, int32_t dx, int32_t dy, int32_t dz, int32_t fx,
+                      int32_t fy, int32_t fz, uint8_t *dst, void *stream) {
+    if (!src || !dst) return fail(RO_EINVAL, "null array");
+    return downsample_box(src, dx, dy, dz, fx, fy, fz, dst, (cudaStream_t)stream);
+}
+
+int ro_extract_bricks(const uint8_t *level, int32_t dx, int32_t dy, int32_t dz, int32_t bx,
+                      int32_t by, int32_t bz, uint8_t *dst, void *stream) {
+    if (!level || !dst) return fail(RO_EINVAL, "null array");
+    return extract_bricks(level, dx, dy, dz, bx, by, bz, dst, (cudaStream_t)stream);
 }
 
 int ro_evict_bricks(ro_ctx *c, const ro_state *st, const int64_t *ids, int64_t n,

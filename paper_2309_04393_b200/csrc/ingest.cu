@@ -1,0 +1,473 @@
+// ingest.cu -- brick ingest into the cache on the GPU.
+//
+//  * LZ4 frame decode.  Bricks travel as standard LZ4 frames
+//    (/root/reference/pkg/src/resoctree/lz4io.py:1-110, the system liblz4
+//    1.9.4 frame API: LZ4F_compressFrame / LZ4F_decompress), decoded on the
+//    host by ingest.py:114-117 (decompress_brick) after every fetch
+//    (service.py:71-76, 225-232).  Here the compressed frames are uploaded
+//    and decoded by one warp per frame straight into device memory, then
+//    inserted by the batched LRU path (ro_apply_bricks_lz4): the PCIe bytes
+//    shrink by the compression ratio and no CPU core decompresses.
+//    The decoder follows the published LZ4 frame / block format: magic,
+//    FLG/BD descriptor with its xxHash32 header checksum, linked or
+//    independent blocks up to the declared maximum size, raw (stored) blocks,
+//    optional block / content checksums (xxHash32) and content size.
+//  * range normalisation to u8 (ingest.py:27-35), 2x box downsampling
+//    (ingest.py:38-61) and brick cutting with edge replication
+//    (ingest.py:75-95), for building pyramids of device-resident volumes.
+//    The reference computes these in fp64; the results are exact small
+//    binary fractions, so the integer forms below are bit-identical.
+#include <algorithm>
+#include <vector>
+
+#include "internal.cuh"
+
+namespace ro {
+
+int apply_bricks(ro_ctx *c, const ro_state *st, const int64_t *ids_h, int64_t n,
+                 const void *payloads, int32_t on_device, int64_t frame,
+                 int32_t update_octree, int32_t *slots_out, int64_t *evicted_out,
+                 cudaStream_t s);
+
+namespace {
+
+constexpr int kLz4Warps = 4;  // warps (frames) per CTA
+
+enum : int32_t {
+    LZ4_OK = 0,
+    LZ4_E_MAGIC = -1,      // not an LZ4 frame (or a skippable / legacy one)
+    LZ4_E_HEADER = -2,     // bad descriptor or header checksum
+    LZ4_E_BLOCKSIZE = -3,  // block larger than the declared maximum
+    LZ4_E_TRUNCATED = -4,  // input ends inside the frame
+    LZ4_E_CORRUPT = -5,    // malformed block (bad offset / overrun)
+    LZ4_E_SIZE = -6,       // decoded size differs from the expected one
+    LZ4_E_CHECKSUM = -7,   // block or content checksum mismatch
+    LZ4_E_TRAILING = -8,   // bytes after the end of the frame
+};
+
+__device__ __forceinline__ uint32_t rd32(const uint8_t *p) {
+    return (uint32_t)p[0] | ((uint32_t)p[1] << 8) | ((uint32_t)p[2] << 16) |
+           ((uint32_t)p[3] << 24);
+}
+
+__device__ __forceinline__ uint32_t rotl32(uint32_t x, int r) {
+    return (x << r) | (x >> (32 - r));
+}
+
+// xxHash32 (the frame format's checksum), computed identically by every lane
+__device__ uint32_t xxh32(const uint8_t *p, int64_t len, uint32_t seed) {
+    const uint32_t P1 = 2654435761u, P2 = 2246822519u, P3 = 3266489917u,
+                   P4 = 668265263u, P5 = 374761393u;
+    int64_t i = 0;
+    uint32_t h;
+    if (len >= 16) {
+        uint32_t v1 = seed + P1 + P2, v2 = seed + P2, v3 = seed, v4 = seed - P1;
+        for (; i + 16 <= len; i += 16) {
+            v1 = rotl32(v1 + rd32(p + i) * P2, 13) * P1;
+            v2 = rotl32(v2 + rd32(p + i + 4) * P2, 13) * P1;
+            v3 = rotl32(v3 + rd32(p + i + 8) * P2, 13) * P1;
+            v4 = rotl32(v4 + rd32(p + i + 12) * P2, 13) * P1;
+        }
+        h = rotl32(v1, 1) + rotl32(v2, 7) + rotl32(v3, 12) + rotl32(v4, 18);
+    } else {
+        h = seed + P5;
+    }
+    h += (uint32_t)len;
+    for (; i + 4 <= len; i += 4) h = rotl32(h + rd32(p + i) * P3, 17) * P4;
+    for (; i < len; ++i) h = rotl32(h + p[i] * P5, 11) * P1;
+    h ^= h >> 15;
+    h *= P2;
+    h ^= h >> 13;
+    h *= P3;
+    h ^= h >> 16;
+    return h;
+}
+
+// One LZ4 block into dst[op, limit); matches may reach back to `low`.
+// Every lane parses the same bytes (broadcast loads), so control flow stays
+// warp-uniform; lanes split literal and match copies.  An overlapping match
+// (offset < length) repeats the last `offset` bytes, so output byte j of the
+// match is dst[op - off + j % off]: every lane reads only bytes that are
+// already final and no intra-match synchronisation is needed.
+__device__ int32_t lz4_block_warp(const uint8_t *__restrict__ b, int64_t bl, uint8_t *dst,
+                                  int64_t &op, int64_t low, int64_t limit, int lane) {
+    int64_t ip = 0;
+    while (true) {
+        if (ip >= bl) return LZ4_E_CORRUPT;
+        const uint32_t token = b[ip++];
+        int64_t lit = token >> 4;
+        if (lit == 15) {
+            uint32_t s;
+            do {
+                if (ip >= bl) return LZ4_E_CORRUPT;
+                s = b[ip++];
+                lit += s;
+            } while (s == 255);
+        }
+        if (ip + lit > bl || op + lit > limit) return LZ4_E_CORRUPT;
+        for (int64_t i = lane; i < lit; i += 32) dst[op + i] = b[ip + i];
+        ip += lit;
+        op += lit;
+        if (ip == bl) return LZ4_OK;  // the last sequence holds literals only
+        if (ip + 2 > bl) return LZ4_E_CORRUPT;
+        const int64_t off = (int64_t)b[ip] | ((int64_t)b[ip + 1] << 8);
+        ip += 2;
+        int64_t ml = token & 15;
+        if (ml == 15) {
+            uint32_t s;
+            do {
+                if (ip >= bl) return LZ4_E_CORRUPT;
+                s = b[ip++];
+                ml += s;
+            } while (s == 255);
+        }
+        ml += 4;
+        if (off == 0 || off > op - low || op + ml > limit) return LZ4_E_CORRUPT;
+        __syncwarp();  // literals of this / earlier sequences visible to all lanes
+        const int64_t base = op - off;
+        if (off >= ml) {
+            for (int64_t j = lane; j < ml; j += 32) dst[op + j] = dst[base + j];
+        } else {
+            for (int64_t j = lane; j < ml; j += 32) dst[op + j] = dst[base + j % off];
+        }
+        op += ml;
+        __syncwarp();
+    }
+}
+
+// One frame -> dst[0, cap); returns the decoded size or an LZ4_E_* code.
+__device__ int64_t lz4_frame_warp(const uint8_t *__restrict__ src, int64_t len, uint8_t *dst,
+                                  int64_t cap, int lane) {
+    if (len < 7) return LZ4_E_TRUNCATED;
+    if (rd32(src) != 0x184D2204u) return LZ4_E_MAGIC;
+    const uint32_t flg = src[4], bd = src[5];
+    if ((flg >> 6) != 1 || (flg & 0x02) || (bd & 0x8F)) return LZ4_E_HEADER;
+    const int bsid = (bd >> 4) & 7;
+    if (bsid < 4) return LZ4_E_HEADER;
+    const int64_t bmax = (int64_t)1 << (8 + 2 * bsid);  // 64 KB .. 4 MB
+    const bool indep = flg & 0x20, bchk = flg & 0x10, has_size = flg & 0x08,
+               cchk = flg & 0x04, has_dict = flg & 0x01;
+    int64_t pos = 6;
+    int64_t csize = -1;
+    if (has_size) {
+        if (len < pos + 8) return LZ4_E_TRUNCATED;
+        csize = (int64_t)rd32(src + pos) | ((int64_t)rd32(src + pos + 4) << 32);
+        pos += 8;
+    }
+    if (has_dict) pos += 4;
+    if (len < pos + 1) return LZ4_E_TRUNCATED;
+    if (((xxh32(src + 4, pos - 4, 0) >> 8) & 0xFF) != src[pos]) return LZ4_E_HEADER;
+    pos += 1;
+    int64_t op = 0;
+    while (true) {
+        if (pos + 4 > len) return LZ4_E_TRUNCATED;
+        const uint32_t bs = rd32(src + pos);
+        pos += 4;
+        if (bs == 0) break;  // EndMark
+        const bool raw = bs >> 31;
+        const int64_t bl = bs & 0x7FFFFFFFu;
+        if (bl > bmax) return LZ4_E_BLOCKSIZE;
+        if (pos + bl + (bchk ? 4 : 0) > len) return LZ4_E_TRUNCATED;
+        if (bchk && xxh32(src + pos, bl, 0) != rd32(src + pos + bl)) return LZ4_E_CHECKSUM;
+        const int64_t start = op;
+        const int64_t limit = min(cap, op + bmax);
+        if (raw) {
+            if (op + bl > limit) return LZ4_E_SIZE;
+            for (int64_t i = lane; i < bl; i += 32) dst[op + i] = src[pos + i];
+            op += bl;
+        } else {
+            const int32_t rc = lz4_block_warp(src + pos, bl, dst, op, indep ? start : 0,
+                                              limit, lane);
+            if (rc != LZ4_OK) return rc == LZ4_E_CORRUPT && op >= limit ? LZ4_E_SIZE : rc;
+        }
+        __syncwarp();
+        pos += bl + (bchk ? 4 : 0);
+    }
+    if (cchk) {
+        if (pos + 4 > len) return LZ4_E_TRUNCATED;
+        if (xxh32(dst, op, 0) != rd32(src + pos)) return LZ4_E_CHECKSUM;
+        pos += 4;
+    }
+    if (has_size && op != csize) return LZ4_E_SIZE;
+    if (pos != len) return LZ4_E_TRAILING;
+    return op;
+}
+
+__global__ void __launch_bounds__(32 * kLz4Warps)
+k_lz4_decode(int64_t n, const uint8_t *__restrict__ src, const int64_t *__restrict__ off,
+             uint8_t *__restrict__ dst, int64_t stride, int64_t expected,
+             int32_t *__restrict__ status, int32_t *__restrict__ first_bad) {
+    const int lane = threadIdx.x & 31;
+    const int64_t i = (int64_t)blockIdx.x * kLz4Warps + (threadIdx.x >> 5);
+    if (i >= n) return;
+    const int64_t o0 = off[0];
+    const int64_t a = off[i] - o0, b = off[i + 1] - o0;
+    int64_t r = (b < a) ? LZ4_E_TRUNCATED
+                        : lz4_frame_warp(src + a, b - a, dst + i * stride, stride, lane);
+    if (r >= 0 && expected >= 0 && r != expected) r = LZ4_E_SIZE;
+    if (lane == 0) {
+        status[i] = r < 0 ? (int32_t)r : 0;
+        if (r < 0 && first_bad) atomicMin(first_bad, (int32_t)i);
+    }
+}
+
+// ---- normalisation (ingest.py:27-35) ----------------------------------------
+
+template <typename T> struct OrderedKey;
+template <> struct OrderedKey<uint8_t> {
+    static __device__ uint32_t of(uint8_t v) { return v; }
+    static __device__ double val(uint32_t k) { return (double)k; }
+};
+template <> struct OrderedKey<uint16_t> {
+    static __device__ uint32_t of(uint16_t v) { return v; }
+    static __device__ double val(uint32_t k) { return (double)k; }
+};
+template <> struct OrderedKey<uint32_t> {
+    static __device__ uint32_t of(uint32_t v) { return v; }
+    static __device__ double val(uint32_t k) { return (double)k; }
+};
+template <> struct OrderedKey<float> {  // total order of finite floats
+    static __device__ uint32_t of(float v) {
+        const uint32_t u = __float_as_uint(v);
+        return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+    }
+    static __device__ double val(uint32_t k) {
+        const uint32_t u = (k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k;
+        return (double)__uint_as_float(u);
+    }
+};
+
+template <typename T>
+__global__ void k_minmax(int64_t n, const T *__restrict__ src, uint32_t *__restrict__ mm) {
+    uint32_t lo = 0xFFFFFFFFu, hi = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t k = OrderedKey<T>::of(src[i]);
+        lo = min(lo, k);
+        hi = max(hi, k);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(mm, lo);
+        atomicMax(mm + 1, hi);
+    }
+}
+
+template <typename T>
+__global__ void k_normalize(int64_t n, const T *__restrict__ src,
+                            const uint32_t *__restrict__ mm, uint8_t *__restrict__ dst) {
+    const double lo = OrderedKey<T>::val(mm[0]), hi = OrderedKey<T>::val(mm[1]);
+    const bool flat = hi == lo;
+    const double scale = flat ? 0.0 : 255.0 / (hi - lo);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        uint8_t out = 0;
+        if (!flat) {
+            // numpy: floor((data - lo) * (255 / (hi - lo)) + 0.5).clip(0, 255)
+            const double v = floor(((double)src[i] - lo) * scale + 0.5);
+            out = (uint8_t)(v < 0.0 ? 0.0 : (v > 255.0 ? 255.0 : v));
+        }
+        dst[i] = out;
+    }
+}
+
+// ---- 2x box downsampling (ingest.py:38-61) ------------------------------------
+// Each averaged axis halves exactly in fp64, so the reference's value is
+// sum / 2^f and floor(sum / 2^f + 0.5) == (sum + 2^(f-1)) >> f.
+__global__ void k_downsample_box(const uint8_t *__restrict__ src, int dx, int dy, int dz,
+                                 int fx, int fy, int fz, int ox, int oy, int oz,
+                                 uint8_t *__restrict__ dst) {
+    const int64_t total = (int64_t)ox * oy * oz;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int x = (int)(i % ox), y = (int)((i / ox) % oy), z = (int)(i / ((int64_t)ox * oy));
+        int sum = 0;
+        for (int c = 0; c < fz; ++c) {
+            const int zz = min(z * fz + c, dz - 1);
+            for (int b = 0; b < fy; ++b) {
+                const int yy = min(y * fy + b, dy - 1);
+                for (int a = 0; a < fx; ++a) {
+                    const int xx = min(x * fx + a, dx - 1);
+                    sum += src[((int64_t)zz * dy + yy) * dx + xx];
+                }
+            }
+        }
+        const int f = (fx == 2) + (fy == 2) + (fz == 2);
+        dst[i] = (uint8_t)(f ? (sum + (1 << (f - 1))) >> f : sum);
+    }
+}
+
+// ---- brick cutting with edge replication (ingest.py:75-95) --------------------
+// All bricks of one level in (z, y, x) grid order, 16 bytes per thread.
+__global__ void k_extract_bricks(const uint8_t *__restrict__ level, int dx, int dy, int dz,
+                                 int bx, int by, int bz, int gx, int gy, int64_t n_bricks,
+                                 uint8_t *__restrict__ dst) {
+    const int64_t bvox = (int64_t)bx * by * bz;
+    const int64_t total = n_bricks * bvox;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t br = i / bvox, v = i % bvox;
+        const int cx = (int)(br % gx), cy = (int)((br / gx) % gy), cz = (int)(br / ((int64_t)gx * gy));
+        const int x = (int)(v % bx), y = (int)((v / bx) % by), z = (int)(v / ((int64_t)bx * by));
+        const int xx = min(cx * bx + x, dx - 1), yy = min(cy * by + y, dy - 1),
+                  zz = min(cz * bz + z, dz - 1);
+        dst[i] = level[((int64_t)zz * dy + yy) * dx + xx];
+    }
+}
+
+unsigned grid_for(int64_t n, int threads = 256) {
+    int64_t b = (n + threads - 1) / threads;
+    if (b > 148 * 32) b = 148 * 32;
+    return (unsigned)(b < 1 ? 1 : b);
+}
+
+const char *lz4_reason(int32_t code) {
+    switch (code) {
+        case LZ4_E_MAGIC: return "not an LZ4 frame";
+        case LZ4_E_HEADER: return "bad frame descriptor or header checksum";
+        case LZ4_E_BLOCKSIZE: return "block larger than the declared maximum";
+        case LZ4_E_TRUNCATED: return "truncated LZ4 frame";
+        case LZ4_E_CORRUPT: return "corrupt LZ4 block";
+        case LZ4_E_SIZE: return "decompressed size differs from the brick size";
+        case LZ4_E_CHECKSUM: return "LZ4 checksum mismatch";
+        case LZ4_E_TRAILING: return "trailing bytes after LZ4 frame";
+        default: return "LZ4 decode error";
+    }
+}
+
+}  // namespace
+
+int lz4_decode(ro_ctx *c, const uint8_t *src, const int64_t *off, int64_t n, uint8_t *dst,
+               int64_t stride, int64_t expected, int32_t *status, int32_t *first_bad,
+               cudaStream_t s) {
+    (void)c;
+    if (n <= 0) return RO_OK;
+    const int64_t blocks = (n + kLz4Warps - 1) / kLz4Warps;
+    k_lz4_decode<<<(unsigned)blocks, 32 * kLz4Warps, 0, s>>>(n, src, off, dst, stride, expected,
+                                                            status, first_bad);
+    RO_CUDA(cudaGetLastError());
+    return RO_OK;
+}
+
+// Upload n LZ4 frames, decode them into brick payloads on the device and
+// insert them with the batched LRU (apply_bricks).  Nothing is inserted if a
+// frame is corrupt (the reference raises before apply_brick:
+// service.py:225-232).
+int apply_bricks_lz4(ro_ctx *c, const ro_state *st, const int64_t *ids_h, int64_t n,
+                     const uint8_t *frames, const int64_t *off_h, int32_t on_device,
+                     int64_t frame, int32_t update_octree, int32_t *slots_out,
+                     int64_t *evicted_out, cudaStream_t s) {
+    if (n <= 0) return RO_OK;
+    if (!ids_h || !frames || !off_h) return fail(RO_EINVAL, "null ids / frames / offsets");
+    const int64_t bytes = off_h[n] - off_h[0];
+    for (int64_t i = 0; i < n; ++i)
+        if (off_h[i + 1] < off_h[i]) return fail(RO_EINVAL, "frame offsets not monotone");
+    int rc;
+    void *p_frames, *p_off, *p_payload;
+    if ((rc = scratch(c, 5, (size_t)bytes + 16, &p_frames))) return rc;
+    if ((rc = scratch(c, 6, sizeof(int64_t) * (n + 1) + sizeof(int32_t) * (n + 1) + 64, &p_off)))
+        return rc;
+    if ((rc = scratch(c, 2, (size_t)c->bvox * n, &p_payload))) return rc;
+    int64_t *d_off = (int64_t *)p_off;
+    int32_t *d_status = (int32_t *)(d_off + n + 1);
+    int32_t *d_first = d_status + n;
+    const uint8_t *d_frames;
+    if (on_device) {
+        d_frames = frames;  // frame i at frames + (off[i] - off[0])
+    } else {
+        if (c->staging_bytes < (size_t)bytes) {
+            if (c->staging) cudaFreeHost(c->staging);
+            c->staging = nullptr;
+            c->staging_bytes = 0;
+            RO_CUDA(cudaMallocHost(&c->staging, (size_t)bytes));
+            c->staging_bytes = (size_t)bytes;
+        }
+        RO_CUDA(cudaEventSynchronize(c->upload_done));  // staging free again
+        memcpy(c->staging, frames + off_h[0], (size_t)bytes);
+        RO_CUDA(cudaMemcpyAsync(p_frames, c->staging, (size_t)bytes, cudaMemcpyHostToDevice, s));
+        RO_CUDA(cudaEventRecord(c->upload_done, s));
+        d_frames = (const uint8_t *)p_frames;
+    }
+    RO_CUDA(cudaMemcpyAsync(d_off, off_h, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, s));
+    const int32_t big = 0x7FFFFFFF;
+    RO_CUDA(cudaMemcpyAsync(d_first, &big, sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    if ((rc = lz4_decode(c, d_frames, d_off, n, (uint8_t *)p_payload, c->bvox, c->bvox,
+                         d_status, d_first, s)))
+        return rc;
+    int32_t *h = reinterpret_cast<int32_t *>(c->pinned_small);
+    RO_CUDA(cudaMemcpyAsync(h + 8, d_first, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    RO_CUDA(cudaStreamSynchronize(s));
+    if (h[8] != big) {
+        int32_t code = 0;
+        cudaMemcpy(&code, d_status + h[8], sizeof(int32_t), cudaMemcpyDeviceToHost);
+        char msg[160];
+        snprintf(msg, sizeof msg, "brick %d of the batch (id %lld): %s", h[8],
+                 (long long)ids_h[h[8]], lz4_reason(code));
+        return fail(RO_EINVAL, msg);
+    }
+    return apply_bricks(c, st, ids_h, n, p_payload, 1, frame, update_octree, slots_out,
+                        evicted_out, s);
+}
+
+int normalize_to_u8(ro_ctx *c, const void *src, int32_t dtype, int64_t n, uint8_t *dst,
+                    cudaStream_t s) {
+    if (n <= 0) return RO_OK;
+    void *p;
+    int rc;
+    if ((rc = scratch(c, 7, 64, &p))) return rc;
+    uint32_t *mm = (uint32_t *)p;
+    const uint32_t init[2] = {0xFFFFFFFFu, 0u};
+    RO_CUDA(cudaMemcpyAsync(mm, init, sizeof init, cudaMemcpyHostToDevice, s));
+    const unsigned g = grid_for(n);
+    switch (dtype) {
+        case 1:
+            k_minmax<<<g, 256, 0, s>>>(n, (const uint8_t *)src, mm);
+            k_normalize<<<g, 256, 0, s>>>(n, (const uint8_t *)src, mm, dst);
+            break;
+        case 2:
+            k_minmax<<<g, 256, 0, s>>>(n, (const uint16_t *)src, mm);
+            k_normalize<<<g, 256, 0, s>>>(n, (const uint16_t *)src, mm, dst);
+            break;
+        case 3:
+            k_minmax<<<g, 256, 0, s>>>(n, (const uint32_t *)src, mm);
+            k_normalize<<<g, 256, 0, s>>>(n, (const uint32_t *)src, mm, dst);
+            break;
+        case 4:
+            k_minmax<<<g, 256, 0, s>>>(n, (const float *)src, mm);
+            k_normalize<<<g, 256, 0, s>>>(n, (const float *)src, mm, dst);
+            break;
+        default:
+            return fail(RO_EINVAL, "dtype must be 1 (u8), 2 (u16), 3 (u32) or 4 (f32)");
+    }
+    RO_CUDA(cudaGetLastError());
+    return RO_OK;
+}
+
+int downsample_box(const uint8_t *src, int32_t dx, int32_t dy, int32_t dz, int32_t fx,
+                   int32_t fy, int32_t fz, uint8_t *dst, cudaStream_t s) {
+    for (int f : {fx, fy, fz})
+        if (f != 1 && f != 2) return fail(RO_EINVAL, "downsample factors must be 1 or 2");
+    if (dx < 1 || dy < 1 || dz < 1) return fail(RO_EINVAL, "empty level");
+    const int ox = (dx + fx - 1) / fx, oy = (dy + fy - 1) / fy, oz = (dz + fz - 1) / fz;
+    k_downsample_box<<<grid_for((int64_t)ox * oy * oz), 256, 0, s>>>(src, dx, dy, dz, fx, fy, fz,
+                                                                     ox, oy, oz, dst);
+    RO_CUDA(cudaGetLastError());
+    return RO_OK;
+}
+
+int extract_bricks(const uint8_t *level, int32_t dx, int32_t dy, int32_t dz, int32_t bx,
+                   int32_t by, int32_t bz, uint8_t *dst, cudaStream_t s) {
+    if (dx < 1 || dy < 1 || dz < 1 || bx < 1 || by < 1 || bz < 1)
+        return fail(RO_EINVAL, "empty level or brick");
+    const int gx = (dx + bx - 1) / bx, gy = (dy + by - 1) / by, gz = (dz + bz - 1) / bz;
+    const int64_t nb = (int64_t)gx * gy * gz;
+    k_extract_bricks<<<grid_for(nb * bx * by * bz), 256, 0, s>>>(level, dx, dy, dz, bx, by, bz,
+                                                                 gx, gy, nb, dst);
+    RO_CUDA(cudaGetLastError());
+    return RO_OK;
+}
+
+}  // namespace ro

@@ -281,10 +281,22 @@ class MultiChannelPaging:
     # -- mutation -----------------------------------------------------------
 
     def _ids_array(self, brick_ids) -> np.ndarray:
+        """Validate a list of brick ids (vectorised decode_brick_id +
+        _entry_index range checks); raises PagingError on the first bad one."""
         ids = np.ascontiguousarray(np.asarray(brick_ids, dtype=np.int64).reshape(-1))
-        for b in ids:
-            slot, level, coord = self.decode(int(b))
-            self._entry_index(slot, level, coord)
+        if len(ids) == 0:
+            return ids
+        k, m = self.config.k, self.config.m
+        pt = (ids >> 24) & 0xFF
+        slot, level = pt // k, pt % k
+        xyz = np.stack([ids & 0xFF, (ids >> 8) & 0xFF, (ids >> 16) & 0xFF], axis=1)
+        grids = np.asarray(self.level_grids, dtype=np.int64)[np.minimum(level, k - 1)]
+        ok = (ids >= 0) & (ids < (1 << 32)) & (slot < m) & (xyz < grids).all(axis=1)
+        if not ok.all():
+            b = int(ids[int(np.flatnonzero(~ok)[0])])
+            slot_b, level_b, coord_b = self.decode(b)
+            self._entry_index(slot_b, level_b, coord_b)  # raises with the reason
+            raise PagingError(f"bad brick id {b:#x}")
         return ids
 
     def _payload_arg(self, payloads, n):
@@ -326,6 +338,38 @@ class MultiChannelPaging:
             slots.ctypes.data if return_slots else None,
             evicted.ctypes.data if return_slots else None, N.stream_ptr()))
         del keep
+        return (slots, evicted) if return_slots else None
+
+    def insert_bricks_lz4(self, brick_ids, frames, frame: int, update_octree: bool = False,
+                          return_slots: bool = True):
+        """insert_bricks with LZ4-framed payloads (the wire format,
+        ingest.py:114-117), decoded on the GPU into the cache.  ``frames``:
+        list of bytes or (uint8 buffer, int64 offsets[n+1]); a torch CUDA
+        buffer is decoded in place.  Nothing is inserted if a frame is bad."""
+        from .ingest import pack_frames
+        ids = self._ids_array(brick_ids)
+        n = len(ids)
+        if n == 0:
+            return (np.zeros(0, np.int32), np.zeros(0, np.int64)) if return_slots else None
+        buf, offs = frames if isinstance(frames, tuple) else pack_frames(list(frames))
+        offs = np.ascontiguousarray(offs, dtype=np.int64)
+        if len(offs) != n + 1:
+            raise PagingError(f"{len(offs) - 1} frames for {n} bricks")
+        on_dev = isinstance(buf, torch.Tensor) and buf.is_cuda
+        if isinstance(buf, torch.Tensor) and not on_dev:
+            buf = buf.numpy()
+        if not on_dev:
+            buf = np.ascontiguousarray(buf, dtype=np.uint8)
+        # host frames are indexed from frames + offs[0]
+        ptr = buf.data_ptr() if on_dev else buf.ctypes.data
+        slots = np.zeros(n, dtype=np.int32) if return_slots else None
+        evicted = np.zeros(n, dtype=np.int64) if return_slots else None
+        st = self.state(with_words=update_octree)
+        N.check(N.lib().ro_apply_bricks_lz4(
+            self.ctx, C.byref(st), ids.ctypes.data, n, ptr, offs.ctypes.data,
+            1 if on_dev else 0, int(frame), 1 if update_octree else 0,
+            slots.ctypes.data if return_slots else None,
+            evicted.ctypes.data if return_slots else None, N.stream_ptr()))
         return (slots, evicted) if return_slots else None
 
     def insert_brick(self, brick_id, payload, frame):

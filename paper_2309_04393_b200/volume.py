@@ -185,6 +185,17 @@ class VolumeStore:
         self._check(c, l, coord)
         return extract_brick(self.pyramids[c][l], coord, self.manifest.brick_size)
 
+    def brick_bytes(self, c, l, coord) -> bytes:
+        """The brick as one LZ4 frame (service.py:63-69: the stored / served
+        form), compressed once with liblz4 and cached."""
+        from .ingest import compress_brick
+        key = (c, l, tuple(coord))
+        cache = self.__dict__.setdefault("_frames", {})
+        data = cache.get(key)
+        if data is None:
+            data = cache[key] = compress_brick(self.brick(c, l, coord))
+        return data
+
     def level_array(self, c, l) -> np.ndarray:
         self._check(c, l)
         return self.pyramids[c][l]
@@ -215,6 +226,10 @@ class LocalTransport:
 
     def fetch_brick(self, c, l, coord):
         return self.store.brick(c, l, coord)
+
+    def fetch_brick_bytes(self, c, l, coord) -> bytes:
+        """The LZ4 frame the server would send (service.py:130-136)."""
+        return self.store.brick_bytes(c, l, coord)
 
     def fetch_metadata(self, c, l, box):
         return self.store.region_min_max(c, l, box)

@@ -443,6 +443,32 @@ def baselines_vessel256():
     return meta, rec
 
 
+def lz4_frames():
+    """Wire-format fixtures: bricks compressed by the reference's own
+    compress_brick (ingest.py:110-111 -> lz4io.compress -> liblz4
+    LZ4F_compressFrame) and the sha256 of what its decompress_brick returns:
+    vessel bricks, an all-zero brick, an incompressible (raw-block) brick and
+    a 64^3 brick spanning four 64 KB blocks."""
+    from resoctree.ingest import compress_brick, decompress_brick, extract_brick
+    vol = datasets.vessel_volume(128)
+    rng = np.random.default_rng(3)
+    bricks = [("vessel", (32, 32, 32), extract_brick(vol, c, (32, 32, 32)))
+              for c in ((0, 0, 0), (1, 2, 1), (2, 1, 2), (3, 3, 3))]
+    bricks.append(("zero", (32, 32, 32), np.zeros((32, 32, 32), np.uint8)))
+    bricks.append(("random", (32, 32, 32),
+                   rng.integers(0, 256, size=(32, 32, 32), dtype=np.uint8)))
+    bricks.append(("vessel64", (64, 64, 64), extract_brick(vol, (1, 0, 1), (64, 64, 64))))
+    rec, items = {}, []
+    for i, (kind, size, payload) in enumerate(bricks):
+        frame = compress_brick(payload)
+        back = decompress_brick(frame, size)
+        assert np.array_equal(back, payload)
+        rec[f"frame{i}"] = np.frombuffer(frame, dtype=np.uint8)
+        items.append({"kind": kind, "brick": list(size), "bytes": len(frame),
+                      "payload_sha": h(back)})
+    return {"items": items, "volume": {"kind": "vessel", "n": 128, "seed": 7}}, rec
+
+
 def main():
     tmp = tempfile.mkdtemp()
     only = set(sys.argv[1:])
@@ -451,7 +477,8 @@ def main():
                      ("skip_audit_shell64", lambda: skip_audit_shell64(tmp)),
                      ("lru_replay", lru_replay),
                      ("baselines_sparse256x4", lambda: baselines_sparse256x4(tmp)),
-                     ("baselines_vessel256", baselines_vessel256)):
+                     ("baselines_vessel256", baselines_vessel256),
+                     ("lz4_frames", lz4_frames)):
         if only and name not in only:
             continue
         print("generating", name, flush=True)
