@@ -36,6 +36,9 @@
  *   ro_lz4_decode        lz4io.py:69-110 decompress (batched, device)
  *   ro_normalize_to_u8 / ro_downsample_box / ro_extract_bricks
  *                        ingest.py:27-95 (device pyramid + bricks)
+ *   ro_node_minmax       service.py:102-115 region_min_max / engine.py:186-219
+ *                        _box_minmax_grid (one tree level, device volume)
+ *   ro_fill_metadata     engine.py:138-152 fill_metadata_from_volumes
  *
  * Errors: every call returns 0 on success or a negative RO_E* code; the
  * message is available from ro_last_error() (thread-local).  Asynchronous
@@ -237,6 +240,23 @@ int ro_downsample_box(const uint8_t *src, int32_t dx, int32_t dy, int32_t dz,
 int ro_extract_bricks(const uint8_t *level, int32_t dx, int32_t dy, int32_t dz,
                       int32_t bx, int32_t by, int32_t bz, uint8_t *dst,
                       void *stream);
+
+/* ---- culling metadata producer on the GPU ---- */
+
+/* Min / max of a device level-0 volume [dz][dy][dx] over every depth-d node
+   extent dilated by `pad` voxels (engine.py:109-127 metadata_box; the
+   per-request service.py:102-115 region_min_max and the per-level
+   engine.py:186-219 _box_minmax_grid compute the same numbers): mins / maxs
+   [8^d] in (z, y, x) node order; windows empty on an axis give (0, 0).
+   Asynchronous. */
+int ro_node_minmax(ro_ctx *ctx, const uint8_t *volume, int32_t dx, int32_t dy,
+                   int32_t dz, int32_t d, int32_t pad, uint8_t *mins,
+                   uint8_t *maxs, void *stream);
+/* engine.py:138-152 fill_metadata_from_volumes for one slot: every tree
+   level's min / max written into the octree words (mask bits kept). */
+int ro_fill_metadata(ro_ctx *ctx, const ro_state *state, int32_t slot,
+                     const uint8_t *volume, int32_t dx, int32_t dy, int32_t dz,
+                     int32_t pad, void *stream);
 
 int ro_evict_bricks(ro_ctx *ctx, const ro_state *state, const int64_t *ids,
                     int64_t n, int32_t update_octree, void *stream);

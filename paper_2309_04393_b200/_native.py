@@ -111,6 +111,8 @@ _SIGS = {
     "ro_normalize_to_u8": ([_p, _p, _i32, _i64, _p, _p], _i32),
     "ro_downsample_box": ([_p, _i32, _i32, _i32, _i32, _i32, _i32, _p, _p], _i32),
     "ro_extract_bricks": ([_p, _i32, _i32, _i32, _i32, _i32, _i32, _p, _p], _i32),
+    "ro_node_minmax": ([_p, _p, _i32, _i32, _i32, _i32, _i32, _p, _p, _p], _i32),
+    "ro_fill_metadata": ([_p, C.POINTER(State), _i32, _p, _i32, _i32, _i32, _i32, _p], _i32),
 }
 
 EXPORTED = tuple(_SIGS)

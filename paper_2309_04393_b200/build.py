@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 LIB = os.path.join(HERE, "libresoct.so")
-SOURCES = ["raycast.cu", "feedback.cu", "residency.cu", "ingest.cu", "api.cu"]
+SOURCES = ["raycast.cu", "feedback.cu", "residency.cu", "ingest.cu", "metadata.cu", "api.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -80,6 +80,11 @@ int downsample_box(const uint8_t *src, int32_t dx, int32_t dy, int32_t dz, int32
 int extract_bricks(const uint8_t *level, int32_t dx, int32_t dy, int32_t dz, int32_t bx,
                    int32_t by, int32_t bz, uint8_t *dst, cudaStream_t s);
 
+int node_minmax(ro_ctx *c, const uint8_t *vol, int32_t dx, int32_t dy, int32_t dz, int32_t d,
+                int32_t pad, uint8_t *mins, uint8_t *maxs, cudaStream_t s);
+int fill_metadata(ro_ctx *c, const ro_state *st, int32_t slot, const uint8_t *vol, int32_t dx,
+                  int32_t dy, int32_t dz, int32_t pad, cudaStream_t s);
+
 static int check_state(const ro_ctx *c, const ro_state *st) {
     if (!c) return fail(RO_EINVAL, "null context");
     if (!st || !st->pt || !st->slot_brick || !st->slot_last_used || !st->free_stack ||
@@ -190,7 +195,7 @@ int ro_destroy(ro_ctx *c) {
     cudaFree(c->meta_touched);
     cudaFree(c->touched_n);
     cudaFree(c->claim);
-    for (int i = 0; i < 8; ++i) cudaFree(c->scratch[i]);
+    for (int i = 0; i < 12; ++i) cudaFree(c->scratch[i]);
     if (c->pinned_small) cudaFreeHost(c->pinned_small);
     if (c->staging) cudaFreeHost(c->staging);
     if (c->upload) cudaStreamDestroy(c->upload);
@@ -276,6 +281,23 @@ int ro_extract_bricks(const uint8_t *level, int32_t dx, int32_t dy, int32_t dz, 
                       int32_t by, int32_t bz, uint8_t *dst, void *stream) {
     if (!level || !dst) return fail(RO_EINVAL, "null array");
     return extract_bricks(level, dx, dy, dz, bx, by, bz, dst, (cudaStream_t)stream);
+}
+
+int ro_node_minmax(ro_ctx *c, const uint8_t *volume, int32_t dx, int32_t dy, int32_t dz,
+                   int32_t d, int32_t pad, uint8_t *mins, uint8_t *maxs, void *stream) {
+    if (!c) return fail(RO_EINVAL, "null context");
+    return node_minmax(c, volume, dx, dy, dz, d, pad, mins, maxs, (cudaStream_t)stream);
+}
+
+int ro_fill_metadata(ro_ctx *c, const ro_state *st, int32_t slot, const uint8_t *volume,
+                     int32_t dx, int32_t dy, int32_t dz, int32_t pad, void *stream) {
+    int rc = check_state(c, st);
+    if (rc) return rc;
+    if (!volume) return fail(RO_EINVAL, "null volume");
+    if (dx != c->layout.level_dims[0][0] || dy != c->layout.level_dims[0][1] ||
+        dz != c->layout.level_dims[0][2])
+        return fail(RO_EINVAL, "volume dims differ from level 0 of the layout");
+    return fill_metadata(c, st, slot, volume, dx, dy, dz, pad, (cudaStream_t)stream);
 }
 
 int ro_evict_bricks(ro_ctx *c, const ro_state *st, const int64_t *ids, int64_t n,

@@ -172,8 +172,8 @@ struct ro_ctx {
     int64_t *pinned_small = nullptr;          // host pinned scratch [64]
 
     // generic grow-only device scratch
-    void *scratch[8] = {nullptr};
-    size_t scratch_bytes[8] = {0};
+    void *scratch[12] = {nullptr};
+    size_t scratch_bytes[12] = {0};
     // pinned host staging for payload uploads
     void *staging = nullptr;
     size_t staging_bytes = 0;

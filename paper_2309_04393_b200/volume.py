@@ -227,6 +227,18 @@ class LocalTransport:
     def fetch_brick(self, c, l, coord):
         return self.store.brick(c, l, coord)
 
+    def metadata_pyramid(self, c, depth, pad):
+        """Every node's region_min_max over its dilated box (service.py:102-115
+        for all nodes at once), reduced on the GPU from the level-0 volume
+        (metadata.MetadataPyramid); cached per (channel, depth, pad)."""
+        from .metadata import MetadataPyramid
+        cache = self.__dict__.setdefault("_pyramids", {})
+        key = (c, depth, pad)
+        pyr = cache.get(key)
+        if pyr is None:
+            pyr = cache[key] = MetadataPyramid(self.store.level_array(c, 0), depth, pad)
+        return pyr
+
     def fetch_brick_bytes(self, c, l, coord) -> bytes:
         """The LZ4 frame the server would send (service.py:130-136)."""
         return self.store.brick_bytes(c, l, coord)
