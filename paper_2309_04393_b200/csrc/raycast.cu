@@ -37,6 +37,9 @@
 #ifndef RO_PERSISTENT
 #define RO_PERSISTENT 1
 #endif
+#ifndef RO_NCH_FAST
+#define RO_NCH_FAST 0
+#endif
 #ifndef RO_WARPS
 #define RO_WARPS 4
 #endif
@@ -352,13 +355,13 @@ struct SampleCtx {
     int tp2_lev;
 };
 
-template <int MODE, bool CHECK, int BX, int BY>
+template <int MODE, bool CHECK, int BX, int BY, int NCH>
 __global__ void __launch_bounds__(kBlock, RO_MINB * 4 / kWarps)
 k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A) {
     __shared__ FrameSmem S;
     extern __shared__ int32_t dyn[];  // per-thread channel state
     const int tid = threadIdx.x;
-    const int n_ch = F.n_ch;
+    const int n_ch = NCH > 0 ? NCH : F.n_ch;  // NCH: compile-time channel count
     const int k = A.L.k;
     const int m = A.L.m;
 
@@ -592,7 +595,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                 // up to the exit of their brick box
                 bool all_empty = true;
                 skip_exit = 1e30;
-#pragma unroll 1
+#pragma unroll(NCH > 0 ? NCH : 1)
                 for (int ci = 0; ci < n_ch; ++ci) {
                     const int lev = clampi(raw, S.lo[ci], S.hi[ci]);
                     if (sc.lp.lev != lev) level_pos(sc.lp, lev, px, py, pz, S, lbx, lby, lbz);
@@ -631,7 +634,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                 const int qx = (int)(px * cside), qy = (int)(py * cside), qz = (int)(pz * cside);
                 bool all_empty = true;
                 int deep_d = -1, dix = 0, diy = 0, diz = 0;
-#pragma unroll 1
+#pragma unroll(NCH > 0 ? NCH : 1)
                 for (int ci = 0; ci < n_ch; ++ci) {
                     const int slot = S.slot[ci];
                     const int lev = clampi(raw, S.lo[ci], S.hi[ci]);
@@ -682,7 +685,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                                          (dix + 1) * s, (diy + 1) * s, (diz + 1) * s);
                 }
             } else if (MODE == RO_MODE_REFERENCE) {  // kernels.py:301-314
-#pragma unroll 1
+#pragma unroll(NCH > 0 ? NCH : 1)
                 for (int ci = 0; ci < n_ch; ++ci) {
                     const int lev = clampi(raw, S.lo[ci], S.hi[ci]);
                     if (sc.lp.lev != lev) level_pos(sc.lp, lev, px, py, pz, S, lbx, lby, lbz);
@@ -739,7 +742,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                     d = d0 + stop;
                 }
 #endif
-#pragma unroll 1
+#pragma unroll(NCH > 0 ? NCH : 1)
                 for (int ci = 0; ci < n_ch; ++ci) {
                     const int slot = S.slot[ci];
                     while (true) {
@@ -948,7 +951,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
     }
 }
 
-template <int MODE, bool CHECK, int BX, int BY>
+template <int MODE, bool CHECK, int BX, int BY, int NCH = 0>
 cudaError_t launch_b(const ro_frame &F, const RayArgs &A, cudaStream_t s) {
     int n_tiles = ((F.width + kTileW - 1) / kTileW) * ((A.local_rows + kTileH - 1) / kTileH);
     static int sm_count = 0;
@@ -958,7 +961,7 @@ cudaError_t launch_b(const ro_frame &F, const RayArgs &A, cudaStream_t s) {
         cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev);
     }
     size_t dyn = (size_t)F.n_ch * kBlock * 4 * 3 + (size_t)F.n_ch * A.L.k * kBlock * 4;
-    auto kern = k_raycast<MODE, CHECK, BX, BY>;
+    auto kern = k_raycast<MODE, CHECK, BX, BY, NCH>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)dyn);
     if (e != cudaSuccess) return e;
@@ -979,6 +982,11 @@ cudaError_t launch_b(const ro_frame &F, const RayArgs &A, cudaStream_t s) {
 // brick sizes with compile-time tap offsets; anything else uses runtime ones
 template <int MODE, bool CHECK>
 cudaError_t launch(const ro_frame &F, const RayArgs &A, cudaStream_t s) {
+#if RO_NCH_FAST
+    if (MODE == RO_MODE_RESIDENCY && !CHECK && F.n_ch == RO_NCH_FAST && A.L.bx == 32 &&
+        A.L.by == 32)
+        return launch_b<MODE, CHECK, 32, 32, RO_NCH_FAST>(F, A, s);
+#endif
     if (A.L.bx == 32 && A.L.by == 32) return launch_b<MODE, CHECK, 32, 32>(F, A, s);
     if (A.L.bx == 16 && A.L.by == 16) return launch_b<MODE, CHECK, 16, 16>(F, A, s);
     return launch_b<MODE, CHECK, 0, 0>(F, A, s);
