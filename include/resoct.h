@@ -64,6 +64,7 @@ extern "C" {
 #define RO_MAX_CH 8
 #define RO_MAX_TF_POINTS 16
 #define RO_NUM_COUNTERS 8
+#define RO_SUB_EDGE 4        /* sub-block edge of ro_state.sub_max */
 
 #define RO_MODE_RESIDENCY 0
 #define RO_MODE_REFERENCE 1
@@ -102,6 +103,16 @@ typedef struct ro_state {
     int64_t *slot_last_used; /* [S]   LRU frame stamp */
     int32_t *free_stack;     /* [S]   LIFO free list, top at free_count-1 */
     int32_t *free_count;     /* [1]   device scalar */
+    uint8_t *sub_max;        /* [S*nsb] optional (NULL = off), kept by
+                                ro_apply_bricks*: for bricks with every side
+                                >= 4, nsb = (bx/4)(by/4)(bz/4) sub-blocks of
+                                4^3 voxels per slot (RO_SUB_EDGE), each holding
+                                the max of its voxels dilated by one on every
+                                side (clipped to the brick); lets the ray
+                                caster skip the taps of a sample whose
+                                neighbourhood is wholly in a transfer
+                                function's transparent range (an exact +0
+                                contribution) */
 } ro_state;
 
 /* One visible channel in importance order (render.py:35-44,101-122). */

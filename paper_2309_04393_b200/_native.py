@@ -25,6 +25,8 @@ RO_MODE_PAGETABLE = 2
 RO_MODE_CLASSIC = 3
 RO_PT_UNMAPPED = -1
 RO_PT_EMPTY = -2
+RO_SUB_EDGE = 4          # sub-block edge of ro_state.sub_max (resoct.h)
+RO_SUB_EDGE_ALLOC = int(os.environ.get("RESOCT_SUB_EDGE_ALLOC", RO_SUB_EDGE))
 
 _p = C.c_void_p
 _i32 = C.c_int32
@@ -49,7 +51,8 @@ class Layout(C.Structure):
 
 class State(C.Structure):
     _fields_ = [("words", _p), ("pt", _p), ("cache", _p), ("slot_brick", _p),
-                ("slot_last_used", _p), ("free_stack", _p), ("free_count", _p)]
+                ("slot_last_used", _p), ("free_stack", _p), ("free_count", _p),
+                ("sub_max", _p)]
 
 
 class Channel(C.Structure):

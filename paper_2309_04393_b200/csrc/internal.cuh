@@ -10,6 +10,12 @@
 
 #define RO_BVOX_MAX (1 << 21)
 
+// edge of the sub-blocks of ro_state.sub_max (RO_SUB_E^3 voxels)
+#ifndef RO_SUB_LOG
+#define RO_SUB_LOG 2  // 4^3 sub-blocks: measured 8 % faster ray cast than 8^3, same as 2^3
+#endif
+#define RO_SUB_E (1 << RO_SUB_LOG)  // == RO_SUB_EDGE of resoct.h in the default build
+
 namespace ro {
 
 // thread-local last error (ro_last_error)

@@ -37,6 +37,9 @@
 #ifndef RO_PERSISTENT
 #define RO_PERSISTENT 1
 #endif
+#ifndef RO_SUBMAX
+#define RO_SUBMAX 1
+#endif
 #ifndef RO_NCH_FAST
 #define RO_NCH_FAST 0
 #endif
@@ -125,6 +128,8 @@ struct RayArgs {
     int32_t *touched_n;
     int32_t local_rows;
     int32_t *tile_counter;   // persistent-CTA work counter (zeroed per launch)
+    const uint8_t *sub_max;  // [S*nsb] dilated 8^3 sub-block maxima (optional)
+    int32_t nsb;             // sub-blocks per slot
 };
 
 __device__ __forceinline__ double lerp(double a, double b, double t) {
@@ -541,9 +546,9 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
             double skip_exit = -1.0;
             int end_depth = prev_depth;
 
-            auto finish = [&](int ci, int lev, int slot_lin, const LevelPos &lp, const Taps &tp) {
-                int tv[8];
-                load_taps<BX, BY>(tv, A.cache + (int64_t)slot_lin * bvox + tp.o, bx, bx * by);
+            // usage mask / histogram / per-pixel brick switches of a sampled
+            // channel (kernels.py:670-676)
+            auto account = [&](int ci, int lev, const LevelPos &lp) {
                 const int32_t e = S.ptoff[ci][lev] + lp.local;
                 int32_t &pb = prev_brick[ci * kBlock + tid];
                 if (e != pb) {
@@ -552,6 +557,28 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                     A.required[e] = 1;
                 }
                 hist_t[(ci * k + lev) * kBlock + tid] += 1;
+            };
+            // Sub-block skip: the taps with non-zero weight lie within one
+            // voxel of int(local coordinate), i.e. inside the dilated 8^3
+            // sub-block holding it; if that block's max is in the TF's
+            // leading transparent range, so is the trilinear value (a convex
+            // combination of those taps) and the channel adds exactly +0.
+            auto sub_skip = [&](int ci, int slot_lin, const LevelPos &lp) -> bool {
+#if RO_SUBMAX
+                if (A.sub_max == nullptr) return false;
+                const int xi = min((int)lp.P[0] - lp.cb[0] * bx, bx - 1) >> RO_SUB_LOG;
+                const int yi = min((int)lp.P[1] - lp.cb[1] * by, by - 1) >> RO_SUB_LOG;
+                const int zi = min((int)lp.P[2] - lp.cb[2] * bz, bz - 1) >> RO_SUB_LOG;
+                const int nsx = bx >> RO_SUB_LOG, nsy = by >> RO_SUB_LOG;
+                const int q = (zi * nsy + yi) * nsx + xi;
+                return (int)__ldg(A.sub_max + (int64_t)slot_lin * A.nsb + q) <= S.zero_upto[ci];
+#else
+                return false;
+#endif
+            };
+            auto finish = [&](int ci, int slot_lin, const Taps &tp) {
+                int tv[8];
+                load_taps<BX, BY>(tv, A.cache + (int64_t)slot_lin * bvox + tp.o, bx, bx * by);
                 // The trilinear value never exceeds the largest tap (every lerp
                 // is a rounded convex combination).  If that tap lies in the
                 // TF's leading zero-opacity range, r*a, g*a, b*a are +0 and
@@ -569,18 +596,22 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
             };
             // sample at the desired level (sc.lp already holds it)
             auto sample = [&](int ci, int lev, int slot_lin) {
+                account(ci, lev, sc.lp);
+                if (sub_skip(ci, slot_lin, sc.lp)) return;
                 if (sc.tp_lev != lev) { taps_of(sc.tp, sc.lp, bx, by, bz, S); sc.tp_lev = lev; }
-                finish(ci, lev, slot_lin, sc.lp, sc.tp);
+                finish(ci, slot_lin, sc.tp);
             };
             // sample at a substitute level (sc.lp2 holds it)
             auto sample2 = [&](int ci, int lev, int slot_lin) {
+                account(ci, lev, sc.lp2);
+                if (sub_skip(ci, slot_lin, sc.lp2)) return;
 #if RO_SUBCACHE
                 if (sc.tp2_lev != lev) { taps_of(sc.tp2, sc.lp2, bx, by, bz, S); sc.tp2_lev = lev; }
-                finish(ci, lev, slot_lin, sc.lp2, sc.tp2);
+                finish(ci, slot_lin, sc.tp2);
 #else
                 Taps t2;
                 taps_of(t2, sc.lp2, bx, by, bz, S);
-                finish(ci, lev, slot_lin, sc.lp2, t2);
+                finish(ci, slot_lin, t2);
 #endif
             };
 
@@ -1068,6 +1099,11 @@ int render(ro_ctx *c, const ro_frame *F, const ro_state *st,
     A.meta_touched = c->meta_touched;
     A.touched_n = c->touched_n;
     A.tile_counter = c->touched_n + 2;
+    const bool sub_ok = c->layout.brick[0] >= RO_SUB_E && c->layout.brick[1] >= RO_SUB_E &&
+                        c->layout.brick[2] >= RO_SUB_E;
+    A.sub_max = sub_ok ? st->sub_max : nullptr;
+    A.nsb = sub_ok ? (c->layout.brick[0] >> RO_SUB_LOG) * (c->layout.brick[1] >> RO_SUB_LOG) *
+                         (c->layout.brick[2] >> RO_SUB_LOG) : 0;
     A.local_rows = (int32_t)ro_local_rows(F->height, F->n_parts, F->part, F->tile_rows);
     RO_CUDA(cudaMemsetAsync(out->required, 0, (size_t)c->E, s));
     RO_CUDA(cudaMemsetAsync(out->hist, 0, sizeof(int64_t) * F->n_ch * c->layout.k, s));

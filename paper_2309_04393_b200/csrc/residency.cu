@@ -154,6 +154,36 @@ __global__ void k_copy_payloads(int32_t n, int64_t bvox,
     }
 }
 
+// per-slot 8^3 sub-block maxima, dilated by one voxel (ro_state.sub_max):
+// one CTA per batch brick, one thread per sub-block
+__global__ void k_sub_max(int32_t n, int bx, int by, int bz, const uint8_t *__restrict__ src,
+                          const int32_t *__restrict__ slots,
+                          const uint8_t *__restrict__ final_flag, uint8_t *__restrict__ sub_max) {
+    const int i = blockIdx.x;
+    if (i >= n || !final_flag[i]) return;
+    const int nx = bx >> RO_SUB_LOG, ny = by >> RO_SUB_LOG, nz = bz >> RO_SUB_LOG,
+              nsb = nx * ny * nz;
+    constexpr int E = RO_SUB_E;
+    const int64_t bvox = (int64_t)bx * by * bz;
+    const uint8_t *b = src ? src + (int64_t)i * bvox : nullptr;
+    for (int q = threadIdx.x; q < nsb; q += blockDim.x) {
+        unsigned mx = 255;
+        if (b) {
+            const int sx = q % nx, sy = (q / nx) % ny, sz = q / (nx * ny);
+            const int x0 = max(E * sx - 1, 0), x1 = min(E * sx + E + 1, bx);
+            const int y0 = max(E * sy - 1, 0), y1 = min(E * sy + E + 1, by);
+            const int z0 = max(E * sz - 1, 0), z1 = min(E * sz + E + 1, bz);
+            mx = 0;
+            for (int z = z0; z < z1; ++z)
+                for (int y = y0; y < y1; ++y) {
+                    const uint8_t *row = b + ((int64_t)z * by + y) * bx;
+                    for (int x = x0; x < x1; ++x) mx = max(mx, (unsigned)row[x]);
+                }
+        }
+        sub_max[(int64_t)slots[i] * nsb + q] = (uint8_t)mx;
+    }
+}
+
 __global__ void k_copy_payloads_bytes(int32_t n, int64_t bvox,
                                       const uint8_t *__restrict__ src,
                                       const int32_t *__restrict__ slots,
@@ -639,6 +669,13 @@ int apply_bricks(ro_ctx *c, const ro_state *st, const int64_t *ids_h, int64_t n6
         else
             k_copy_payloads_bytes<<<blocks_for(bvox * n), kThreads, 0, s>>>(
                 n, bvox, d_payload, d_slots, d_final, st->cache);
+        RO_CUDA(cudaGetLastError());
+    }
+    if (st->sub_max && c->layout.brick[0] >= RO_SUB_E && c->layout.brick[1] >= RO_SUB_E &&
+        c->layout.brick[2] >= RO_SUB_E) {
+        k_sub_max<<<n, 128, 0, s>>>(n, c->layout.brick[0], c->layout.brick[1],
+                                    c->layout.brick[2], d_payload, d_slots, d_final,
+                                    st->sub_max);
         RO_CUDA(cudaGetLastError());
     }
     if (update_octree && st->words) {

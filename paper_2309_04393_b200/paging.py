@@ -127,6 +127,15 @@ class MultiChannelPaging:
         self.free_stack = torch.arange(self.num_slots - 1, -1, -1, dtype=torch.int32,
                                        device=dev)
         self.free_count = torch.tensor([self.num_slots], dtype=torch.int32, device=dev)
+        # dilated 8^3 sub-block maxima per slot (resoct.h ro_state.sub_max),
+        # maintained by every insert; 255 = unknown
+        if min(sx, sy, sz) >= N.RO_SUB_EDGE:
+            e = N.RO_SUB_EDGE_ALLOC
+            nsb = (sx // e) * (sy // e) * (sz // e)
+            self.sub_max = torch.full((self.num_slots * nsb,), 255, dtype=torch.uint8,
+                                      device=dev)
+        else:
+            self.sub_max = None
         self.channel_mapping = list(range(config.m))
         self._octree_words = None
         self._depth = 0
@@ -176,6 +185,7 @@ class MultiChannelPaging:
         st.slot_last_used = self.slot_last_used_dev.data_ptr()
         st.free_stack = self.free_stack.data_ptr()
         st.free_count = self.free_count.data_ptr()
+        st.sub_max = self.sub_max.data_ptr() if self.sub_max is not None else None
         return st
 
     def __del__(self):
