@@ -240,6 +240,7 @@ struct LevelPos {
     double P[3];
     int cb[3];
     int local;  // (cz*gy + cy)*gx + cx
+    int sub;    // 4^3 sub-block of int(P) inside the brick (ro_state.sub_max index)
 };
 
 __device__ __forceinline__ void level_pos(LevelPos &lp, int lev, double px, double py,
@@ -248,14 +249,20 @@ __device__ __forceinline__ void level_pos(LevelPos &lp, int lev, double px, doub
     lp.lev = lev;
     const double p3[3] = {px, py, pz};
     const int lb3[3] = {lbx, lby, lbz};
+    int sb[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
         lp.P[a] = p3[a] * S.dimd[lev][a];
-        int c = ((int)lp.P[a]) >> lb3[a];
+        const int ip = (int)lp.P[a];
+        int c = ip >> lb3[a];
         const int g = S.grids[lev][a];
         lp.cb[a] = c > g - 1 ? g - 1 : c;
+        // local integer coordinate (>= B only on a clamped edge brick)
+        sb[a] = min(ip - (lp.cb[a] << lb3[a]), (1 << lb3[a]) - 1) >> RO_SUB_LOG;
     }
     lp.local = (lp.cb[2] * S.grids[lev][1] + lp.cb[1]) * S.grids[lev][0] + lp.cb[0];
+    // (bricks smaller than a sub-block have no sub_max table: lp.sub unused)
+    lp.sub = (((sb[2] << max(lby - RO_SUB_LOG, 0)) + sb[1]) << max(lbx - RO_SUB_LOG, 0)) + sb[0];
 }
 
 // kernels.py:518-549: nearest resident level in the node's mask, coarser
@@ -264,15 +271,21 @@ __device__ __forceinline__ void level_pos(LevelPos &lp, int lev, double px, doub
 RARE __device__ int2 substitute(const int32_t *__restrict__ pt, const FrameSmem &S, int ci,
                                 int lev, int k, uint32_t mask, double px, double py,
                                 double pz, int lbx, int lby, int lbz, LevelPos &lp2) {
-    for (int delta = 1; delta < k; ++delta) {
-#pragma unroll
-        for (int sgn = 0; sgn < 2; ++sgn) {
-            const int cand = sgn == 0 ? lev + delta : lev - delta;
-            if (cand < 0 || cand >= k || !((mask >> cand) & 1u)) continue;
-            if (lp2.lev != cand) level_pos(lp2, cand, px, py, pz, S, lbx, lby, lbz);
-            const int pv2 = __ldg(pt + S.ptoff[ci][cand] + lp2.local);
-            if (pv2 >= 0) return make_int2(cand, pv2);
-        }
+    // Visit the levels present in the mask in the reference's order
+    // (distance 1, 2, ...; the coarser one first on a tie) by taking the
+    // nearest remaining set bit on either side, instead of scanning every
+    // candidate distance.
+    uint32_t mk = mask & ((1u << k) - 1u) & ~(1u << lev);
+    while (mk) {
+        const uint32_t above = mk >> (lev + 1);
+        const uint32_t below = mk & ((1u << lev) - 1u);
+        const int da = above ? __ffs(above) : 64;
+        const int db = below ? lev - (31 - __clz(below)) : 64;
+        const int cand = da <= db ? lev + da : lev - db;
+        if (lp2.lev != cand) level_pos(lp2, cand, px, py, pz, S, lbx, lby, lbz);
+        const int pv2 = __ldg(pt + S.ptoff[ci][cand] + lp2.local);
+        if (pv2 >= 0) return make_int2(cand, pv2);
+        mk &= ~(1u << cand);
     }
     return make_int2(-1, -1);
 }
@@ -566,12 +579,8 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
             auto sub_skip = [&](int ci, int slot_lin, const LevelPos &lp) -> bool {
 #if RO_SUBMAX
                 if (A.sub_max == nullptr) return false;
-                const int xi = min((int)lp.P[0] - lp.cb[0] * bx, bx - 1) >> RO_SUB_LOG;
-                const int yi = min((int)lp.P[1] - lp.cb[1] * by, by - 1) >> RO_SUB_LOG;
-                const int zi = min((int)lp.P[2] - lp.cb[2] * bz, bz - 1) >> RO_SUB_LOG;
-                const int nsx = bx >> RO_SUB_LOG, nsy = by >> RO_SUB_LOG;
-                const int q = (zi * nsy + yi) * nsx + xi;
-                return (int)__ldg(A.sub_max + (int64_t)slot_lin * A.nsb + q) <= S.zero_upto[ci];
+                return (int)__ldg(A.sub_max + (int64_t)slot_lin * A.nsb + lp.sub) <=
+                       S.zero_upto[ci];
 #else
                 return false;
 #endif
