@@ -37,6 +37,9 @@
 #ifndef RO_PERSISTENT
 #define RO_PERSISTENT 1
 #endif
+#ifndef RO_FIXED_STRIDE
+#define RO_FIXED_STRIDE 0
+#endif
 #ifndef RO_SUBMAX
 #define RO_SUBMAX 1
 #endif
@@ -447,10 +450,17 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
         S.eps_i = F.eps_h >= 255.0 ? 255 : (F.eps_h < 0.0 ? -1 : (int)F.eps_h);
     }
     // per-thread arrays: [ci*kBlock + tid]
+#if RO_FIXED_STRIDE
+    // constant array offsets (sized for RO_MAX_CH): every access is
+    // tid*4 + ci*512 + an immediate
+    constexpr int kChStride = RO_MAX_CH * kBlock;
+#else
+    const int kChStride = n_ch * kBlock;
+#endif
     int32_t *prev_brick = dyn;                        // n_ch
-    int32_t *last_breq = prev_brick + n_ch * kBlock;  // n_ch
-    int32_t *last_mreq = last_breq + n_ch * kBlock;   // n_ch
-    uint32_t *hist_t = reinterpret_cast<uint32_t *>(last_mreq + n_ch * kBlock);
+    int32_t *last_breq = prev_brick + kChStride;      // n_ch
+    int32_t *last_mreq = last_breq + kChStride;       // n_ch
+    uint32_t *hist_t = reinterpret_cast<uint32_t *>(last_mreq + kChStride);
     for (int i = 0; i < n_ch * k; ++i) hist_t[i * kBlock + tid] = 0;
     const int lane = tid & 31;
     [[maybe_unused]] const int warp = tid >> 5;
@@ -1000,7 +1010,11 @@ cudaError_t launch_b(const ro_frame &F, const RayArgs &A, cudaStream_t s) {
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev);
     }
+#if RO_FIXED_STRIDE
+    size_t dyn = (size_t)RO_MAX_CH * kBlock * 4 * 3 + (size_t)F.n_ch * A.L.k * kBlock * 4;
+#else
     size_t dyn = (size_t)F.n_ch * kBlock * 4 * 3 + (size_t)F.n_ch * A.L.k * kBlock * 4;
+#endif
     auto kern = k_raycast<MODE, CHECK, BX, BY, NCH>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)dyn);
