@@ -399,6 +399,8 @@ def run_ours(args):
                        "l2_policy": "inputs larger than L2 (brick cache > 126 MB)",
                        "parallelism": f"sort-first x{world}" if world > 1 else "1 GPU"},
             "gsamples_per_s": samples * fps / 1e9,
+            # 8 trilinear taps per fetch (SURVEY 8(d) "sampled voxels/s"), whole job
+            "sampled_gvoxels_per_s": 8.0 * F / (ms_per_step / 1e3) / 1e9,
             "frame_work": {"samples": samples, "fetches": F, "traversal_steps": S,
                            "pixels": P, "livelocked_rays": int(counters[4])},
             "kernel_ms": {"raycast": kern_ms, "feedback": fb_ms},

@@ -21,6 +21,8 @@ M = {
     "l2_hit_pct": "lts__t_sector_hit_rate.pct",
     "fp64_pipe_pct": "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
     "active_threads_per_inst": "smsp__thread_inst_executed_per_inst_executed.ratio",
+    "l2_sectors": "lts__t_sectors.sum",
+    "l1_sectors": "SM_B.TriageCompute.l1tex__t_sectors.sum",
 }
 STALLS = ["wait", "long_scoreboard", "selected", "short_scoreboard", "branch_resolving",
           "not_selected", "no_instructions", "barrier", "math_pipe_throttle", "lg_throttle",
@@ -62,6 +64,12 @@ def main():
     s["stall_share_pct"] = {k: round(100 * v / tot, 1)
                             for k, v in sorted(st.items(), key=lambda kv: -kv[1]) if v > 0}
     s["dram_bytes_per_launch"] = s["dram_bytes_read"] + s["dram_bytes_write"]
+    t = s["duration_ms"] / 1e3
+    s["achieved_GBps"] = {"dram": s["dram_bytes_per_launch"] / t / 1e9,
+                          "l2": 32 * s["l2_sectors"] / t / 1e9,
+                          "l1": 32 * s["l1_sectors"] / t / 1e9}
+    s["warp_divergence"] = {"active_threads_per_inst": s["active_threads_per_inst"],
+                            "lane_efficiency_pct": 100.0 * s["active_threads_per_inst"] / 32}
     with open(out, "w") as f:
         json.dump(s, f, indent=1)
     print(json.dumps(s, indent=1))
