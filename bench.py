@@ -148,13 +148,29 @@ def _ncu_traffic(world):
         return None
 
 
+def _hang_guard():
+    """RESOCT_HANG_DUMP_S=<s>: dump every thread's stack and exit if a rank
+    is still running after s seconds (debugging multi-rank runs)."""
+    t = os.environ.get("RESOCT_HANG_DUMP_S")
+    if t:
+        import faulthandler
+        faulthandler.dump_traceback_later(float(t), exit=True)
+
+
 def _dist_init():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if world > 1:
         import torch.distributed as dist
         local = int(os.environ.get("LOCAL_RANK", "0"))
+        # one process per GPU; RESOCT_DIST_BACKEND=gloo (host collectives) is
+        # only for functional checks of this path with fewer GPUs than ranks
+        backend = os.environ.get("RESOCT_DIST_BACKEND", "nccl")
+        local = local % max(1, torch.cuda.device_count())
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
         return dist.get_rank(), world, local
     return 0, 1, 0
 
@@ -241,6 +257,7 @@ def run_reference(args):
 
 
 def run_ours(args):
+    _hang_guard()
     rank, world, local = _dist_init()
     from paper_2309_04393_b200 import _native as N
     from paper_2309_04393_b200 import scenarios
@@ -335,10 +352,64 @@ def run_ours(args):
     peak, peak_kind = _peaks()
     achieved = part_bytes / (kern_ms / 1000.0) / 1e9
 
+    # ---- e2e of the sort-first frame (N > 1): every rank renders its rows,
+    # one exchange, rank 0 receives the assembled image and reads it (plus
+    # the merged feedback) into host memory; wall time, max over ranks ----
+    e2e_multi = None
+    if world > 1 and not args.no_e2e:
+        from paper_2309_04393_b200.distributed import exchange as _exchange
+        pin_img = torch.empty((h, w, 4), dtype=torch.float32, pin_memory=True)
+
+        def e2e_step():
+            fp.render()
+            fp.collect()
+            b = fp.buf
+            res = _exchange(dict(image=b.image, required=b.required,
+                                 pix_required=b.pix_required, hist=b.hist, counters=b.counters,
+                                 fb=b.fb, counts=b.counts),
+                            cfg.image_dims, 8, cfg.max_requests_per_frame, m)
+            if rank == 0:
+                pin_img.copy_(res["image"], non_blocking=True)
+            torch.cuda.synchronize()
+            return res
+        for _ in range(2):
+            e2e_step()
+        torch.distributed.barrier()
+        n_e2e = max(3, args.steps // 2)
+        t0 = time.perf_counter()
+        for _ in range(n_e2e):
+            res = e2e_step()
+        el = torch.tensor([(time.perf_counter() - t0) / n_e2e], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(el, op=torch.distributed.ReduceOp.MAX)
+        e2e_multi = {"value": 1.0 / float(el[0]), "unit": "frames/s",
+                     "h2d_bytes_per_step": ctypes.sizeof(N.Frame) * world,
+                     "d2h_bytes_per_step": int(pin_img.numel() * 4 + 8 * 4 * fp.buf.fb.shape[1]
+                                               * world),
+                     "note": ("sort-first frame through FramePass + distributed.exchange: "
+                              "rows rendered per GPU, NCCL exchange (usage MAX, hist/counters "
+                              "SUM, request lists all-gathered + merged), image gathered to "
+                              "rank 0 and copied to pinned host memory; wall time, max over "
+                              "ranks")}
+
+    # ---- kernel launches in one step (profiler, untimed).  Every rank runs
+    # the step: it contains the exchange collectives. ----
+    launches = None
+    try:
+        from torch.profiler import ProfilerActivity, profile
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            step()
+            torch.cuda.synchronize()
+        names = [e.name for e in prof.events() if e.device_type.name == "CUDA"]
+        launches = sum(1 for n in names if ("ro::" in n or "cub::" in n or "k_raycast" in n))
+    except Exception:
+        if world > 1:
+            raise  # a rank that skipped the step's collectives would hang the others
+        launches = None
+
     result = None
     if rank == 0:
         # ---- e2e through the public API (host buffers) ----
-        e2e = None
+        e2e = e2e_multi
         if world == 1 and not args.no_e2e:
             for _ in range(2):
                 out = render_frame(eng.paging, eng.octree, scn.channels, scn.camera, cfg)
@@ -357,18 +428,6 @@ def run_ours(args):
                              "the kernel into pinned host memory over PCIe (zero-copy), "
                              "usage mask / histogram / counters / requests copied after; "
                              "numpy outputs")}
-        # ---- kernel launches in one step (profiler, untimed) ----
-        launches = None
-        try:
-            from torch.profiler import ProfilerActivity, profile
-            with profile(activities=[ProfilerActivity.CUDA]) as prof:
-                step()
-                torch.cuda.synchronize()
-            names = [e.name for e in prof.events() if e.device_type.name == "CUDA"]
-            launches = sum(1 for n in names if ("ro::" in n or "cub::" in n
-                                                or "k_raycast" in n))
-        except Exception:
-            launches = None
         # ---- CPU baseline (oracle, all cores) + parity of the sampled rows ----
         cpu = None
         parity = None

@@ -132,13 +132,15 @@ def exchange(local: dict, image_dims, tile_rows: int, budget: int, m: int,
         max_rows = max(len(part_rows(h, world, p, tile_rows)) for p in range(world))
         img = torch.zeros((max_rows * w, 4), dtype=torch.float32, device=dev)
         img[:local["image"].shape[0]] = local["image"]
-        parts = [torch.empty_like(img) for _ in range(world)] if rank == 0 else None
-        try:
+        # NCCL: gather to rank 0; other backends (gloo, CPU tests): all-gather.
+        # The choice depends only on the backend, so every rank takes the
+        # same collective.
+        if dist.get_backend() == "nccl":
+            parts = [torch.empty_like(img) for _ in range(world)] if rank == 0 else None
             dist.gather(img, parts, dst=0)
-        except (RuntimeError, ValueError):
-            parts_all = [torch.empty_like(img) for _ in range(world)]
-            dist.all_gather(parts_all, img)
-            parts = parts_all if rank == 0 else None
+        else:
+            parts = [torch.empty_like(img) for _ in range(world)]
+            dist.all_gather(parts, img)
         if rank == 0:
             full = torch.empty((h, w, 4), dtype=torch.float32, device=dev)
             for p in range(world):
