@@ -34,6 +34,10 @@ def main():
     ap.add_argument("--image", type=int, nargs=2, default=[1920, 1080])
     ap.add_argument("--frames", type=int, default=30)
     ap.add_argument("--swap-at", type=int, default=10)
+    ap.add_argument("--device-metadata", action="store_true",
+                    help="answer metadata requests from the GPU min/max pyramid")
+    ap.add_argument("--lz4", action="store_true",
+                    help="fetch LZ4 frames and decode them on the GPU into the cache")
     ap.add_argument("--oracle", action="store_true",
                     help="also time the reference-semantics Python updates")
     args = ap.parse_args()
@@ -54,7 +58,8 @@ def main():
     rconf = RenderConfig(image_dims=tuple(args.image), base_step=1.0 / 256.0,
                          max_requests_per_frame=512, traversal_start_level=2)
     econf = EngineConfig(octree_depth=5, cache_slots=(16, 16, 8), channel_slots=4)
-    sess = Session(LocalTransport(store), econf, rconf, chans)
+    sess = Session(LocalTransport(store), econf, rconf, chans,
+                   device_metadata=args.device_metadata, compressed_transfer=args.lz4)
     eng = sess.engine
     pose = orbit_pose(0.6)
 
@@ -82,11 +87,17 @@ def main():
         tf0 = time.perf_counter()
         ids = list(out.brick_requests)
         pays = [sess._fetch_brick(b)[1] for b in ids]
-        metas = [sess._fetch_metadata(n, s) for n, s in out.metadata_requests]
+        if args.device_metadata and out.metadata_requests:
+            metas = list(zip(*sess._lookup_metadata(out.metadata_requests)))
+        else:
+            metas = [sess._fetch_metadata(n, s) for n, s in out.metadata_requests]
         fetch_ms = (time.perf_counter() - tf0) * 1e3
         e[3].record()
         if ids:
-            eng.apply_bricks(ids, np.stack(pays))
+            if args.lz4:
+                eng.apply_bricks_lz4(ids, pays)
+            else:
+                eng.apply_bricks(ids, np.stack(pays))
         e[4].record()
         if metas:
             eng.apply_metadata_batch([m[0] for m in metas], [m[1] for m in metas],
@@ -111,6 +122,8 @@ def main():
             "apply_bricks_ms_median": float(np.median(upd)) if upd else None,
             "apply_bricks_us_per_brick_median": 1e3 * float(np.median(per_brick)) if per_brick else None,
             "apply_metadata_ms_median": float(np.median([r["apply_metadata_ms"] for r in frames])),
+            "host_fetch_ms_median": float(np.median([r["host_fetch_ms"] for r in frames])),
+            "device_metadata": args.device_metadata, "lz4_transfer": args.lz4,
             "swap_ms": [r["swap_ms"] for r in rows if "swap_ms" in r],
             "per_frame": rows}
     if args.oracle:
