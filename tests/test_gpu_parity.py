@@ -515,3 +515,50 @@ def test_gpu_baselines_errors():
     eng = Engine(man, EngineConfig(octree_depth=3, cache_slots=(2, 2, 2), channel_slots=1))
     with pytest.raises(RenderError):
         ClassicMetadata(eng.paging)
+
+
+def test_gpu_sub_block_maxima_and_skip_is_exact():
+    """ro_state.sub_max == max over each 4^3 sub-block dilated by one voxel
+    (clipped) for every occupied slot, kept across LRU replacement; rendering
+    with the table and without it (NULL) gives identical outputs."""
+    import torch
+    import torch.nn.functional as Fn
+    from paper_2309_04393_b200 import render as R
+    from paper_2309_04393_b200 import _native as N
+    eng = _prepared_engine("shell64", depth=3)
+    p = eng.paging
+    e = N.RO_SUB_EDGE
+    occ = torch.nonzero(p.slot_brick_dev >= 0).flatten()
+    cache = p.cache_dev[occ].float()
+    ref = Fn.max_pool3d(cache.unsqueeze(1), kernel_size=e + 2, stride=e, padding=1)
+    bz, by, bx = p.cache_dev.shape[1:]
+    nsb = (bx // e) * (by // e) * (bz // e)
+    got = p.sub_max.view(-1, nsb)[occ].float()
+    assert torch.equal(got, ref.reshape(len(occ), -1))
+    # LRU replacement rewrites the table of the reused slots
+    st = scenes.store("shell64")
+    g = st.manifest.levels[0].brick_grid_dims
+    ids = [eng.paging.encode(0, 0, (x, y, z)) for z in range(g[2]) for y in range(g[1])
+           for x in range(g[0])][:3]
+    eng.evict_bricks(ids)
+    eng.advance_frame()
+    eng.apply_bricks(ids, np.stack([np.full((bz, by, bx), 7, np.uint8)] * 3))
+    for b in ids:
+        s = int(p.pt[eng.paging._entry_index(*eng.paging.decode(b))])
+        assert int(p.sub_max.view(-1, nsb)[s].max()) == 7
+    # identical render with the table switched off
+    chans = [R.ChannelSettings(slot=0, tf=__import__(
+        "paper_2309_04393_b200").grayscale_ramp_tf(40.0))]
+    from paper_2309_04393_b200 import RenderConfig, orbit_pose
+    cfg = RenderConfig(image_dims=(96, 80), base_step=1.0 / 64.0, max_requests_per_frame=256)
+    a = R.render_frame(p, eng.octree, chans, orbit_pose(0.9), cfg)
+    keep = p.sub_max
+    p.sub_max = None
+    try:
+        b = R.render_frame(p, eng.octree, chans, orbit_pose(0.9), cfg)
+    finally:
+        p.sub_max = keep
+    assert np.array_equal(a.image, b.image)
+    assert a.brick_requests == b.brick_requests
+    assert np.array_equal(a.required_mask, b.required_mask)
+    assert np.array_equal(a.level_histogram, b.level_histogram)
