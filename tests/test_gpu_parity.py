@@ -562,3 +562,53 @@ def test_gpu_sub_block_maxima_and_skip_is_exact():
     assert a.brick_requests == b.brick_requests
     assert np.array_equal(a.required_mask, b.required_mask)
     assert np.array_equal(a.level_histogram, b.level_histogram)
+
+
+def test_gpu_config2_full_size_properties():
+    """BASELINE config 2 at full size (2048x2048x128 x4 channels, 1080p):
+    sampled row bands bit-exact against the oracle (usage mask and
+    histogram of the bands contained in the frame's), and the frame split
+    sort-first into 3 parts and merged equals the single-pass frame
+    (image, ordered requests, usage, histogram, counters)."""
+    import os
+    import torch
+    from oracle import raycast as orc
+    from paper_2309_04393_b200 import render_frame, scenarios
+    from paper_2309_04393_b200.distributed import merge_parts
+    from paper_2309_04393_b200.render import MODE_RESIDENCY, FramePass
+    scn = scenarios.cycif(device="cuda")
+    eng = scenarios.build_engine(scn)
+    cfg = scn.render
+    w, h = cfg.image_dims
+    out = render_frame(eng.paging, eng.octree, scn.channels, scn.camera, cfg)
+    ref = orc.OracleState(**scenarios.reference_state(scn))
+    och = [orc.OracleChannel(slot=c.slot, points=c.tf.points, level_range=c.level_range)
+           for c in scn.channels]
+    for a in (0, 300, 536, 760, 1076):
+        o = orc.render(ref, och, cam_tuple(scn.camera), cfg.image_dims, cfg.base_step,
+                       budget=cfg.max_requests_per_frame, rows=(a, a + 4),
+                       threads=os.cpu_count() or 1)
+        assert np.array_equal(out.image[a:a + 4], o.image[a:a + 4]), a
+        assert not (o.required_mask & ~out.required_mask).any(), a
+        assert (o.level_histogram <= out.level_histogram).all(), a
+    parts = []
+    for p in range(3):
+        fp = FramePass(MODE_RESIDENCY, eng.paging, eng.octree, scn.channels, scn.camera, cfg,
+                       partition=(3, p, 8), bricks_first=False)
+        fp.render()
+        fp.collect()
+        b = fp.buf
+        parts.append({k: (v.clone() if isinstance(v, torch.Tensor) else v.copy())
+                      for k, v in dict(image=b.image, required=b.required,
+                                       pix_required=b.pix_required, hist=b.hist,
+                                       counters=b.counters, fb=b.fb, counts=b.counts).items()})
+    merged = merge_parts(parts, cfg.image_dims, 3, 8, cfg.max_requests_per_frame,
+                         eng.paging.config.m)
+    assert np.array_equal(merged["image"], out.image)
+    assert merged["bricks"] == out.brick_requests
+    assert merged["metas"] == out.metadata_requests
+    assert np.array_equal(merged["required"], out.required_mask)
+    assert np.array_equal(merged["hist"], out.level_histogram)
+    assert np.array_equal(merged["pix_required"], out.pixel_required)
+    assert int(merged["counters"][1] + merged["counters"][2]) == \
+        out.stats.samples_evaluated + out.stats.samples_skipped
