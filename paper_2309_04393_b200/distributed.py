@@ -16,6 +16,12 @@ One exchange step per frame, over NCCL / NVLink:
 The merged result is bit-identical to a single-GPU frame (tested in
 tests/test_gpu_parity.py and, for the exchange itself, with gloo on CPU in
 tests/test_distributed.py).
+
+Capacity mode (``Session(partition=...)``): every GPU keeps its own cache,
+LRU and octree for its own rows only (no feedback exchange, so per-GPU cache
+capacity adds up); ``gather_image`` collects the tiles on rank 0.  Images
+equal the single-GPU ones once the parts have converged (every desired brick
+resident), like the reference's full-residency image.
 """
 
 from __future__ import annotations
@@ -149,3 +155,33 @@ def exchange(local: dict, image_dims, tile_rows: int, budget: int, m: int,
                 full.index_copy_(0, idx, parts[p][:len(rows) * w].reshape(len(rows), w, 4))
             out["image"] = full
     return out
+
+
+def gather_image(local_rows_image, image_dims, tile_rows: int):
+    """Gather every rank's rows (local_rows, w, 4) into the full (h, w, 4)
+    frame on rank 0 (None elsewhere).  NCCL: gather to rank 0; other
+    backends: all-gather (the choice depends only on the backend)."""
+    world = dist.get_world_size()
+    rank = dist.get_rank()
+    w, h = image_dims
+    local = torch.as_tensor(local_rows_image)
+    dev = torch.device("cuda", torch.cuda.current_device()) \
+        if dist.get_backend() == "nccl" else torch.device("cpu")
+    max_rows = max(len(part_rows(h, world, p, tile_rows)) for p in range(world))
+    buf = torch.zeros((max_rows * w, 4), dtype=torch.float32, device=dev)
+    flat = local.reshape(-1, 4).to(dev)
+    buf[:flat.shape[0]] = flat
+    if dist.get_backend() == "nccl":
+        parts = [torch.empty_like(buf) for _ in range(world)] if rank == 0 else None
+        dist.gather(buf, parts, dst=0)
+    else:
+        parts = [torch.empty_like(buf) for _ in range(world)]
+        dist.all_gather(parts, buf)
+    if rank != 0:
+        return None
+    full = torch.empty((h, w, 4), dtype=torch.float32, device=dev)
+    for p in range(world):
+        rows = part_rows(h, world, p, tile_rows)
+        idx = torch.as_tensor(rows, device=dev, dtype=torch.long)
+        full.index_copy_(0, idx, parts[p][:len(rows) * w].reshape(len(rows), w, 4))
+    return full.cpu().numpy()

@@ -347,10 +347,10 @@ def _copy_stream(device) -> torch.cuda.Stream:
 
 
 def _run(mode, paging, channels, camera, config, octree=None,
-         reference_paging=None, classic=None) -> FrameOutput:
+         reference_paging=None, classic=None, partition=(1, 0, 8)) -> FrameOutput:
     start = time.perf_counter()
     fp = FramePass(mode, paging, octree, channels, camera, config, reference_paging,
-                   classic=classic)
+                   partition=partition, classic=classic)
     buf = fp.buf
     # Zero-copy image: the ray caster stores each pixel's RGBA and brick
     # count straight into pinned host memory (UVA-mapped), so the 20 B/pixel
@@ -400,7 +400,8 @@ def _run(mode, paging, channels, camera, config, octree=None,
                        requests_issued=len(bricks) + len(metas), render_ms=elapsed_ms,
                        livelocked_rays=int(counters[4]))
     w, h = config.image_dims
-    return FrameOutput(image=img.numpy().reshape(h, w, 4), brick_requests=bricks,
+    rows = buf.image.shape[0] // w  # local rows of a partition (h for a full frame)
+    return FrameOutput(image=img.numpy().reshape(rows, w, 4), brick_requests=bricks,
                        metadata_requests=metas, stats=stats, required_mask=required,
                        level_histogram=hist, pixel_required=pixr.numpy(),
                        required_mask_device=buf.required)
@@ -413,6 +414,18 @@ def render_frame(paging: MultiChannelPaging, octree: ResidencyOctree,
     audit every skip."""
     return _run(MODE_RESIDENCY, paging, channels, camera, config, octree=octree,
                 reference_paging=reference_paging)
+
+
+def render_frame_part(paging: MultiChannelPaging, octree: ResidencyOctree, channels,
+                      camera: Camera, config: RenderConfig, partition) -> FrameOutput:
+    """render_frame for the rows of one sort-first part.  ``partition`` =
+    (n_parts, part, tile_rows): rows are cut in blocks of tile_rows and block
+    b belongs to part b % n_parts.  The image / pixel_required hold only this
+    part's rows (in order); requests, usage and histogram are this part's,
+    with the bricks-first budget applied to them -- the per-GPU frame of a
+    capacity-mode Session (distributed.gather_image assembles the frame)."""
+    return _run(MODE_RESIDENCY, paging, channels, camera, config, octree=octree,
+                partition=tuple(partition))
 
 
 def render_reference(paging: MultiChannelPaging, channels, camera: Camera,

@@ -125,3 +125,33 @@ def test_sort_first_exchange_gloo_world2(oracle_lib):
         assert np.array_equal(res["hist"], full.level_histogram)
         assert list(res["counters"][:5]) == list(full.counters)
     assert np.array_equal(results[0]["image"], full.image)
+
+
+def _gather_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2309_04393_b200.distributed import gather_image, part_rows
+    w, h = 11, 37
+    full = np.arange(h * w * 4, dtype=np.float32).reshape(h, w, 4)
+    local = full[part_rows(h, world, rank, TILE)]
+    got = gather_image(local, (w, h), TILE)
+    if rank == 0:
+        q.put(bool(np.array_equal(got, full)))
+    else:
+        q.put(got is None)
+    dist.destroy_process_group()
+
+
+def test_gather_image_assembles_capacity_mode_tiles():
+    """distributed.gather_image (capacity-mode frame assembly) over gloo."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gather_worker, args=(r, 3, port, q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(res), res

@@ -612,3 +612,43 @@ def test_gpu_config2_full_size_properties():
     assert np.array_equal(merged["pix_required"], out.pixel_required)
     assert int(merged["counters"][1] + merged["counters"][2]) == \
         out.stats.samples_evaluated + out.stats.samples_skipped
+
+
+def test_gpu_capacity_mode_parts_converge_to_single_gpu_image():
+    """Sort-first capacity mode: two part sessions, each
+    with its own cache / LRU / octree fed only by its own rows' requests,
+    converge independently; their stitched rows equal the single-session
+    converged image and the full-residency reference render (parity at image
+    level once every desired brick is resident)."""
+    from paper_2309_04393_b200 import (ChannelSettings, EngineConfig, LocalTransport,
+                                       RenderConfig, Session, grayscale_ramp_tf, orbit_pose,
+                                       render_reference)
+    from paper_2309_04393_b200.distributed import part_rows
+    st = scenes.store("vessel256")
+    econf = EngineConfig(octree_depth=5, cache_slots=(9, 9, 9), channel_slots=1)
+    cfg = RenderConfig(image_dims=(160, 120), base_step=1.0 / 128.0,
+                       max_requests_per_frame=512, traversal_start_level=2)
+    chans = [ChannelSettings(slot=0, tf=grayscale_ramp_tf(40.0))]
+    pose = orbit_pose(0.8)
+    single = Session(LocalTransport(st), econf, cfg, chans)
+    single.run_until_converged(pose, max_frames=50)
+    assert single.converged
+    ref_img = single.history[-1].output.image
+    w, h = cfg.image_dims
+    stitched = np.zeros_like(ref_img)
+    resident = []
+    for p in range(2):
+        sess = Session(LocalTransport(st), econf, cfg, chans, partition=(2, p, 8))
+        recs = sess.run_until_converged(pose, max_frames=50)
+        assert sess.converged, p
+        rows = part_rows(h, 2, p, 8)
+        assert recs[-1].output.image.shape == (len(rows), w, 4)
+        stitched[rows] = recs[-1].output.image
+        resident.append(sess.engine.paging.occupied_slot_count())
+        sess.close()
+    assert np.array_equal(stitched, ref_img)
+    full = _prepared_engine("vessel256", depth=5)
+    assert np.array_equal(render_reference(full.paging, chans, pose, cfg).image, ref_img)
+    # each part caches only what its own rows need
+    assert max(resident) < single.engine.paging.occupied_slot_count() <= sum(resident)
+    single.close()
