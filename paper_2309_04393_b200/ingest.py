@@ -96,13 +96,16 @@ LZ4_STATUS = {0: "ok", -1: "not an LZ4 frame", -2: "bad descriptor / header chec
               -6: "size mismatch", -7: "checksum mismatch", -8: "trailing bytes"}
 
 
+_INGEST_CTX = {}
+
+
 def _ctx():
-    """A context for the ingest calls that need scratch (one per process)."""
-    global _INGEST_CTX
-    try:
-        return _INGEST_CTX
-    except NameError:
-        pass
+    """A context for the ingest calls that need device scratch (one per
+    device; the layout is a 1-brick placeholder, only the scratch is used)."""
+    dev = torch.cuda.current_device()
+    h = _INGEST_CTX.get(dev)
+    if h is not None:
+        return h
     lay = N.Layout()
     lay.m, lay.k, lay.depth = 1, 1, 0
     lay.brick = (N._i32 * 3)(2, 2, 2)
@@ -113,7 +116,7 @@ def _ctx():
     lay.num_slots = 1
     h = C.c_void_p()
     N.check(N.lib().ro_create(C.byref(lay), C.byref(h)))
-    _INGEST_CTX = h
+    _INGEST_CTX[dev] = h
     return h
 
 
