@@ -269,6 +269,14 @@ int ro_fill_metadata(ro_ctx *ctx, const ro_state *state, int32_t slot,
                      const uint8_t *volume, int32_t dx, int32_t dy, int32_t dz,
                      int32_t pad, void *stream);
 
+/* octree.py:275-306 compute_node_metadata_from_bricks (min / max part), for
+   servers without a metadata endpoint: bricks [n][bz][by][bx] (device) and
+   brick-local half-open sub-boxes boxes[n][6] = x0,y0,z0,x1,y1,z1 (device);
+   mins / maxs [n] (device; an empty sub-box gives 255 / 0).  Asynchronous. */
+int ro_bricks_box_minmax(const uint8_t *bricks, const int32_t *boxes, int64_t n,
+                         int32_t bx, int32_t by, int32_t bz, uint8_t *mins,
+                         uint8_t *maxs, void *stream);
+
 int ro_evict_bricks(ro_ctx *ctx, const ro_state *state, const int64_t *ids,
                     int64_t n, int32_t update_octree, void *stream);
 int ro_mark_empty(ro_ctx *ctx, const ro_state *state, const int64_t *ids,

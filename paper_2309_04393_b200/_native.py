@@ -116,6 +116,7 @@ _SIGS = {
     "ro_extract_bricks": ([_p, _i32, _i32, _i32, _i32, _i32, _i32, _p, _p], _i32),
     "ro_node_minmax": ([_p, _p, _i32, _i32, _i32, _i32, _i32, _p, _p, _p], _i32),
     "ro_fill_metadata": ([_p, C.POINTER(State), _i32, _p, _i32, _i32, _i32, _i32, _p], _i32),
+    "ro_bricks_box_minmax": ([_p, _p, _i64, _i32, _i32, _i32, _p, _p, _p], _i32),
 }
 
 EXPORTED = tuple(_SIGS)

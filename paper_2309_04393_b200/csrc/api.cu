@@ -84,6 +84,8 @@ int node_minmax(ro_ctx *c, const uint8_t *vol, int32_t dx, int32_t dy, int32_t d
                 int32_t pad, uint8_t *mins, uint8_t *maxs, cudaStream_t s);
 int fill_metadata(ro_ctx *c, const ro_state *st, int32_t slot, const uint8_t *vol, int32_t dx,
                   int32_t dy, int32_t dz, int32_t pad, cudaStream_t s);
+int bricks_box_minmax(const uint8_t *bricks, const int32_t *boxes, int64_t n, int32_t bx,
+                      int32_t by, int32_t bz, uint8_t *mins, uint8_t *maxs, cudaStream_t s);
 
 static int check_state(const ro_ctx *c, const ro_state *st) {
     if (!c) return fail(RO_EINVAL, "null context");
@@ -298,6 +300,11 @@ int ro_fill_metadata(ro_ctx *c, const ro_state *st, int32_t slot, const uint8_t 
         dz != c->layout.level_dims[0][2])
         return fail(RO_EINVAL, "volume dims differ from level 0 of the layout");
     return fill_metadata(c, st, slot, volume, dx, dy, dz, pad, (cudaStream_t)stream);
+}
+
+int ro_bricks_box_minmax(const uint8_t *bricks, const int32_t *boxes, int64_t n, int32_t bx,
+                         int32_t by, int32_t bz, uint8_t *mins, uint8_t *maxs, void *stream) {
+    return bricks_box_minmax(bricks, boxes, n, bx, by, bz, mins, maxs, (cudaStream_t)stream);
 }
 
 int ro_evict_bricks(ro_ctx *c, const ro_state *st, const int64_t *ids, int64_t n,

@@ -115,6 +115,48 @@ __global__ void k_minmax_z(const uchar2 *__restrict__ in, int dz, int side, int 
     }
 }
 
+// octree.py:275-306 compute_node_metadata_from_bricks, the min / max part:
+// brick i contributes the voxels of its sub-box boxes[i] = x0,y0,z0,x1,y1,z1
+// (half-open, brick-local); one CTA per brick, block reduction.
+__global__ void k_brick_box_minmax(int64_t n, const uint8_t *__restrict__ bricks, int bx,
+                                   int by, int bz, const int32_t *__restrict__ boxes,
+                                   uint8_t *__restrict__ mins, uint8_t *__restrict__ maxs) {
+    __shared__ unsigned red[2][32];
+    const int64_t i = blockIdx.x;
+    if (i >= n) return;
+    const int32_t *b = boxes + i * 6;
+    const int x0 = b[0], y0 = b[1], z0 = b[2], x1 = b[3], y1 = b[4], z1 = b[5];
+    const int nx = max(x1 - x0, 0), ny = max(y1 - y0, 0), nz = max(z1 - z0, 0);
+    const int64_t cnt = (int64_t)nx * ny * nz;
+    const uint8_t *p = bricks + i * (int64_t)bx * by * bz;
+    unsigned mn = 255, mx = 0;
+    for (int64_t j = threadIdx.x; j < cnt; j += blockDim.x) {
+        const int x = x0 + (int)(j % nx), y = y0 + (int)((j / nx) % ny),
+                  z = z0 + (int)(j / ((int64_t)nx * ny));
+        const unsigned v = p[((int64_t)z * by + y) * bx + x];
+        mn = min(mn, v);
+        mx = max(mx, v);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        red[0][w] = mn;
+        red[1][w] = mx;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int q = 1; q < (int)(blockDim.x >> 5); ++q) {
+            mn = min(mn, red[0][q]);
+            mx = max(mx, red[1][q]);
+        }
+        mins[i] = (uint8_t)mn;  // 255 / 0 for an empty sub-box
+        maxs[i] = (uint8_t)mx;
+    }
+}
+
 unsigned grid_of(int64_t n) {
     int64_t b = (n + 255) / 256;
     if (b > 148 * 16) b = 148 * 16;
@@ -140,6 +182,16 @@ int node_minmax(ro_ctx *c, const uint8_t *vol, int32_t dx, int32_t dy, int32_t d
                                                                   side, pad, (uchar2 *)pb);
     k_minmax_z<<<grid_of((int64_t)side * side * side), 256, 0, s>>>((const uchar2 *)pb, dz, side,
                                                                     pad, mins, maxs);
+    RO_CUDA(cudaGetLastError());
+    return RO_OK;
+}
+
+int bricks_box_minmax(const uint8_t *bricks, const int32_t *boxes, int64_t n, int32_t bx,
+                      int32_t by, int32_t bz, uint8_t *mins, uint8_t *maxs, cudaStream_t s) {
+    if (n <= 0) return RO_OK;
+    if (!bricks || !boxes || !mins || !maxs) return fail(RO_EINVAL, "null array");
+    if (n > 0x7FFFFFFF) return fail(RO_EINVAL, "too many bricks");
+    k_brick_box_minmax<<<(unsigned)n, 256, 0, s>>>(n, bricks, bx, by, bz, boxes, mins, maxs);
     RO_CUDA(cudaGetLastError());
     return RO_OK;
 }

@@ -167,6 +167,65 @@ class ResidencyOctree:
                 for y in range(ranges[1][0], ranges[1][1] + 1)
                 for x in range(ranges[0][0], ranges[0][1] + 1)]
 
+    # -- metadata from bricks (octree.py:275-329) ----------------------------
+
+    def _voxel_ranges(self, addr: NodeAddress, level: int) -> list:
+        """Half-open voxel ranges of `level` whose open cells meet the node's
+        open extent (octree.py:316-329, exact integer form)."""
+        dims = self.paging.level_dims[level]
+        side = 1 << addr.d
+        node = (addr.x, addr.y, addr.z)
+        out = []
+        for a in range(3):
+            n = int(dims[a])
+            v0 = max(0, _floor_div(node[a] * n, side))
+            v1 = min(n, _ceil_div((node[a] + 1) * n, side))
+            out.append((v0, v1))
+        return out
+
+    def choose_metadata_level(self, addr: NodeAddress) -> int:
+        """Coarsest level whose footprint in the node meets
+        min_metadata_voxels (octree.py:307-314)."""
+        for level in range(self.paging.config.k - 1, -1, -1):
+            count = 1
+            for v0, v1 in self._voxel_ranges(addr, level):
+                count *= max(0, v1 - v0)
+            if count >= self.config.min_metadata_voxels:
+                return level
+        return 0
+
+    def compute_node_metadata_from_bricks(self, addr: NodeAddress, slot: int, fetch):
+        """Min / max over the node's extent at choose_metadata_level, from the
+        overlapping bricks (octree.py:275-306).  fetch(slot, level, coord)
+        returns a payload (numpy or torch); it may raise, leaving the node
+        INVALID.  The reduction runs on the device (ro_bricks_box_minmax)."""
+        level = self.choose_metadata_level(addr)
+        dims = [int(v) for v in self.paging.level_dims[level]]
+        B = self.paging.config.brick_size
+        vr = self._voxel_ranges(addr, level)
+        coords, boxes = [], []
+        for coord in self.bricks_overlapping(addr, level):
+            box = []
+            for a in range(3):
+                c0 = coord[a] * B[a]
+                box.append((max(vr[a][0], c0) - c0, min(vr[a][1], c0 + B[a], dims[a]) - c0))
+            if any(lo >= hi for lo, hi in box):
+                continue
+            coords.append(coord)
+            boxes.append([box[0][0], box[1][0], box[2][0], box[0][1], box[1][1], box[2][1]])
+        if not coords:
+            return 0, 0  # the extent met no in-volume voxels
+        dev = self.paging.device
+        pays = torch.stack([torch.as_tensor(fetch(slot, level, c)).to(dev).reshape(
+            B[2], B[1], B[0]) for c in coords]).contiguous()
+        bx_ = torch.as_tensor(np.array(boxes, dtype=np.int32)).to(dev)
+        mins = torch.empty(len(coords), dtype=torch.uint8, device=dev)
+        maxs = torch.empty(len(coords), dtype=torch.uint8, device=dev)
+        N.check(N.lib().ro_bricks_box_minmax(pays.data_ptr(), bx_.data_ptr(), len(coords),
+                                             B[0], B[1], B[2], mins.data_ptr(),
+                                             maxs.data_ptr(), N.stream_ptr()))
+        return int(mins.min().item()), int(maxs.max().item())
+
     # -- residency updates (native) -----------------------------------------
 
     def update_for_bricks(self, brick_ids):
@@ -209,6 +268,43 @@ class ResidencyOctree:
 
     def is_valid(self, addr, slot) -> bool:
         return self.metadata(addr, slot) is not None
+
+    def is_empty(self, addr: NodeAddress, slots, tfs: dict) -> bool:
+        """octree.py:333-342: every slot has valid metadata whose range maps
+        to zero opacity under that slot's transfer function."""
+        for slot in slots:
+            meta = self.metadata(addr, slot)
+            if meta is None or tfs[slot].interval_max_opacity(meta[0], meta[1]) != 0.0:
+                return False
+        return True
+
+    def is_homogeneous(self, addr: NodeAddress, slots) -> bool:
+        """octree.py:344-351"""
+        for slot in slots:
+            meta = self.metadata(addr, slot)
+            if meta is None or meta[1] - meta[0] > self.config.homogeneity_eps:
+                return False
+        return True
+
+    def overlapping_leaves(self, box_lo, box_hi) -> list:
+        """octree.py:126-147: leaves whose open extent meets the open box
+        (coordinates as Fractions, ints or floats; exact)."""
+        from fractions import Fraction
+        import math
+        side = 1 << self.config.depth
+        ranges = []
+        for a in range(3):
+            lo = Fraction(box_lo[a]) * side
+            hi = Fraction(box_hi[a]) * side
+            i_lo = max(0, math.floor(lo))
+            i_hi = min(side - 1, math.ceil(hi) - 1)
+            if i_lo > i_hi:
+                return []
+            ranges.append((i_lo, i_hi))
+        D = self.config.depth
+        return [NodeAddress(D, x, y, z) for z in range(ranges[2][0], ranges[2][1] + 1)
+                for y in range(ranges[1][0], ranges[1][1] + 1)
+                for x in range(ranges[0][0], ranges[0][1] + 1)]
 
     def set_node_metadata(self, addr: NodeAddress, slot: int, min_val: int, max_val: int):
         self.set_metadata_batch([addr.index], [slot], [min_val], [max_val])

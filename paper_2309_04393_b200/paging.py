@@ -421,6 +421,26 @@ class MultiChannelPaging:
         N.check(N.lib().ro_evict_bricks(self.ctx, C.byref(st), ids.ctypes.data, len(ids),
                                         1 if update_octree else 0, N.stream_ptr()))
 
+    def sample(self, slot, local_coord) -> float:
+        """paging.py:241-261: trilinear value of one cache slot at a
+        brick-local coordinate (query helper; reads that slot's brick)."""
+        brick = self.cache_dev[self.slot_linear(slot)].double().cpu().numpy()
+        sx, sy, sz = self.config.brick_size
+        lx = min(max(local_coord[0] - 0.5, 0.0), sx - 1.0)
+        ly = min(max(local_coord[1] - 0.5, 0.0), sy - 1.0)
+        lz = min(max(local_coord[2] - 0.5, 0.0), sz - 1.0)
+        x0, y0, z0 = int(lx), int(ly), int(lz)
+        x1, y1, z1 = min(x0 + 1, sx - 1), min(y0 + 1, sy - 1), min(z0 + 1, sz - 1)
+        fx, fy, fz = lx - x0, ly - y0, lz - z0
+
+        def lerp(a, b, t):
+            return a + (b - a) * t
+        c00 = lerp(brick[z0, y0, x0], brick[z0, y0, x1], fx)
+        c10 = lerp(brick[z0, y1, x0], brick[z0, y1, x1], fx)
+        c01 = lerp(brick[z1, y0, x0], brick[z1, y0, x1], fx)
+        c11 = lerp(brick[z1, y1, x0], brick[z1, y1, x1], fx)
+        return float(lerp(lerp(c00, c10, fy), lerp(c01, c11, fy), fz))
+
     def set_channel_mapping(self, channel_slot, dataset_channel, channel_count=None,
                             _invalidate_octree: bool = False):
         if not 0 <= channel_slot < self.config.m:
