@@ -39,6 +39,9 @@
  *   ro_node_minmax       service.py:102-115 region_min_max / engine.py:186-219
  *                        _box_minmax_grid (one tree level, device volume)
  *   ro_fill_metadata     engine.py:138-152 fill_metadata_from_volumes
+ *   ro_upload_state / ro_download_state
+ *                        reference-layout state (paging.py:95-112,
+ *                        octree.py:116-118) <-> device state
  *
  * Errors: every call returns 0 on success or a negative RO_E* code; the
  * message is available from ro_last_error() (thread-local).  Asynchronous
@@ -302,6 +305,34 @@ int ro_octree_update(ro_ctx *ctx, const ro_state *state, const int64_t *ids,
                      int64_t n, void *stream);
 
 int ro_rebuild_masks(ro_ctx *ctx, const ro_state *state, void *stream);
+
+/* Reference-layout state on the HOST (paging.py:95-112 arrays,
+   octree.py:116-118 words): pt_status i8[E] (0 UNMAPPED, 1 MAPPED, 2 EMPTY)
+   + pt_slot i32[E], words u32[N*m] (may be NULL), cache u8[S*bvox],
+   slot_brick / slot_last_used i64[S], the LIFO free list (top last). */
+typedef struct ro_host_state {
+    const int8_t *pt_status;
+    const int32_t *pt_slot;
+    const uint32_t *words;
+    const uint8_t *cache;
+    const int64_t *slot_brick;
+    const int64_t *slot_last_used;
+    const int32_t *free_list;
+    int64_t free_count;
+} ro_host_state;
+
+/* Copy a reference-layout host state into the device state (packing the
+   page table; sub_max, if present, is rebuilt from the cache).  Synchronises
+   the stream. */
+int ro_upload_state(ro_ctx *ctx, const ro_host_state *host, const ro_state *state,
+                    void *stream);
+/* The inverse (host arrays written: pt_status, pt_slot, words, cache,
+   slot_brick, slot_last_used, free_list; *free_count_out = free count).
+   Synchronises the stream. */
+int ro_download_state(ro_ctx *ctx, const ro_state *state, int8_t *pt_status,
+                      int32_t *pt_slot, uint32_t *words, uint8_t *cache,
+                      int64_t *slot_brick, int64_t *slot_last_used, int32_t *free_list,
+                      int64_t *free_count_out, void *stream);
 
 int ro_sync(ro_ctx *ctx, void *stream);
 

@@ -55,6 +55,12 @@ class State(C.Structure):
                 ("sub_max", _p)]
 
 
+class HostState(C.Structure):
+    _fields_ = [("pt_status", _p), ("pt_slot", _p), ("words", _p), ("cache", _p),
+                ("slot_brick", _p), ("slot_last_used", _p), ("free_list", _p),
+                ("free_count", _i64)]
+
+
 class Channel(C.Structure):
     _fields_ = [("slot", _i32), ("lo", _i32), ("hi", _i32), ("npoints", _i32),
                 ("tf_x", _d * RO_MAX_TF_POINTS),
@@ -108,6 +114,8 @@ _SIGS = {
     "ro_octree_update": ([_p, C.POINTER(State), _p, _i64, _p], _i32),
     "ro_rebuild_masks": ([_p, C.POINTER(State), _p], _i32),
     "ro_sync": ([_p, _p], _i32),
+    "ro_upload_state": ([_p, C.POINTER(HostState), C.POINTER(State), _p], _i32),
+    "ro_download_state": ([_p, C.POINTER(State), _p, _p, _p, _p, _p, _p, _p, _p, _p], _i32),
     "ro_apply_bricks_lz4": ([_p, C.POINTER(State), _p, _i64, _p, _p, _i32, _i64, _i32, _p,
                              _p, _p], _i32),
     "ro_lz4_decode": ([_p, _p, _p, _i64, _p, _i64, _i64, _p, _p], _i32),

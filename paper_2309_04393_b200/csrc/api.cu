@@ -3,6 +3,8 @@
 #include <cstring>
 #include <string>
 
+#include <vector>
+
 #include "internal.cuh"
 
 namespace ro {
@@ -86,6 +88,7 @@ int fill_metadata(ro_ctx *c, const ro_state *st, int32_t slot, const uint8_t *vo
                   int32_t dy, int32_t dz, int32_t pad, cudaStream_t s);
 int bricks_box_minmax(const uint8_t *bricks, const int32_t *boxes, int64_t n, int32_t bx,
                       int32_t by, int32_t bz, uint8_t *mins, uint8_t *maxs, cudaStream_t s);
+int rebuild_sub_max(ro_ctx *c, const ro_state *st, cudaStream_t s);
 
 static int check_state(const ro_ctx *c, const ro_state *st) {
     if (!c) return fail(RO_EINVAL, "null context");
@@ -359,6 +362,85 @@ int ro_rebuild_masks(ro_ctx *c, const ro_state *st, void *stream) {
     int rc = check_state(c, st);
     if (rc) return rc;
     return rebuild_masks(c, st, (cudaStream_t)stream);
+}
+
+int ro_upload_state(ro_ctx *c, const ro_host_state *h, const ro_state *st, void *stream) {
+    int rc = check_state(c, st);
+    if (rc) return rc;
+    if (!h || !h->pt_status || !h->pt_slot || !h->slot_brick || !h->slot_last_used ||
+        (h->free_count > 0 && !h->free_list))
+        return fail(RO_EINVAL, "incomplete host state");
+    if (h->free_count < 0 || h->free_count > c->S) return fail(RO_EINVAL, "bad free count");
+    cudaStream_t s = (cudaStream_t)stream;
+    std::vector<int32_t> pt((size_t)c->E);
+    for (int64_t e = 0; e < c->E; ++e) {
+        const int8_t stt = h->pt_status[e];
+        if (stt == 1) {
+            if (h->pt_slot[e] < 0 || h->pt_slot[e] >= c->S)
+                return fail(RO_EINVAL, "MAPPED entry with a slot outside the cache");
+            pt[(size_t)e] = h->pt_slot[e];
+        } else if (stt == 2) {
+            pt[(size_t)e] = RO_PT_EMPTY;
+        } else if (stt == 0) {
+            pt[(size_t)e] = RO_PT_UNMAPPED;
+        } else {
+            return fail(RO_EINVAL, "pt_status must be 0, 1 or 2");
+        }
+    }
+    RO_CUDA(cudaMemcpyAsync(st->pt, pt.data(), sizeof(int32_t) * c->E, cudaMemcpyHostToDevice, s));
+    if (h->words && st->words)
+        RO_CUDA(cudaMemcpyAsync(st->words, h->words, sizeof(uint32_t) * c->num_nodes * c->layout.m,
+                                cudaMemcpyHostToDevice, s));
+    if (h->cache && st->cache)
+        RO_CUDA(cudaMemcpyAsync(st->cache, h->cache, (size_t)c->S * c->bvox,
+                                cudaMemcpyHostToDevice, s));
+    RO_CUDA(cudaMemcpyAsync(st->slot_brick, h->slot_brick, sizeof(int64_t) * c->S,
+                            cudaMemcpyHostToDevice, s));
+    RO_CUDA(cudaMemcpyAsync(st->slot_last_used, h->slot_last_used, sizeof(int64_t) * c->S,
+                            cudaMemcpyHostToDevice, s));
+    if (h->free_count > 0)
+        RO_CUDA(cudaMemcpyAsync(st->free_stack, h->free_list, sizeof(int32_t) * h->free_count,
+                                cudaMemcpyHostToDevice, s));
+    const int32_t fc = (int32_t)h->free_count;
+    RO_CUDA(cudaMemcpyAsync(st->free_count, &fc, sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    if (h->cache && st->cache && (rc = rebuild_sub_max(c, st, s))) return rc;
+    RO_CUDA(cudaStreamSynchronize(s));
+    return RO_OK;
+}
+
+int ro_download_state(ro_ctx *c, const ro_state *st, int8_t *pt_status, int32_t *pt_slot,
+                      uint32_t *words, uint8_t *cache, int64_t *slot_brick,
+                      int64_t *slot_last_used, int32_t *free_list, int64_t *free_count_out,
+                      void *stream) {
+    int rc = check_state(c, st);
+    if (rc) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    std::vector<int32_t> pt((size_t)c->E);
+    int32_t fc = 0;
+    RO_CUDA(cudaMemcpyAsync(pt.data(), st->pt, sizeof(int32_t) * c->E, cudaMemcpyDeviceToHost, s));
+    RO_CUDA(cudaMemcpyAsync(&fc, st->free_count, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    if (words && st->words)
+        RO_CUDA(cudaMemcpyAsync(words, st->words, sizeof(uint32_t) * c->num_nodes * c->layout.m,
+                                cudaMemcpyDeviceToHost, s));
+    if (cache && st->cache)
+        RO_CUDA(cudaMemcpyAsync(cache, st->cache, (size_t)c->S * c->bvox, cudaMemcpyDeviceToHost,
+                                s));
+    if (slot_brick)
+        RO_CUDA(cudaMemcpyAsync(slot_brick, st->slot_brick, sizeof(int64_t) * c->S,
+                                cudaMemcpyDeviceToHost, s));
+    if (slot_last_used)
+        RO_CUDA(cudaMemcpyAsync(slot_last_used, st->slot_last_used, sizeof(int64_t) * c->S,
+                                cudaMemcpyDeviceToHost, s));
+    RO_CUDA(cudaStreamSynchronize(s));
+    if (free_list && fc > 0)
+        RO_CUDA(cudaMemcpy(free_list, st->free_stack, sizeof(int32_t) * fc, cudaMemcpyDeviceToHost));
+    if (free_count_out) *free_count_out = fc;
+    for (int64_t e = 0; e < c->E; ++e) {
+        const int32_t v = pt[(size_t)e];
+        if (pt_status) pt_status[e] = v >= 0 ? 1 : (v == RO_PT_EMPTY ? 2 : 0);
+        if (pt_slot) pt_slot[e] = v >= 0 ? v : -1;
+    }
+    return RO_OK;
 }
 
 int ro_sync(ro_ctx *c, void *stream) {

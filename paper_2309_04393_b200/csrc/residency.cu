@@ -239,6 +239,32 @@ __global__ void k_sequential_insert(const DevLayout L, int32_t n,
     }
 }
 
+// sub_max of every slot from the cache (ro_upload_state)
+__global__ void k_sub_max_all(int64_t S, int bx, int by, int bz, const uint8_t *__restrict__ cache,
+                              const int64_t *__restrict__ slot_brick,
+                              uint8_t *__restrict__ sub_max) {
+    const int nx = bx >> RO_SUB_LOG, ny = by >> RO_SUB_LOG, nz = bz >> RO_SUB_LOG,
+              nsb = nx * ny * nz;
+    constexpr int E = RO_SUB_E;
+    const int64_t bvox = (int64_t)bx * by * bz;
+    for (int64_t i = blockIdx.x; i < S; i += gridDim.x) {
+        const uint8_t *b = cache + i * bvox;
+        const bool occupied = slot_brick[i] >= 0;
+        for (int q = threadIdx.x; q < nsb; q += blockDim.x) {
+            unsigned mx = 255;
+            if (occupied) {
+                const int sx = q % nx, sy = (q / nx) % ny, sz = q / (nx * ny);
+                mx = 0;
+                for (int z = max(E * sz - 1, 0); z < min(E * sz + E + 1, bz); ++z)
+                    for (int y = max(E * sy - 1, 0); y < min(E * sy + E + 1, by); ++y)
+                        for (int x = max(E * sx - 1, 0); x < min(E * sx + E + 1, bx); ++x)
+                            mx = max(mx, (unsigned)b[((int64_t)z * by + y) * bx + x]);
+            }
+            sub_max[i * nsb + q] = (uint8_t)mx;
+        }
+    }
+}
+
 // explicit eviction / mark_empty (sequential: duplicates are no-ops)
 __global__ void k_release(const DevLayout L, int32_t n, const int64_t *__restrict__ ids,
                           int32_t new_status, int32_t *__restrict__ pt,
@@ -822,6 +848,18 @@ int rebuild_masks(ro_ctx *c, const ro_state *st, cudaStream_t s) {
     k_rebuild_leaves<<<kGridStride, kThreads, 0, s>>>(c->dl, st->pt, st->words);
     for (int dd = D - 1; dd >= 0; --dd)
         k_rebuild_level<<<kGridStride, kThreads, 0, s>>>(c->dl, dd, st->words);
+    RO_CUDA(cudaGetLastError());
+    return RO_OK;
+}
+
+int rebuild_sub_max(ro_ctx *c, const ro_state *st, cudaStream_t s) {
+    if (!st->sub_max || c->layout.brick[0] < RO_SUB_E || c->layout.brick[1] < RO_SUB_E ||
+        c->layout.brick[2] < RO_SUB_E)
+        return RO_OK;
+    const int64_t S = c->S;
+    const unsigned g = (unsigned)(S < 148 * 64 ? S : 148 * 64);
+    k_sub_max_all<<<g, 128, 0, s>>>(S, c->layout.brick[0], c->layout.brick[1],
+                                    c->layout.brick[2], st->cache, st->slot_brick, st->sub_max);
     RO_CUDA(cudaGetLastError());
     return RO_OK;
 }

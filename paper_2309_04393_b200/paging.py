@@ -461,6 +461,28 @@ class MultiChannelPaging:
     def occupied_slot_count(self) -> int:
         return int((self.slot_brick_dev >= 0).sum().item())
 
+    def load_reference_state(self, pt_status, pt_slot, cache, slot_brick, slot_last_used,
+                             free_list, words=None):
+        """Adopt a reference-layout host state (paging.py:95-112 arrays, and
+        octree.py:116-118 words if given) through ro_upload_state."""
+        arr = dict(
+            pt_status=np.ascontiguousarray(pt_status, dtype=np.int8),
+            pt_slot=np.ascontiguousarray(pt_slot, dtype=np.int32),
+            cache=np.ascontiguousarray(cache, dtype=np.uint8),
+            slot_brick=np.ascontiguousarray(slot_brick, dtype=np.int64),
+            slot_last_used=np.ascontiguousarray(slot_last_used, dtype=np.int64),
+            free_list=np.ascontiguousarray(free_list, dtype=np.int32))
+        if arr["pt_status"].size != self.total_entries or arr["slot_brick"].size != self.num_slots:
+            raise PagingError("reference state does not match this layout")
+        w = None if words is None else np.ascontiguousarray(words, dtype=np.uint32)
+        h = N.HostState(arr["pt_status"].ctypes.data, arr["pt_slot"].ctypes.data,
+                        w.ctypes.data if w is not None else None, arr["cache"].ctypes.data,
+                        arr["slot_brick"].ctypes.data, arr["slot_last_used"].ctypes.data,
+                        arr["free_list"].ctypes.data if arr["free_list"].size else None,
+                        int(arr["free_list"].size))
+        st = self.state(with_words=w is not None)
+        N.check(N.lib().ro_upload_state(self.ctx, C.byref(h), C.byref(st), N.stream_ptr()))
+
     def check_bijection(self):
         p = self.pt.cpu().numpy()
         sb = self.slot_brick

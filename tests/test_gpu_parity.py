@@ -652,3 +652,39 @@ def test_gpu_capacity_mode_parts_converge_to_single_gpu_image():
     # each part caches only what its own rows need
     assert max(resident) < single.engine.paging.occupied_slot_count() <= sum(resident)
     single.close()
+
+
+def test_gpu_upload_reference_state_through_c_abi():
+    """INTEGRATION.md path B: a reference-layout state (pt_status + pt_slot,
+    words, cache, LRU arrays, free list) adopted through ro_upload_state
+    renders the reference's golden frames; ro_download_state returns it."""
+    import ctypes as C
+    from oracle.session import prepare_full
+    from paper_2309_04393_b200 import Engine, EngineConfig, orbit_pose, render_frame
+    from paper_2309_04393_b200 import _native as N
+    from paper_2309_04393_b200.volume import box_minmax_grid
+    meta, rec = load_golden("vessel256_full")
+    e = meta["engine"]
+    st = scenes.store("vessel256")
+    ref = prepare_full(st, {0: 0}, 1, e["depth"], e["cache_slots"], e["pad"], box_minmax_grid)
+    eng = Engine(st.manifest, EngineConfig(octree_depth=e["depth"],
+                                           cache_slots=tuple(e["cache_slots"]), channel_slots=1))
+    eng.paging.load_reference_state(ref.pt_status, ref.pt_slot, ref.cache, ref.slot_brick,
+                                    ref.slot_last_used, ref.free, words=ref.words)
+    assert not diff_hashes(device_state_hashes(eng), meta["state"])
+    chans = scenes.product_channels(meta["channels"])
+    cfg = scenes.render_config(meta["render"])
+    for i, a in enumerate(meta["angles"][:2]):
+        out = render_frame(eng.paging, eng.octree, chans, orbit_pose(a), cfg)
+        assert not _check(rec, f"res{i}_", out), i
+    p = eng.paging
+    E, S = p.total_entries, p.num_slots
+    ps, sl = np.zeros(E, np.int8), np.zeros(E, np.int32)
+    sb, lu = np.zeros(S, np.int64), np.zeros(S, np.int64)
+    fl, fc = np.zeros(S, np.int32), C.c_int64(0)
+    N.check(N.lib().ro_download_state(p.ctx, C.byref(p.state()), ps.ctypes.data, sl.ctypes.data,
+                                      None, None, sb.ctypes.data, lu.ctypes.data, fl.ctypes.data,
+                                      C.byref(fc), N.stream_ptr()))
+    assert np.array_equal(ps, ref.pt_status) and np.array_equal(sl, ref.pt_slot)
+    assert np.array_equal(sb, ref.slot_brick) and np.array_equal(lu, ref.slot_last_used)
+    assert list(fl[:fc.value]) == list(ref.free)

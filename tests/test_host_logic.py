@@ -31,7 +31,8 @@ def test_ctypes_structs_match_c_layout():
     equals the ctypes mirror."""
     from paper_2309_04393_b200 import _native as N
     structs = {"ro_layout": N.Layout, "ro_state": N.State, "ro_channel": N.Channel,
-               "ro_frame": N.Frame, "ro_outputs": N.Outputs, "ro_feedback": N.Feedback}
+               "ro_frame": N.Frame, "ro_outputs": N.Outputs, "ro_feedback": N.Feedback,
+               "ro_host_state": N.HostState}
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "resoct.h"',
              'int main(void) {']
     for cname, py in structs.items():
