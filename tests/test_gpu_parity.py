@@ -688,3 +688,76 @@ def test_gpu_upload_reference_state_through_c_abi():
     assert np.array_equal(ps, ref.pt_status) and np.array_equal(sl, ref.pt_slot)
     assert np.array_equal(sb, ref.slot_brick) and np.array_equal(lu, ref.slot_last_used)
     assert list(fl[:fc.value]) == list(ref.free)
+
+
+def _random_tf(rng):
+    from paper_2309_04393_b200 import TransferFunction
+    n = int(rng.integers(2, 7))
+    xs = np.sort(rng.choice(np.arange(0, 256), size=n, replace=False)).astype(float)
+    pts = []
+    for x in xs:
+        a = 0.0 if rng.random() < 0.35 else float(rng.uniform(0.01, 1.0))
+        pts.append((float(x), (float(rng.random()), float(rng.random()),
+                               float(rng.random()), a)))
+    return TransferFunction(points=tuple(pts))
+
+
+@pytest.mark.parametrize("seed", list(range(int(__import__("os").environ.get("RESOCT_FUZZ_N",
+                                                                             "24")))))
+def test_gpu_randomized_frames_match_oracle(seed):
+    """Randomised sweep beyond the golden scenes: random residency and INVALID
+    metadata, random TFs / level ranges / channel order / eps, odd image sizes
+    with exactly axis-aligned centre rays (the |d| < 1e-12 box branches),
+    cameras inside the volume, random t0 / start level / early termination /
+    budget.  Everything bit-exact against the C oracle."""
+    from oracle import raycast as orc
+    from paper_2309_04393_b200 import Camera, ChannelSettings, RenderConfig, render_frame
+    rng = np.random.default_rng(1000 + seed)
+    m = int(rng.integers(1, 5))
+    depth = int(rng.integers(2, 5))
+    eps = float(rng.choice([0.0, 3.0, 12.0]))
+    eng = _random_partial_engine(seed, eps=eps, depth=depth, m=m)
+    k = eng.paging.config.k
+    chans = []
+    for s in rng.permutation(m):
+        lo = int(rng.integers(0, k))
+        hi = int(rng.integers(lo, k))
+        chans.append(ChannelSettings(slot=int(s), tf=_random_tf(rng), level_range=(lo, hi)))
+    kind = seed % 3
+    if kind == 0:      # axis-aligned view, odd size: the centre ray has dx = dy = 0
+        cam = Camera(position=(0.5, 0.5, -1.2), target=(0.5, 0.5, 0.5), up=(0.0, 1.0, 0.0),
+                     fov_deg=40.0)
+        dims = (int(rng.integers(8, 20)) * 2 + 1, int(rng.integers(6, 16)) * 2 + 1)
+    elif kind == 1:    # camera inside the volume
+        pos = tuple(float(v) for v in rng.uniform(0.2, 0.8, 3))
+        cam = Camera(position=pos, target=(0.5, 0.5, 0.5 + 1e-3 if pos == (0.5,) * 3 else 0.5),
+                     up=(0.0, 0.0, 1.0), fov_deg=float(rng.uniform(30, 90)))
+        dims = (int(rng.integers(16, 40)), int(rng.integers(12, 30)))
+    else:              # random outside orbit
+        a = float(rng.uniform(0, 6.28))
+        r = float(rng.uniform(1.2, 2.6))
+        cam = Camera(position=(0.5 + r * np.cos(a), 0.5 + float(rng.uniform(-0.8, 0.8)),
+                               0.5 + r * np.sin(a)), target=(0.5, 0.5, 0.5), fov_deg=45.0)
+        dims = (int(rng.integers(16, 48)), int(rng.integers(12, 36)))
+    cfg = RenderConfig(image_dims=dims, base_step=float(rng.choice([1 / 32, 1 / 50, 1 / 64, 1 / 100])),
+                       lod_reference_distance=float(rng.choice([0.5, 1.0, 1.7])),
+                       early_term_alpha=float(rng.choice([0.5, 0.99, 1.0])),
+                       max_requests_per_frame=int(rng.integers(1, 400)),
+                       traversal_start_level=int(rng.integers(0, 4)))
+    out = render_frame(eng.paging, eng.octree, chans, cam, cfg)
+    ost = oracle_state_from_device(eng)
+    och = [orc.OracleChannel(slot=c.slot, points=c.tf.points, level_range=c.level_range)
+           for c in chans]
+    want = orc.render(ost, och, cam_tuple(cam), dims, cfg.base_step,
+                      t0=cfg.lod_reference_distance, early_alpha=cfg.early_term_alpha,
+                      budget=cfg.max_requests_per_frame,
+                      start_level=cfg.traversal_start_level)
+    assert np.array_equal(out.image, want.image), (
+        int((out.image != want.image).sum()), float(np.abs(out.image - want.image).max()))
+    assert out.brick_requests == want.brick_requests
+    assert out.metadata_requests == want.metadata_requests
+    assert np.array_equal(out.required_mask, want.required_mask)
+    assert np.array_equal(out.level_histogram, want.level_histogram)
+    assert np.array_equal(out.pixel_required, want.pixel_required)
+    assert [out.stats.traversal_steps, out.stats.samples_evaluated,
+            out.stats.samples_skipped] == list(want.counters[:3])
