@@ -37,14 +37,8 @@
 #ifndef RO_PERSISTENT
 #define RO_PERSISTENT 1
 #endif
-#ifndef RO_FIXED_STRIDE
-#define RO_FIXED_STRIDE 0
-#endif
 #ifndef RO_SUBMAX
 #define RO_SUBMAX 1
-#endif
-#ifndef RO_NCH_FAST
-#define RO_NCH_FAST 0
 #endif
 #ifndef RO_WARPS
 #define RO_WARPS 4
@@ -55,19 +49,8 @@
 #ifndef RO_TILE_H
 #define RO_TILE_H 8
 #endif
-#ifndef RO_SUBCACHE
-#define RO_SUBCACHE 0
-#endif
 #ifndef RO_FAST_DESCENT
 #define RO_FAST_DESCENT 1
-#endif
-#ifndef RO_RARE_NOINLINE
-#define RO_RARE_NOINLINE 0
-#endif
-#if RO_RARE_NOINLINE
-#define RARE __noinline__
-#else
-#define RARE __forceinline__
 #endif
 
 namespace ro {
@@ -231,7 +214,7 @@ __device__ __forceinline__ void axis_box(double o, double d, double &tmin,
 // each touched entry once.
 // Fire-and-forget (RED.MIN): the lane never waits on the L2 round trip;
 // feedback.cu finds the touched entries by scanning the key arrays.
-RARE __device__ void request(unsigned long long *keys, int32_t *, int32_t *,
+__device__ __forceinline__ void request(unsigned long long *keys, int32_t *, int32_t *,
                              int32_t entry, unsigned long long key) {
     atomicMin(keys + entry, key);
 }
@@ -271,7 +254,7 @@ __device__ __forceinline__ void level_pos(LevelPos &lp, int lev, double px, doub
 // kernels.py:518-549: nearest resident level in the node's mask, coarser
 // first on ties; returns (level, cache slot) or level -1.  The position of
 // the chosen level is left in `lp2` (a one-entry cache across channels).
-RARE __device__ int2 substitute(const int32_t *__restrict__ pt, const FrameSmem &S, int ci,
+__device__ __forceinline__ int2 substitute(const int32_t *__restrict__ pt, const FrameSmem &S, int ci,
                                 int lev, int k, uint32_t mask, double px, double py,
                                 double pz, int lbx, int lby, int lbz, LevelPos &lp2) {
     // Visit the levels present in the mask in the reference's order
@@ -372,17 +355,15 @@ struct SampleCtx {
     Taps tp;       // tap offsets / weights of tp_lev
     int tp_lev;
     LevelPos lp2;  // the last substitute level (kernels.py:518-549)
-    Taps tp2;
-    int tp2_lev;
 };
 
-template <int MODE, bool CHECK, int BX, int BY, int NCH>
+template <int MODE, bool CHECK, int BX, int BY>
 __global__ void __launch_bounds__(kBlock, RO_MINB * 4 / kWarps)
 k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A) {
     __shared__ FrameSmem S;
     extern __shared__ int32_t dyn[];  // per-thread channel state
     const int tid = threadIdx.x;
-    const int n_ch = NCH > 0 ? NCH : F.n_ch;  // NCH: compile-time channel count
+    const int n_ch = F.n_ch;
     const int k = A.L.k;
     const int m = A.L.m;
 
@@ -450,13 +431,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
         S.eps_i = F.eps_h >= 255.0 ? 255 : (F.eps_h < 0.0 ? -1 : (int)F.eps_h);
     }
     // per-thread arrays: [ci*kBlock + tid]
-#if RO_FIXED_STRIDE
-    // constant array offsets (sized for RO_MAX_CH): every access is
-    // tid*4 + ci*512 + an immediate
-    constexpr int kChStride = RO_MAX_CH * kBlock;
-#else
     const int kChStride = n_ch * kBlock;
-#endif
     int32_t *prev_brick = dyn;                        // n_ch
     int32_t *last_breq = prev_brick + kChStride;      // n_ch
     int32_t *last_mreq = last_breq + kChStride;       // n_ch
@@ -559,7 +534,6 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
             sc.lp.lev = -1;
             sc.tp_lev = -1;
             sc.lp2.lev = -1;
-            sc.tp2_lev = -1;
             // channel contributions, accumulated in the reference's channel
             // order the moment each channel resolves (kernels.py:637-681)
             double sR = 0.0, sG = 0.0, sB = 0.0, trans = 1.0;
@@ -624,14 +598,9 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
             auto sample2 = [&](int ci, int lev, int slot_lin) {
                 account(ci, lev, sc.lp2);
                 if (sub_skip(ci, slot_lin, sc.lp2)) return;
-#if RO_SUBCACHE
-                if (sc.tp2_lev != lev) { taps_of(sc.tp2, sc.lp2, bx, by, bz, S); sc.tp2_lev = lev; }
-                finish(ci, slot_lin, sc.tp2);
-#else
                 Taps t2;
                 taps_of(t2, sc.lp2, bx, by, bz, S);
                 finish(ci, slot_lin, t2);
-#endif
             };
 
             // sample channel ci from `slot_lin` at level `lev` (any level)
@@ -645,7 +614,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                 // up to the exit of their brick box
                 bool all_empty = true;
                 skip_exit = 1e30;
-#pragma unroll(NCH > 0 ? NCH : 1)
+#pragma unroll 1
                 for (int ci = 0; ci < n_ch; ++ci) {
                     const int lev = clampi(raw, S.lo[ci], S.hi[ci]);
                     if (sc.lp.lev != lev) level_pos(sc.lp, lev, px, py, pz, S, lbx, lby, lbz);
@@ -684,7 +653,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                 const int qx = (int)(px * cside), qy = (int)(py * cside), qz = (int)(pz * cside);
                 bool all_empty = true;
                 int deep_d = -1, dix = 0, diy = 0, diz = 0;
-#pragma unroll(NCH > 0 ? NCH : 1)
+#pragma unroll 1
                 for (int ci = 0; ci < n_ch; ++ci) {
                     const int slot = S.slot[ci];
                     const int lev = clampi(raw, S.lo[ci], S.hi[ci]);
@@ -735,7 +704,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                                          (dix + 1) * s, (diy + 1) * s, (diz + 1) * s);
                 }
             } else if (MODE == RO_MODE_REFERENCE) {  // kernels.py:301-314
-#pragma unroll(NCH > 0 ? NCH : 1)
+#pragma unroll 1
                 for (int ci = 0; ci < n_ch; ++ci) {
                     const int lev = clampi(raw, S.lo[ci], S.hi[ci]);
                     if (sc.lp.lev != lev) level_pos(sc.lp, lev, px, py, pz, S, lbx, lby, lbz);
@@ -792,7 +761,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                     d = d0 + stop;
                 }
 #endif
-#pragma unroll(NCH > 0 ? NCH : 1)
+#pragma unroll 1
                 for (int ci = 0; ci < n_ch; ++ci) {
                     const int slot = S.slot[ci];
                     while (true) {
@@ -1001,7 +970,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
     }
 }
 
-template <int MODE, bool CHECK, int BX, int BY, int NCH = 0>
+template <int MODE, bool CHECK, int BX, int BY>
 cudaError_t launch_b(const ro_frame &F, const RayArgs &A, cudaStream_t s) {
     int n_tiles = ((F.width + kTileW - 1) / kTileW) * ((A.local_rows + kTileH - 1) / kTileH);
     static int sm_count = 0;
@@ -1010,12 +979,8 @@ cudaError_t launch_b(const ro_frame &F, const RayArgs &A, cudaStream_t s) {
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev);
     }
-#if RO_FIXED_STRIDE
-    size_t dyn = (size_t)RO_MAX_CH * kBlock * 4 * 3 + (size_t)F.n_ch * A.L.k * kBlock * 4;
-#else
     size_t dyn = (size_t)F.n_ch * kBlock * 4 * 3 + (size_t)F.n_ch * A.L.k * kBlock * 4;
-#endif
-    auto kern = k_raycast<MODE, CHECK, BX, BY, NCH>;
+    auto kern = k_raycast<MODE, CHECK, BX, BY>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)dyn);
     if (e != cudaSuccess) return e;
@@ -1036,11 +1001,6 @@ cudaError_t launch_b(const ro_frame &F, const RayArgs &A, cudaStream_t s) {
 // brick sizes with compile-time tap offsets; anything else uses runtime ones
 template <int MODE, bool CHECK>
 cudaError_t launch(const ro_frame &F, const RayArgs &A, cudaStream_t s) {
-#if RO_NCH_FAST
-    if (MODE == RO_MODE_RESIDENCY && !CHECK && F.n_ch == RO_NCH_FAST && A.L.bx == 32 &&
-        A.L.by == 32)
-        return launch_b<MODE, CHECK, 32, 32, RO_NCH_FAST>(F, A, s);
-#endif
     if (A.L.bx == 32 && A.L.by == 32) return launch_b<MODE, CHECK, 32, 32>(F, A, s);
     if (A.L.bx == 16 && A.L.by == 16) return launch_b<MODE, CHECK, 16, 16>(F, A, s);
     return launch_b<MODE, CHECK, 0, 0>(F, A, s);
