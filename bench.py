@@ -276,20 +276,44 @@ def run_ours(args):
     w, h = cfg.image_dims
     from paper_2309_04393_b200.render import MODE_REFERENCE
     mode = MODE_REFERENCE if args.mode == "reference" else MODE_RESIDENCY
-    fp = FramePass(mode, eng.paging, eng.octree, scn.channels, scn.camera, cfg,
-                   partition=(world, rank, 8), bricks_first=(world == 1))
     stream = torch.cuda.current_stream()
     m = eng.paging.config.m
+    # N > 1: sort-first exchange fused into the ray cast over peer memory
+    # (distributed.PeerFrame) when every rank can reach GPU 0's memory, else
+    # the NCCL exchange (distributed.exchange); the choice is agreed by all
+    exchange_kind = "single"
+    peer = None
+    if world > 1:
+        ok = args.exchange == "peer" and (
+            local == 0 or torch.cuda.can_device_access_peer(local, 0)
+            or torch.cuda.device_count() == 1)
+        flag = torch.tensor([1 if ok else 0], device=dev)
+        torch.distributed.all_reduce(flag, op=torch.distributed.ReduceOp.MIN)
+        exchange_kind = "peer" if int(flag[0]) else "nccl"
+        if exchange_kind == "peer":
+            from paper_2309_04393_b200.distributed import PeerFrame
+            peer = PeerFrame(eng.paging, eng.octree, len(scn.channels), cfg.image_dims)
+    fp = FramePass(mode, eng.paging, eng.octree, scn.channels, scn.camera, cfg,
+                   partition=(world, rank, 8),
+                   bricks_first=(world == 1 or exchange_kind == "peer"))
 
-    def step():
+    def step(events=None):
+        if peer is not None:
+            return peer.frame(fp, cfg.max_requests_per_frame, m, events)
+        if events:
+            events[0].record(stream)
         fp.render()
+        if events:
+            events[1].record(stream)
         fp.collect()
         if world > 1:
             from paper_2309_04393_b200.distributed import exchange
             b = fp.buf
-            exchange(dict(image=b.image, required=b.required, pix_required=b.pix_required,
-                          hist=b.hist, counters=b.counters, fb=b.fb, counts=b.counts),
-                     cfg.image_dims, 8, cfg.max_requests_per_frame, m)
+            return exchange(dict(image=b.image, required=b.required,
+                                 pix_required=b.pix_required, hist=b.hist,
+                                 counters=b.counters, fb=b.fb, counts=b.counts),
+                            cfg.image_dims, 8, cfg.max_requests_per_frame, m)
+        return None
 
     for _ in range(args.warmup):
         step()
@@ -310,16 +334,7 @@ def run_ours(args):
     torch.cuda.profiler.start()
     t_start.record(stream)
     for i in range(args.steps):
-        ev[i][0].record(stream)
-        fp.render()
-        ev[i][1].record(stream)
-        fp.collect()
-        if world > 1:
-            from paper_2309_04393_b200.distributed import exchange
-            b = fp.buf
-            exchange(dict(image=b.image, required=b.required, pix_required=b.pix_required,
-                          hist=b.hist, counters=b.counters, fb=b.fb, counts=b.counts),
-                     cfg.image_dims, 8, cfg.max_requests_per_frame, m)
+        step(ev[i])
         ev[i][2].record(stream)
     t_end.record(stream)
     torch.cuda.synchronize()
@@ -336,11 +351,15 @@ def run_ours(args):
     fps = 1000.0 / ms_per_step
 
     # work counters of the full frame (sum over parts)
-    counters = fp.buf.counters.clone()
-    hist = fp.buf.hist.clone()
-    if world > 1:
-        torch.distributed.all_reduce(counters)
-        torch.distributed.all_reduce(hist)
+    if peer is not None:   # the shared accumulators already hold the full frame
+        counters = peer.bufs["counters"].clone()
+        hist = peer.bufs["hist"].clone()
+    else:
+        counters = fp.buf.counters.clone()
+        hist = fp.buf.hist.clone()
+        if world > 1:
+            torch.distributed.all_reduce(counters)
+            torch.distributed.all_reduce(hist)
     counters = counters.cpu().numpy()
     hist = hist.cpu().numpy()
     samples = int(counters[1] + counters[2])
@@ -361,15 +380,20 @@ def run_ours(args):
         pin_img = torch.empty((h, w, 4), dtype=torch.float32, pin_memory=True)
 
         def e2e_step():
-            fp.render()
-            fp.collect()
-            b = fp.buf
-            res = _exchange(dict(image=b.image, required=b.required,
-                                 pix_required=b.pix_required, hist=b.hist, counters=b.counters,
-                                 fb=b.fb, counts=b.counts),
-                            cfg.image_dims, 8, cfg.max_requests_per_frame, m)
-            if rank == 0:
-                pin_img.copy_(res["image"], non_blocking=True)
+            if peer is not None:
+                res = step()
+                if rank == 0:
+                    pin_img.copy_(peer.bufs["image"].reshape(h, w, 4), non_blocking=True)
+            else:
+                fp.render()
+                fp.collect()
+                b = fp.buf
+                res = _exchange(dict(image=b.image, required=b.required,
+                                     pix_required=b.pix_required, hist=b.hist,
+                                     counters=b.counters, fb=b.fb, counts=b.counts),
+                                cfg.image_dims, 8, cfg.max_requests_per_frame, m)
+                if rank == 0:
+                    pin_img.copy_(res["image"], non_blocking=True)
             torch.cuda.synchronize()
             return res
         for _ in range(2):
@@ -385,11 +409,13 @@ def run_ours(args):
                      "h2d_bytes_per_step": ctypes.sizeof(N.Frame) * world,
                      "d2h_bytes_per_step": int(pin_img.numel() * 4 + 8 * 4 * fp.buf.fb.shape[1]
                                                * world),
-                     "note": ("sort-first frame through FramePass + distributed.exchange: "
-                              "rows rendered per GPU, NCCL exchange (usage MAX, hist/counters "
-                              "SUM, request lists all-gathered + merged), image gathered to "
-                              "rank 0 and copied to pinned host memory; wall time, max over "
-                              "ranks")}
+                     "note": (f"sort-first frame ({exchange_kind} exchange): rows rendered "
+                              "per GPU; peer = every GPU's ray caster writes pixels, usage, "
+                              "histogram and request atomics into rank 0's buffers over "
+                              "peer memory, rank 0 orders the requests and broadcasts them; "
+                              "nccl = usage MAX / hist SUM all-reduce, request all-gather + "
+                              "merge, image gather; full image copied to pinned host memory "
+                              "on rank 0; wall time, max over ranks")}
 
     # ---- kernel launches in one step (profiler, untimed).  Every rank runs
     # the step: it contains the exchange collectives. ----
@@ -456,7 +482,8 @@ def run_ours(args):
                        "resident_bricks": int(len(scn.brick_ids)),
                        "cache_bytes": int(len(scn.brick_ids)) * 32768,
                        "l2_policy": "inputs larger than L2 (brick cache > 126 MB)",
-                       "parallelism": f"sort-first x{world}" if world > 1 else "1 GPU"},
+                       "parallelism": (f"sort-first x{world} ({exchange_kind} exchange)"
+                                       if world > 1 else "1 GPU")},
             "gsamples_per_s": samples * fps / 1e9,
             # 8 trilinear taps per fetch (SURVEY 8(d) "sampled voxels/s"), whole job
             "sampled_gvoxels_per_s": 8.0 * F / (ms_per_step / 1e3) / 1e9,
@@ -475,6 +502,8 @@ def run_ours(args):
         }
         print(json.dumps(result), flush=True)
     if world > 1:
+        if peer is not None:
+            peer.close()
         torch.distributed.barrier()
         torch.distributed.destroy_process_group()
     return result
@@ -493,6 +522,8 @@ def main():
                     help="--impl reference: CPU seconds to spread over the timed steps")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--exchange", choices=("peer", "nccl"), default="peer",
+                    help="N > 1: fused peer-memory exchange (default) or NCCL collectives")
     ap.add_argument("--mode", default="residency", choices=["residency", "reference"],
                     help="render mode of the timed pass (reference = MODE_REFERENCE, "
                          "a diagnostic: no traversal / skipping)")

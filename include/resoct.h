@@ -154,6 +154,13 @@ typedef struct ro_frame {
        (render.py:271-315 ClassicMetadata.min_arr / max_arr), device */
     const uint8_t *cls_min;
     const uint8_t *cls_max;
+    /* sort-first over peer memory: 1 = the outputs are the FULL frame's,
+       shared by every part (typically rank 0's buffers opened through
+       ro_ipc_open): image / pix_required are written at the pixel's global
+       row, and ro_render does not clear required / hist / counters (the
+       owner clears them once per frame before any part renders). */
+    int32_t shared_outputs;
+    int32_t _pad1;
     ro_channel ch[RO_MAX_CH];
 } ro_frame;
 
@@ -333,6 +340,25 @@ int ro_download_state(ro_ctx *ctx, const ro_state *state, int8_t *pt_status,
                       int32_t *pt_slot, uint32_t *words, uint8_t *cache,
                       int64_t *slot_brick, int64_t *slot_last_used, int32_t *free_list,
                       int64_t *free_count_out, void *stream);
+
+/* ---- sort-first over peer memory ----
+   The parts of a frame write straight into one set of buffers: each GPU's
+   ray caster stores its pixels into the owner's full-frame image, its usage
+   marks / histogram / counters into the owner's, and its first-seen request
+   keys into the owner's key arrays with the same RED.MIN atomics a single GPU
+   uses -- so the owner's ro_feedback_collect yields exactly the single-GPU
+   request lists.  Buffers are shared through CUDA IPC (NVLink / NVSwitch
+   peer access), set up by the host (torch's CUDA IPC in distributed.py). */
+
+/* Use caller-owned first-seen key arrays instead of the context's own:
+   brick_keys u64[E], meta_keys u64[N*m] (device, every element 0xFF..FF
+   between frames; ro_feedback_collect restores that).  The frame's owner
+   passes arrays it allocated; every other part passes the owner's arrays
+   mapped into its address space (peer memory), so all parts' RED.MIN
+   request atomics land in one place.  NULL, NULL returns to the context's
+   own arrays.  The context never frees external arrays. */
+int ro_set_feedback_buffers(ro_ctx *ctx, unsigned long long *brick_keys,
+                            unsigned long long *meta_keys);
 
 int ro_sync(ro_ctx *ctx, void *stream);
 

@@ -80,7 +80,7 @@ class Frame(C.Structure):
                 ("dt_tab", _i32 * RO_MAX_LEVELS),
                 ("n_parts", _i32), ("part", _i32), ("tile_rows", _i32),
                 ("cls_depth", _i32), ("ref_pt", _p), ("ref_cache", _p),
-                ("cls_min", _p), ("cls_max", _p),
+                ("cls_min", _p), ("cls_max", _p), ("shared_outputs", _i32), ("_pad1", _i32),
                 ("ch", Channel * RO_MAX_CH)]
 
 
@@ -114,6 +114,7 @@ _SIGS = {
     "ro_octree_update": ([_p, C.POINTER(State), _p, _i64, _p], _i32),
     "ro_rebuild_masks": ([_p, C.POINTER(State), _p], _i32),
     "ro_sync": ([_p, _p], _i32),
+    "ro_set_feedback_buffers": ([_p, _p, _p], _i32),
     "ro_upload_state": ([_p, C.POINTER(HostState), C.POINTER(State), _p], _i32),
     "ro_download_state": ([_p, C.POINTER(State), _p, _p, _p, _p, _p, _p, _p, _p, _p], _i32),
     "ro_apply_bricks_lz4": ([_p, C.POINTER(State), _p, _i64, _p, _p, _i32, _i64, _i32, _p,

@@ -443,6 +443,15 @@ int ro_download_state(ro_ctx *c, const ro_state *st, int8_t *pt_status, int32_t 
     return RO_OK;
 }
 
+int ro_set_feedback_buffers(ro_ctx *c, unsigned long long *bk, unsigned long long *mk) {
+    if (!c) return fail(RO_EINVAL, "null context");
+    if ((bk == nullptr) != (mk == nullptr))
+        return fail(RO_EINVAL, "set both key arrays or neither");
+    c->brick_key_ext = bk;
+    c->meta_key_ext = mk;
+    return RO_OK;
+}
+
 int ro_sync(ro_ctx *c, void *stream) {
     if (!c) return fail(RO_EINVAL, "null context");
     RO_CUDA(cudaStreamSynchronize((cudaStream_t)stream));

@@ -142,7 +142,7 @@ int sort_and_emit(ro_ctx *c, unsigned long long *k_in, int32_t *v_in, int32_t n,
 int feedback_collect(ro_ctx *c, int64_t budget, int32_t bricks_first,
                      const ro_feedback *fb, cudaStream_t s) {
     if (budget < 0) return fail(RO_EINVAL, "negative budget");
-    const int64_t n_meta = c->meta_key ? c->n_meta : 0;
+    const int64_t n_meta = meta_keys(c) ? c->n_meta : 0;
     void *p0, *p2;
     int rc;
     // compacted arrays: bricks at [0, E), metas at [E, E + n_meta)
@@ -151,9 +151,9 @@ int feedback_collect(ro_ctx *c, int64_t budget, int32_t bricks_first,
     auto *ck = (unsigned long long *)p0;
     auto *cv = (int32_t *)p2;
     RO_CUDA(cudaMemsetAsync(c->touched_n, 0, 2 * sizeof(int32_t), s));
-    k_compact<<<scan_blocks(c->E), 256, 0, s>>>(c->brick_key, c->E, ck, cv, c->touched_n);
+    k_compact<<<scan_blocks(c->E), 256, 0, s>>>(brick_keys(c), c->E, ck, cv, c->touched_n);
     if (n_meta)
-        k_compact<<<scan_blocks(n_meta), 256, 0, s>>>(c->meta_key, n_meta, ck + c->E,
+        k_compact<<<scan_blocks(n_meta), 256, 0, s>>>(meta_keys(c), n_meta, ck + c->E,
                                                       cv + c->E, c->touched_n + 1);
     RO_CUDA(cudaGetLastError());
     int32_t *hn = reinterpret_cast<int32_t *>(c->pinned_small);

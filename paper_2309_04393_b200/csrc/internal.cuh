@@ -187,10 +187,21 @@ struct ro_ctx {
     cudaEvent_t upload_done = nullptr;
     cudaEvent_t host_done = nullptr;
     uint32_t *claim = nullptr;  // [E] batch dedupe stamps
+    // caller-owned key arrays (ro_set_feedback_buffers; possibly another
+    // process's over peer memory) replacing brick_key / meta_key when set
+    unsigned long long *brick_key_ext = nullptr;
+    unsigned long long *meta_key_ext = nullptr;
     uint32_t epoch = 0;
 };
 
 namespace ro {
+// first-seen key arrays in use (external ones when set)
+inline unsigned long long *brick_keys(ro_ctx *c) {
+    return c->brick_key_ext ? c->brick_key_ext : c->brick_key;
+}
+inline unsigned long long *meta_keys(ro_ctx *c) {
+    return c->meta_key_ext ? c->meta_key_ext : c->meta_key;
+}
 // grow-only scratch buffer i of at least `bytes`
 int scratch(ro_ctx *c, int i, size_t bytes, void **out);
 int ensure_meta_keys(ro_ctx *c);

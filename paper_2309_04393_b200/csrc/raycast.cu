@@ -946,8 +946,9 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
     if (active) {
         const float4 px4 = make_float4(__double2float_rn(accR), __double2float_rn(accG),
                                        __double2float_rn(accB), __double2float_rn(accA));
-        reinterpret_cast<float4 *>(A.image)[lpix] = px4;
-        A.pix_required[lpix] = pixreq;
+        const int64_t opix = F.shared_outputs ? pix : lpix;  // full-frame or local rows
+        reinterpret_cast<float4 *>(A.image)[opix] = px4;
+        A.pix_required[opix] = pixreq;
     }
     }  // packets of the tile
     }  // tile loop
@@ -1048,8 +1049,10 @@ int render(ro_ctx *c, const ro_frame *F, const ro_state *st,
     }
     if (c->bvox >= (int64_t(1) << 24)) return fail(RO_EINVAL, "brick too large");
     if (F->mode == RO_MODE_RESIDENCY) {
-        int rc = ensure_meta_keys(c);
-        if (rc) return rc;
+        if (!c->meta_key_ext) {
+            int rc = ensure_meta_keys(c);
+            if (rc) return rc;
+        }
         if (c->layout.m == 4 && (reinterpret_cast<uintptr_t>(st->words) & 15))
             return fail(RO_EINVAL, "octree words must be 16-byte aligned");
     }
@@ -1076,8 +1079,8 @@ int render(ro_ctx *c, const ro_frame *F, const ro_state *st,
     A.pix_required = static_cast<int32_t *>(dev_out[1]);
     A.hist = reinterpret_cast<unsigned long long *>(out->hist);
     A.counters = reinterpret_cast<unsigned long long *>(out->counters);
-    A.brick_key = c->brick_key;
-    A.meta_key = c->meta_key;
+    A.brick_key = brick_keys(c);
+    A.meta_key = meta_keys(c);
     A.brick_touched = c->brick_touched;
     A.meta_touched = c->meta_touched;
     A.touched_n = c->touched_n;
@@ -1088,9 +1091,11 @@ int render(ro_ctx *c, const ro_frame *F, const ro_state *st,
     A.nsb = sub_ok ? (c->layout.brick[0] >> RO_SUB_LOG) * (c->layout.brick[1] >> RO_SUB_LOG) *
                          (c->layout.brick[2] >> RO_SUB_LOG) : 0;
     A.local_rows = (int32_t)ro_local_rows(F->height, F->n_parts, F->part, F->tile_rows);
-    RO_CUDA(cudaMemsetAsync(out->required, 0, (size_t)c->E, s));
-    RO_CUDA(cudaMemsetAsync(out->hist, 0, sizeof(int64_t) * F->n_ch * c->layout.k, s));
-    RO_CUDA(cudaMemsetAsync(out->counters, 0, sizeof(int64_t) * RO_NUM_COUNTERS, s));
+    if (!F->shared_outputs) {  // shared outputs are cleared once by their owner
+        RO_CUDA(cudaMemsetAsync(out->required, 0, (size_t)c->E, s));
+        RO_CUDA(cudaMemsetAsync(out->hist, 0, sizeof(int64_t) * F->n_ch * c->layout.k, s));
+        RO_CUDA(cudaMemsetAsync(out->counters, 0, sizeof(int64_t) * RO_NUM_COUNTERS, s));
+    }
     if (A.local_rows == 0) return RO_OK;
     RO_CUDA(cudaMemsetAsync(A.tile_counter, 0, sizeof(int32_t), s));
     cudaError_t e;

@@ -185,3 +185,98 @@ def gather_image(local_rows_image, image_dims, tile_rows: int):
         idx = torch.as_tensor(rows, device=dev, dtype=torch.long)
         full.index_copy_(0, idx, parts[p][:len(rows) * w].reshape(len(rows), w, 4))
     return full.cpu().numpy()
+
+
+# ---------------------------------------------------------------------------
+# sort-first over peer memory (fused render + exchange)
+# ---------------------------------------------------------------------------
+
+class PeerFrame:
+    """Sort-first frames whose exchange is done by the ray caster itself.
+
+    Rank 0 (the owner) allocates the full-frame outputs -- image, per-pixel
+    brick counts, usage mask, histogram, counters -- and the first-seen
+    request-key arrays, and shares them with every rank through CUDA IPC
+    (torch's reductions; on an NVLink/NVSwitch box the mappings are peer
+    memory).  Each rank's ``ro_render`` (``shared_outputs = 1``) then writes
+    its pixels at their global rows, ORs its usage marks, adds its histogram
+    / counters and issues its RED.MIN request atomics straight into the
+    owner's buffers while it ray-casts: the image gather, the usage
+    all-reduce and the request all-gather + merge of ``exchange`` all
+    disappear.  One barrier later the owner's ``ro_feedback_collect`` yields
+    exactly the single-GPU request lists (same keys, same atomics), which are
+    broadcast (<= budget ids) so every replica applies the same uploads.
+    """
+
+    def __init__(self, paging, octree, n_ch: int, image_dims):
+        from torch.multiprocessing.reductions import reduce_tensor
+        from . import _native as N
+        self.N = N
+        self.world = dist.get_world_size()
+        self.rank = dist.get_rank()
+        self.paging = paging
+        w, h = image_dims
+        k, m = paging.config.k, paging.config.m
+        dev = paging.device
+        n_meta = octree.num_nodes * m
+        names = ("image", "pix_required", "required", "hist", "counters", "bkeys", "mkeys")
+        if self.rank == 0:
+            bufs = dict(
+                image=torch.zeros((h * w, 4), dtype=torch.float32, device=dev),
+                pix_required=torch.zeros(h * w, dtype=torch.int32, device=dev),
+                required=torch.zeros(paging.total_entries, dtype=torch.uint8, device=dev),
+                hist=torch.zeros((n_ch, k), dtype=torch.int64, device=dev),
+                counters=torch.zeros(N.RO_NUM_COUNTERS, dtype=torch.int64, device=dev),
+                bkeys=torch.full((paging.total_entries,), -1, dtype=torch.int64, device=dev),
+                mkeys=torch.full((n_meta,), -1, dtype=torch.int64, device=dev))
+            torch.cuda.synchronize(dev)
+            shared = [reduce_tensor(bufs[n]) for n in names]
+        else:
+            shared = None
+        box = [shared]
+        dist.broadcast_object_list(box, src=0)
+        if self.rank != 0:
+            bufs = {n: fn(*args) for n, (fn, args) in zip(names, box[0])}
+        self.bufs = bufs
+        N.check(N.lib().ro_set_feedback_buffers(paging.ctx, bufs["bkeys"].data_ptr(),
+                                                bufs["mkeys"].data_ptr()))
+        self.outputs = N.Outputs(bufs["image"].data_ptr(), bufs["required"].data_ptr(),
+                                 bufs["pix_required"].data_ptr(), bufs["hist"].data_ptr(),
+                                 bufs["counters"].data_ptr())
+        dist.barrier()
+
+    def frame(self, fp, budget: int, m: int, events=None):
+        """One sort-first frame: ``fp`` is this rank's FramePass (its
+        partition set, bricks_first=True).  Returns (bricks, metas) on every
+        rank; the full-frame image / usage / histogram / counters are
+        ``self.bufs`` (complete on every rank after the call)."""
+        N = self.N
+        stream = torch.cuda.current_stream()
+        if self.rank == 0:
+            for n in ("required", "hist", "counters"):
+                self.bufs[n].zero_()
+            stream.synchronize()
+        dist.barrier()                     # accumulators clear before any part writes
+        fp.frame.shared_outputs = 1
+        if events:
+            events[0].record(stream)
+        fp.render(self.outputs)
+        if events:
+            events[1].record(stream)
+        stream.synchronize()
+        dist.barrier()                     # every part's writes / atomics landed
+        lists = [None]
+        if self.rank == 0:
+            fp.collect()                   # owner's keys hold every part's requests
+            b = fp.buf
+            nb, nm = b.n_bricks, b.n_metas
+            fb = b.fb.cpu().numpy()
+            lists = [([int(v) for v in fb[1][:nb]],
+                      [(int(v) // m, int(v) % m) for v in fb[3][:nm]])]
+        dist.broadcast_object_list(lists, src=0)
+        return lists[0]
+
+    def close(self):
+        self.N.check(self.N.lib().ro_set_feedback_buffers(self.paging.ctx, None, None))
+        dist.barrier()
+        self.bufs = None
