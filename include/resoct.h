@@ -359,6 +359,9 @@ int ro_download_state(ro_ctx *ctx, const ro_state *state, int8_t *pt_status,
    own arrays.  The context never frees external arrays. */
 int ro_set_feedback_buffers(ro_ctx *ctx, unsigned long long *brick_keys,
                             unsigned long long *meta_keys);
+/* Let kernels of the current device access `peer_device`'s memory
+   (cudaDeviceEnablePeerAccess; already-enabled is not an error). */
+int ro_enable_peer_access(int32_t peer_device);
 
 int ro_sync(ro_ctx *ctx, void *stream);
 

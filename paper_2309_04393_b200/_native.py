@@ -115,6 +115,7 @@ _SIGS = {
     "ro_rebuild_masks": ([_p, C.POINTER(State), _p], _i32),
     "ro_sync": ([_p, _p], _i32),
     "ro_set_feedback_buffers": ([_p, _p, _p], _i32),
+    "ro_enable_peer_access": ([_i32], _i32),
     "ro_upload_state": ([_p, C.POINTER(HostState), C.POINTER(State), _p], _i32),
     "ro_download_state": ([_p, C.POINTER(State), _p, _p, _p, _p, _p, _p, _p, _p, _p], _i32),
     "ro_apply_bricks_lz4": ([_p, C.POINTER(State), _p, _i64, _p, _p, _i32, _i64, _i32, _p,

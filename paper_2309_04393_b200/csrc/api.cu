@@ -452,6 +452,22 @@ int ro_set_feedback_buffers(ro_ctx *c, unsigned long long *bk, unsigned long lon
     return RO_OK;
 }
 
+int ro_enable_peer_access(int32_t peer_device) {
+    int cur = 0;
+    RO_CUDA(cudaGetDevice(&cur));
+    if (peer_device == cur) return RO_OK;
+    int can = 0;
+    RO_CUDA(cudaDeviceCanAccessPeer(&can, cur, peer_device));
+    if (!can) return fail(RO_EINVAL, "device cannot access the peer device's memory");
+    cudaError_t e = cudaDeviceEnablePeerAccess(peer_device, 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();
+        return RO_OK;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+    return RO_OK;
+}
+
 int ro_sync(ro_ctx *c, void *stream) {
     if (!c) return fail(RO_EINVAL, "null context");
     RO_CUDA(cudaStreamSynchronize((cudaStream_t)stream));

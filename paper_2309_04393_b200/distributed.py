@@ -237,6 +237,9 @@ class PeerFrame:
         dist.broadcast_object_list(box, src=0)
         if self.rank != 0:
             bufs = {n: fn(*args) for n, (fn, args) in zip(names, box[0])}
+            owner_dev = bufs["image"].device.index
+            with torch.cuda.device(dev):   # this rank's kernels reach the owner's GPU
+                N.check(N.lib().ro_enable_peer_access(owner_dev))
         self.bufs = bufs
         N.check(N.lib().ro_set_feedback_buffers(paging.ctx, bufs["bkeys"].data_ptr(),
                                                 bufs["mkeys"].data_ptr()))
