@@ -40,6 +40,19 @@
 #ifndef RO_SUBMAX
 #define RO_SUBMAX 1
 #endif
+#ifndef RO_CH_CONST
+#define RO_CH_CONST 1
+#endif
+#if RO_CH_CONST
+// warp-uniform per-channel scalars straight from the kernel-parameter bank
+#define CH_LO(ci) (F.ch[ci].lo)
+#define CH_HI(ci) (F.ch[ci].hi)
+#define CH_SLOT(ci) (F.ch[ci].slot)
+#else
+#define CH_LO(ci) (S.lo[ci])
+#define CH_HI(ci) (S.hi[ci])
+#define CH_SLOT(ci) (S.slot[ci])
+#endif
 #ifndef RO_WARPS
 #define RO_WARPS 4
 #endif
@@ -616,7 +629,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                 skip_exit = 1e30;
 #pragma unroll 1
                 for (int ci = 0; ci < n_ch; ++ci) {
-                    const int lev = clampi(raw, S.lo[ci], S.hi[ci]);
+                    const int lev = clampi(raw, CH_LO(ci), CH_HI(ci));
                     if (sc.lp.lev != lev) level_pos(sc.lp, lev, px, py, pz, S, lbx, lby, lbz);
                     const int32_t e = S.ptoff[ci][lev] + sc.lp.local;
                     const int pv = __ldg(A.pt + e);
@@ -655,8 +668,8 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                 int deep_d = -1, dix = 0, diy = 0, diz = 0;
 #pragma unroll 1
                 for (int ci = 0; ci < n_ch; ++ci) {
-                    const int slot = S.slot[ci];
-                    const int lev = clampi(raw, S.lo[ci], S.hi[ci]);
+                    const int slot = CH_SLOT(ci);
+                    const int lev = clampi(raw, CH_LO(ci), CH_HI(ci));
                     const int d_target = CD - lev > 0 ? CD - lev : 0;
                     int last_slot = -1, last_lev = -1;
                     for (int d = 0;; ++d) {
@@ -706,7 +719,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
             } else if (MODE == RO_MODE_REFERENCE) {  // kernels.py:301-314
 #pragma unroll 1
                 for (int ci = 0; ci < n_ch; ++ci) {
-                    const int lev = clampi(raw, S.lo[ci], S.hi[ci]);
+                    const int lev = clampi(raw, CH_LO(ci), CH_HI(ci));
                     if (sc.lp.lev != lev) level_pos(sc.lp, lev, px, py, pz, S, lbx, lby, lbz);
                     const int pv = __ldg(A.pt + S.ptoff[ci][lev] + sc.lp.local);
                     if (pv >= 0) sample(ci, lev, pv);
@@ -732,7 +745,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                 // INVALID ancestor (it would issue a metadata request) stops the
                 // fast walk at that node, so requests stay in program order.
                 if (dt_ - d0 >= 1 && dt_ - d0 <= kFastDepth) {
-                    const int slot0 = S.slot[0];
+                    const int slot0 = CH_SLOT(0);
                     uint32_t pw[kFastDepth];
 #pragma unroll
                     for (int i = 0; i < kFastDepth; ++i) {
@@ -763,7 +776,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
 #endif
 #pragma unroll 1
                 for (int ci = 0; ci < n_ch; ++ci) {
-                    const int slot = S.slot[ci];
+                    const int slot = CH_SLOT(ci);
                     while (true) {
                         const int sh = D - d;
                         ix = qx >> sh;
@@ -807,7 +820,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                                 break;
                             }
                         }
-                        const int lev = clampi(raw, S.lo[ci], S.hi[ci]);
+                        const int lev = clampi(raw, CH_LO(ci), CH_HI(ci));
                         if (mask == 0) {  // K_MISSU: request the desired brick
                             if (sc.lp.lev != lev)
                                 level_pos(sc.lp, lev, px, py, pz, S, lbx, lby, lbz);
@@ -886,7 +899,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                             const int raw2 = lod_raw(t, t0, S.inv_t0, S.t0_pow2, S);
                             for (int ci = 0; ci < n_ch; ++ci) {
                                 if (!((zero_mask >> ci) & 1u)) continue;
-                                const int lev = clampi(raw2, S.lo[ci], S.hi[ci]);
+                                const int lev = clampi(raw2, CH_LO(ci), CH_HI(ci));
                                 const double rv = ref_value(F, S, ci, lev, qx, qy, qz, bx, by,
                                                             bz, lbx, lby, lbz, bvox);
                                 if (rv >= 0.0) {
@@ -916,7 +929,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                 if (CHECK && zero_mask) {  // kernels.py:644-655
                     for (int ci = 0; ci < n_ch; ++ci) {
                         if (!((zero_mask >> ci) & 1u)) continue;
-                        const int lev = clampi(raw, S.lo[ci], S.hi[ci]);
+                        const int lev = clampi(raw, CH_LO(ci), CH_HI(ci));
                         const double rv = ref_value(F, S, ci, lev, px, py, pz, bx, by, bz, lbx,
                                                     lby, lbz, bvox);
                         if (rv >= 0.0) {
