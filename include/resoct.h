@@ -39,6 +39,8 @@
  *   ro_node_minmax       service.py:102-115 region_min_max / engine.py:186-219
  *                        _box_minmax_grid (one tree level, device volume)
  *   ro_fill_metadata     engine.py:138-152 fill_metadata_from_volumes
+ *   ro_pack_frame        render.py:101-122 + camera.py:32-44 + kernels.py:43-66
+ *                        + transfer.py:38-120 host packing (for C hosts)
  *   ro_upload_state / ro_download_state
  *                        reference-layout state (paging.py:95-112,
  *                        octree.py:116-118) <-> device state
@@ -188,6 +190,35 @@ typedef struct ro_ctx ro_ctx;
 
 int ro_abi_version(void);
 const char *ro_last_error(void);
+
+/* ---- host-side frame packing (for C / C++ hosts; no CUDA calls) ---- */
+typedef struct ro_camera {          /* camera.py:15-30 */
+    double position[3], target[3], up[3];
+    double fov_deg;
+} ro_camera;
+
+typedef struct ro_render_config {   /* render.py:47-67 RenderConfig */
+    int32_t width, height;
+    double base_step, lod_reference_distance, early_term_alpha;
+    int32_t traversal_start_level, _pad0;
+} ro_render_config;
+
+typedef struct ro_channel_desc {    /* render.py:35-44 ChannelSettings */
+    int32_t slot, level_lo, level_hi, npoints;
+    double x[RO_MAX_TF_POINTS];     /* transfer-function knots (transfer.py:16-36) */
+    double rgba[RO_MAX_TF_POINTS][4];
+} ro_channel_desc;
+
+/* Fill `frame` for ro_render exactly as the Python mirror does
+   (render.py:101-122 channel packing, camera.py:32-44 basis, the LOD /
+   step / traversal-depth tables of kernels.py:43-66, the TF emptiness
+   tables of transfer.py:38-120).  k / m = levels / channel slots of the
+   layout; depth = octree depth in residency mode (0 otherwise); eps_h =
+   homogeneity epsilon.  Partition fields default to one part. */
+int ro_pack_frame(int32_t k, int32_t m, int32_t depth, int32_t mode,
+                  const ro_camera *camera, const ro_render_config *config,
+                  const ro_channel_desc *channels, int32_t n_ch, double eps_h,
+                  ro_frame *frame);
 
 int ro_create(const ro_layout *layout, ro_ctx **out);
 int ro_destroy(ro_ctx *ctx);

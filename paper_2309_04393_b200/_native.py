@@ -84,6 +84,21 @@ class Frame(C.Structure):
                 ("ch", Channel * RO_MAX_CH)]
 
 
+class CameraDesc(C.Structure):
+    _fields_ = [("position", _d * 3), ("target", _d * 3), ("up", _d * 3), ("fov_deg", _d)]
+
+
+class RenderConfigDesc(C.Structure):
+    _fields_ = [("width", _i32), ("height", _i32), ("base_step", _d),
+                ("lod_reference_distance", _d), ("early_term_alpha", _d),
+                ("traversal_start_level", _i32), ("_pad0", _i32)]
+
+
+class ChannelDesc(C.Structure):
+    _fields_ = [("slot", _i32), ("level_lo", _i32), ("level_hi", _i32), ("npoints", _i32),
+                ("x", _d * RO_MAX_TF_POINTS), ("rgba", (_d * 4) * RO_MAX_TF_POINTS)]
+
+
 class Outputs(C.Structure):
     _fields_ = [("image", _p), ("required", _p), ("pix_required", _p),
                 ("hist", _p), ("counters", _p)]
@@ -116,6 +131,9 @@ _SIGS = {
     "ro_sync": ([_p, _p], _i32),
     "ro_set_feedback_buffers": ([_p, _p, _p], _i32),
     "ro_enable_peer_access": ([_i32], _i32),
+    "ro_pack_frame": ([_i32, _i32, _i32, _i32, C.POINTER(CameraDesc),
+                       C.POINTER(RenderConfigDesc), C.POINTER(ChannelDesc), _i32, _d,
+                       C.POINTER(Frame)], _i32),
     "ro_upload_state": ([_p, C.POINTER(HostState), C.POINTER(State), _p], _i32),
     "ro_download_state": ([_p, C.POINTER(State), _p, _p, _p, _p, _p, _p, _p, _p, _p], _i32),
     "ro_apply_bricks_lz4": ([_p, C.POINTER(State), _p, _i64, _p, _p, _i32, _i64, _i32, _p,

@@ -10,14 +10,15 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 LIB = os.path.join(HERE, "libresoct.so")
-SOURCES = ["raycast.cu", "feedback.cu", "residency.cu", "ingest.cu", "metadata.cu", "api.cu"]
+SOURCES = ["raycast.cu", "feedback.cu", "residency.cu", "ingest.cu", "metadata.cu", "pack.cu",
+           "api.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
     # the decision path must round exactly like the reference's unfused fp64
     "-fmad=false",
-    "-Xcompiler", "-fPIC",
+    "-Xcompiler", "-fPIC,-ffp-contract=off",
     "--expt-relaxed-constexpr",
 ]
 

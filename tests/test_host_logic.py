@@ -32,7 +32,8 @@ def test_ctypes_structs_match_c_layout():
     from paper_2309_04393_b200 import _native as N
     structs = {"ro_layout": N.Layout, "ro_state": N.State, "ro_channel": N.Channel,
                "ro_frame": N.Frame, "ro_outputs": N.Outputs, "ro_feedback": N.Feedback,
-               "ro_host_state": N.HostState}
+               "ro_host_state": N.HostState, "ro_camera": N.CameraDesc,
+               "ro_render_config": N.RenderConfigDesc, "ro_channel_desc": N.ChannelDesc}
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "resoct.h"',
              'int main(void) {']
     for cname, py in structs.items():
@@ -254,3 +255,60 @@ def test_feedback_merge_rule():
             parts.append(tuple(lists))
         bricks, metas = merge_feedback(parts, budget, 3)
         assert bricks == want_b and metas == want_m
+
+
+
+def test_c_pack_frame_matches_python_packing(native_lib):
+    """ro_pack_frame (C / C++ hosts) fills ro_frame byte for byte like the
+    Python mirror (render._pack_frame: camera basis, LOD thresholds, step /
+    depth tables, channel clamps, TF emptiness tables), no GPU needed."""
+    import ctypes as C
+    import numpy as np
+    from paper_2309_04393_b200 import _native as N
+    from paper_2309_04393_b200 import Camera, ChannelSettings, RenderConfig, TransferFunction
+    from paper_2309_04393_b200.render import _pack_frame
+
+    class _P:  # the layout facts _pack_frame reads
+        def __init__(self, k, m):
+            self.config = type("cfg", (), {"k": k, "m": m})()
+
+    rng = np.random.default_rng(3)
+    for trial in range(40):
+        k, m = int(rng.integers(1, 9)), int(rng.integers(1, 5))
+        depth = int(rng.integers(0, 8))
+        n_ch = int(rng.integers(1, min(m, 4) + 1))
+        chans = []
+        for s in rng.permutation(m)[:n_ch]:
+            n = int(rng.integers(2, 8))
+            xs = np.sort(rng.choice(np.arange(0, 256), size=n, replace=False)).astype(float)
+            pts = tuple((float(x), tuple(float(v) for v in rng.random(4)) if rng.random() < 0.6
+                         else (0.1, 0.2, 0.3, 0.0)) for x in xs)
+            lo = int(rng.integers(0, 12))
+            chans.append(ChannelSettings(slot=int(s), tf=TransferFunction(points=pts),
+                                         level_range=(lo, lo + int(rng.integers(0, 6)))))
+        cam = Camera(position=tuple(float(v) for v in rng.uniform(-3, 3, 3)),
+                     target=tuple(float(v) for v in rng.uniform(0, 1, 3)),
+                     up=(0.0, 1.0, 0.0), fov_deg=float(rng.uniform(20, 90)))
+        cfg = RenderConfig(image_dims=(int(rng.integers(1, 4000)), int(rng.integers(1, 3000))),
+                           base_step=float(rng.choice([1 / 64, 1 / 256, 1 / 1000, 0.3])),
+                           lod_reference_distance=float(rng.uniform(0.2, 3.0)),
+                           early_term_alpha=0.99, traversal_start_level=int(rng.integers(0, 4)))
+        eps = float(rng.choice([0.0, 2.5]))
+        py = _pack_frame(0, _P(k, m), chans, cam, cfg, depth, eps)
+        cd = N.CameraDesc((C.c_double * 3)(*cam.position), (C.c_double * 3)(*cam.target),
+                          (C.c_double * 3)(*cam.up), cam.fov_deg)
+        rc = N.RenderConfigDesc(cfg.image_dims[0], cfg.image_dims[1], cfg.base_step,
+                                cfg.lod_reference_distance, cfg.early_term_alpha,
+                                cfg.traversal_start_level, 0)
+        descs = (N.ChannelDesc * n_ch)()
+        for i, c in enumerate(chans):
+            descs[i].slot, descs[i].level_lo, descs[i].level_hi = c.slot, *c.level_range
+            descs[i].npoints = len(c.tf.points)
+            for j, (x, rgba) in enumerate(c.tf.points):
+                descs[i].x[j] = x
+                for q in range(4):
+                    descs[i].rgba[j][q] = rgba[q]
+        out = N.Frame()
+        N.check(native_lib.ro_pack_frame(k, m, depth, 0, C.byref(cd), C.byref(rc), descs, n_ch,
+                                         eps, C.byref(out)))
+        assert bytes(out) == bytes(py), trial
