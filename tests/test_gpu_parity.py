@@ -762,3 +762,42 @@ def test_gpu_randomized_frames_match_oracle(seed):
     assert np.array_equal(out.pixel_required, want.pixel_required)
     assert [out.stats.traversal_steps, out.stats.samples_evaluated,
             out.stats.samples_skipped] == list(want.counters[:3])
+
+
+@pytest.mark.parametrize("depth", [7, 8])
+def test_gpu_deep_octree_matches_oracle(depth):
+    """Deep trees as config 4 uses (D = 7: 2.4 M nodes, D = 8: 19.2 M): the
+    vessel 256^3 volume with a random third of its bricks evicted and
+    random INVALID metadata; incremental masks == a from-scratch rebuild,
+    and residency frames (long parallel descents, deep skips) equal the
+    oracle bit for bit."""
+    from oracle import raycast as orc
+    from paper_2309_04393_b200 import (ChannelSettings, RenderConfig, grayscale_ramp_tf,
+                                       orbit_pose, render_frame)
+    eng = _prepared_engine("vessel256", depth=depth)
+    rng = np.random.default_rng(depth)
+    ids = eng.paging.resident_brick_ids()
+    eng.evict_bricks([int(b) for b in rng.choice(ids, size=len(ids) // 3, replace=False)])
+    words = eng.octree.words.copy()
+    kill = rng.random(words.shape) < 0.1
+    words[kill] = (words[kill] & np.uint32(0xFFFF)) | np.uint32(0x00FF0000)
+    eng.octree.upload_words(words)
+    before = eng.octree.words.copy()
+    eng.octree.rebuild_masks()
+    assert np.array_equal(before, eng.octree.words)
+    chans = [ChannelSettings(slot=0, tf=grayscale_ramp_tf(40.0))]
+    ost = oracle_state_from_device(eng)
+    och = [orc.OracleChannel(slot=0, points=chans[0].tf.points, level_range=(0, 15))]
+    for angle, step in ((0.7, 1 / 256), (3.3, 1 / 1000)):
+        cfg = RenderConfig(image_dims=(48, 36), base_step=step, max_requests_per_frame=300,
+                           traversal_start_level=2)
+        pose = orbit_pose(angle)
+        out = render_frame(eng.paging, eng.octree, chans, pose, cfg)
+        want = orc.render(ost, och, cam_tuple(pose), cfg.image_dims, step, budget=300,
+                          threads=8)
+        assert np.array_equal(out.image, want.image)
+        assert out.brick_requests == want.brick_requests
+        assert out.metadata_requests == want.metadata_requests
+        assert np.array_equal(out.required_mask, want.required_mask)
+        assert [out.stats.traversal_steps, out.stats.samples_evaluated,
+                out.stats.samples_skipped] == list(want.counters[:3])
