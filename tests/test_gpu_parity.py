@@ -714,10 +714,11 @@ def test_gpu_randomized_frames_match_oracle(seed):
     from oracle import raycast as orc
     from paper_2309_04393_b200 import Camera, ChannelSettings, RenderConfig, render_frame
     rng = np.random.default_rng(1000 + seed)
-    m = int(rng.integers(1, 5))
+    m = int(rng.integers(1, 9))      # m = 4 takes the vector word load, others the scalar one
     depth = int(rng.integers(2, 5))
     eps = float(rng.choice([0.0, 3.0, 12.0]))
-    eng = _random_partial_engine(seed, eps=eps, depth=depth, m=m)
+    eng = _random_partial_engine(seed, eps=eps, depth=depth, m=m,
+                                 cache=(6, 6, 6) if m <= 4 else (8, 8, 8))
     k = eng.paging.config.k
     chans = []
     for s in rng.permutation(m):
