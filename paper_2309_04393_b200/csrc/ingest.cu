@@ -209,19 +209,21 @@ struct CopySink {
     int lane;
     __device__ void seq(int64_t lit_at, int64_t lit, int64_t off, int64_t ml, int64_t op) {
         for (int64_t i = lane; i < lit; i += 32) dst[op + i] = src[lit_at + i];
+        if (!ml) return;  // a literal-only (last) sequence: nothing reads it here
         op += lit;
-        if (ml) {
-            __syncwarp();  // literals of this / earlier sequences visible to all lanes
-            const int64_t base = op - off;
-            if (off >= ml) {
-                for (int64_t j = lane; j < ml; j += 32) dst[op + j] = dst[base + j];
-            } else {
-                for (int64_t j = lane; j < ml; j += 32) dst[op + j] = dst[base + j % off];
-            }
+        __syncwarp();  // literals of this / earlier sequences visible to all lanes
+        const int64_t base = op - off;
+        if (off >= ml) {
+            for (int64_t j = lane; j < ml; j += 32) dst[op + j] = dst[base + j];
+        } else {
+            for (int64_t j = lane; j < ml; j += 32) dst[op + j] = dst[base + j % off];
         }
         __syncwarp();
     }
-    __device__ bool content_ok(int64_t n, uint32_t want) { return xxh32(dst, n, 0) == want; }
+    __device__ bool content_ok(int64_t n, uint32_t want) {
+        __syncwarp();  // every lane's literal stores visible before hashing
+        return xxh32(dst, n, 0) == want;
+    }
 };
 
 __device__ int64_t lz4_frame_warp(const uint8_t *__restrict__ src, int64_t len, uint8_t *dst,
