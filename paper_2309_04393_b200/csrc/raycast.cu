@@ -40,6 +40,16 @@
 #ifndef RO_SUBMAX
 #define RO_SUBMAX 1
 #endif
+// RO_DEBUG_CHECKS=1: device-side bounds assertions at every indexed access of
+// the ray caster (trap on violation); the GPU suite runs against this build
+#ifndef RO_DEBUG_CHECKS
+#define RO_DEBUG_CHECKS 0
+#endif
+#if RO_DEBUG_CHECKS
+#define RO_ASSERT(c) do { if (!(c)) __trap(); } while (0)
+#else
+#define RO_ASSERT(c) do { } while (0)
+#endif
 #ifndef RO_CH_CONST
 #define RO_CH_CONST 1
 #endif
@@ -282,6 +292,7 @@ __device__ __forceinline__ int2 substitute(const int32_t *__restrict__ pt, const
         const int db = below ? lev - (31 - __clz(below)) : 64;
         const int cand = da <= db ? lev + da : lev - db;
         if (lp2.lev != cand) level_pos(lp2, cand, px, py, pz, S, lbx, lby, lbz);
+        RO_ASSERT(cand >= 0 && cand < RO_MAX_LEVELS && lp2.local >= 0);
         const int pv2 = __ldg(pt + S.ptoff[ci][cand] + lp2.local);
         if (pv2 >= 0) return make_int2(cand, pv2);
         mk &= ~(1u << cand);
@@ -564,8 +575,10 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                 if (e != pb) {
                     pb = e;
                     pixreq += 1;
+                    RO_ASSERT(e >= 0 && e < A.L.E);
                     A.required[e] = 1;
                 }
+                RO_ASSERT(lev >= 0 && lev < k && ci < n_ch);
                 hist_t[(ci * k + lev) * kBlock + tid] += 1;
             };
             // Sub-block skip: the taps with non-zero weight lie within one
@@ -576,6 +589,8 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
             auto sub_skip = [&](int ci, int slot_lin, const LevelPos &lp) -> bool {
 #if RO_SUBMAX
                 if (A.sub_max == nullptr) return false;
+                RO_ASSERT(slot_lin >= 0 && slot_lin < A.L.num_slots && lp.sub >= 0 &&
+                          lp.sub < A.nsb);
                 return (int)__ldg(A.sub_max + (int64_t)slot_lin * A.nsb + lp.sub) <=
                        S.zero_upto[ci];
 #else
@@ -584,6 +599,8 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
             };
             auto finish = [&](int ci, int slot_lin, const Taps &tp) {
                 int tv[8];
+                RO_ASSERT(slot_lin >= 0 && slot_lin < A.L.num_slots && tp.o >= 0 &&
+                          tp.o + (int64_t)bx * by + bx + 1 < 2 * (int64_t)bvox);
                 load_taps<BX, BY>(tv, A.cache + (int64_t)slot_lin * bvox + tp.o, bx, bx * by);
                 // The trilinear value never exceeds the largest tap (every lerp
                 // is a rounded convex combination).  If that tap lies in the
@@ -632,6 +649,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                     const int lev = clampi(raw, CH_LO(ci), CH_HI(ci));
                     if (sc.lp.lev != lev) level_pos(sc.lp, lev, px, py, pz, S, lbx, lby, lbz);
                     const int32_t e = S.ptoff[ci][lev] + sc.lp.local;
+                    RO_ASSERT(e >= 0 && e < A.L.E);
                     const int pv = __ldg(A.pt + e);
                     if (pv >= 0) {
                         all_empty = false;
@@ -688,7 +706,8 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                         const int lev_d = CD - d;
                         const int32_t e = S.ptoff[ci][lev_d] + local;  // grid 2^d per axis
                         A.required[e] = 1;
-                        const int pv = __ldg(A.pt + e);
+                        RO_ASSERT(e >= 0 && e < A.L.E);
+                    const int pv = __ldg(A.pt + e);
                         if (pv < 0) {
                             const unsigned long long key = key_hi | ev++;
                             int32_t &lb = last_breq[ci * kBlock + tid];
@@ -755,6 +774,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                             const int sh = D - dd;
                             const int nidx = S.lvl_off[dd] +
                                 ((((qz >> sh) << dd) + (qy >> sh)) << dd) + (qx >> sh);
+                            RO_ASSERT(nidx >= 0 && nidx < A.L.num_nodes);
                             pw[i] = __ldg(A.words + nidx * m + slot0);
                         }
                     }
@@ -787,11 +807,13 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                         uint32_t w;
                         if (vec4) {
                             if (nidx != cur_node) {
+                                RO_ASSERT(nidx >= 0 && nidx < A.L.num_nodes);
                                 wv = __ldg(reinterpret_cast<const uint4 *>(A.words) + nidx);
                                 cur_node = nidx;
                             }
                             w = slot == 0 ? wv.x : slot == 1 ? wv.y : slot == 2 ? wv.z : wv.w;
                         } else {
+                            RO_ASSERT(nidx >= 0 && nidx < A.L.num_nodes);
                             w = __ldg(A.words + nidx * m + slot);
                         }
                         const int mn = (w >> 16) & 0xFF, mx = (w >> 24) & 0xFF;
@@ -841,7 +863,8 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                         all_cz = false;
                         if (sc.lp.lev != lev) level_pos(sc.lp, lev, px, py, pz, S, lbx, lby, lbz);
                         const int32_t e = S.ptoff[ci][lev] + sc.lp.local;
-                        const int pv = __ldg(A.pt + e);
+                        RO_ASSERT(e >= 0 && e < A.L.E);
+                    const int pv = __ldg(A.pt + e);
                         if (pv >= 0) {
                             sample(ci, lev, pv);
                             break;
