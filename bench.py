@@ -292,7 +292,19 @@ def run_ours(args):
         exchange_kind = "peer" if int(flag[0]) else "nccl"
         if exchange_kind == "peer":
             from paper_2309_04393_b200.distributed import PeerFrame
-            peer = PeerFrame(eng.paging, eng.octree, len(scn.channels), cfg.image_dims)
+            try:
+                peer = PeerFrame(eng.paging, eng.octree, len(scn.channels), cfg.image_dims)
+                ok = 1
+            except Exception as exc:  # e.g. no IPC / peer access on this box
+                print(f"[rank {rank}] peer exchange unavailable: {exc!r}", file=sys.stderr)
+                peer, ok = None, 0
+            flag = torch.tensor([ok], device=dev)
+            torch.distributed.all_reduce(flag, op=torch.distributed.ReduceOp.MIN)
+            if not int(flag[0]):      # every rank falls back together
+                if peer is not None:
+                    peer.close()
+                    peer = None
+                exchange_kind = "nccl"
     fp = FramePass(mode, eng.paging, eng.octree, scn.channels, scn.camera, cfg,
                    partition=(world, rank, 8),
                    bricks_first=(world == 1 or exchange_kind == "peer"))

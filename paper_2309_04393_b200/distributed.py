@@ -246,7 +246,9 @@ class PeerFrame:
         self.outputs = N.Outputs(bufs["image"].data_ptr(), bufs["required"].data_ptr(),
                                  bufs["pix_required"].data_ptr(), bufs["hist"].data_ptr(),
                                  bufs["counters"].data_ptr())
-        dist.barrier()
+        # no trailing collective: a rank that failed after the broadcast must
+        # meet the others at the caller's next collective (bench.py agrees on
+        # peer vs NCCL exchange with one all-reduce)
 
     def frame(self, fp, budget: int, m: int, events=None):
         """One sort-first frame: ``fp`` is this rank's FramePass (its
