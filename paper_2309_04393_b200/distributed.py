@@ -254,9 +254,11 @@ class PeerFrame:
         """One sort-first frame: ``fp`` is this rank's FramePass (its
         partition set, bricks_first=True).  Returns (bricks, metas) on every
         rank; the full-frame image / usage / histogram / counters are
-        ``self.bufs`` (complete on every rank after the call)."""
+        ``self.bufs`` (complete on every rank after the call, valid until the
+        next ``frame`` call, which first waits for every rank)."""
         N = self.N
         stream = torch.cuda.current_stream()
+        dist.barrier()                     # every rank is done with the previous frame's buffers
         if self.rank == 0:
             for n in ("required", "hist", "counters"):
                 self.bufs[n].zero_()
