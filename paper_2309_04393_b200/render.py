@@ -167,10 +167,65 @@ def _channel_block(slot: int, lo: int, hi: int, tf: TransferFunction) -> N.Chann
     return ch
 
 
+@functools.lru_cache(maxsize=256)
+def _channel_descs(key) -> "C.Array":
+    """ro_channel_desc[] of a channel list, built once per list."""
+    descs = (N.ChannelDesc * len(key))()
+    for i, (slot, (lo, hi), tf) in enumerate(key):
+        d = descs[i]
+        d.slot, d.level_lo, d.level_hi = slot, lo, hi
+        d.npoints = len(tf.points)
+        for j, (x, rgba) in enumerate(tf.points):
+            d.x[j] = float(x)
+            for q in range(4):
+                d.rgba[j][q] = float(rgba[q])
+    return descs
+
+
 def _pack_frame(mode, paging: MultiChannelPaging, channels, camera: Camera,
                 config: RenderConfig, depth: int, eps_h: float,
                 reference_paging: MultiChannelPaging | None = None,
                 partition=(1, 0, 8), classic: "ClassicMetadata | None" = None) -> N.Frame:
+    """The product packing: ro_pack_frame (csrc/pack.cu) fills the frame in
+    native code (camera basis, LOD thresholds, step / depth tables, channel
+    blocks); _pack_frame_py below is its Python restatement, kept byte-equal
+    by tests/test_host_logic.py."""
+    if not channels:
+        raise RenderError("need at least one active channel")
+    if len(channels) > N.RO_MAX_CH:
+        raise RenderError(f"at most {N.RO_MAX_CH} active channels")
+    for c in channels:
+        if not 0 <= c.slot < paging.config.m:
+            raise RenderError(f"channel slot {c.slot} out of range")
+        if len(c.tf.points) > N.RO_MAX_TF_POINTS:
+            raise RenderError(f"transfer function with > {N.RO_MAX_TF_POINTS} points")
+    w, h = config.image_dims
+    cam = N.CameraDesc((C.c_double * 3)(*camera.position), (C.c_double * 3)(*camera.target),
+                       (C.c_double * 3)(*camera.up), float(camera.fov_deg))
+    rc = N.RenderConfigDesc(int(w), int(h), float(config.base_step),
+                            float(config.lod_reference_distance),
+                            float(config.early_term_alpha), int(config.traversal_start_level), 0)
+    descs = _channel_descs(tuple((c.slot, tuple(c.level_range), c.tf) for c in channels))
+    F = N.Frame()
+    N.check(N.lib().ro_pack_frame(paging.config.k, paging.config.m, depth, mode, C.byref(cam),
+                                  C.byref(rc), descs, len(channels), float(eps_h), C.byref(F)))
+    F.n_parts, F.part, F.tile_rows = partition
+    if reference_paging is not None:
+        F.check_skips = 1
+        F.ref_pt = reference_paging.pt.data_ptr()
+        F.ref_cache = reference_paging.cache_dev.data_ptr()
+    if classic is not None:
+        F.cls_depth = classic.depth
+        F.cls_min = classic.min_arr.data_ptr()
+        F.cls_max = classic.max_arr.data_ptr()
+    return F
+
+
+def _pack_frame_py(mode, paging: MultiChannelPaging, channels, camera: Camera,
+                   config: RenderConfig, depth: int, eps_h: float,
+                   reference_paging: MultiChannelPaging | None = None,
+                   partition=(1, 0, 8), classic: "ClassicMetadata | None" = None) -> N.Frame:
+    """Python restatement of ro_pack_frame (render.py:101-122 packing)."""
     if not channels:
         raise RenderError("need at least one active channel")
     if len(channels) > N.RO_MAX_CH:

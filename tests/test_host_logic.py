@@ -266,7 +266,7 @@ def test_c_pack_frame_matches_python_packing(native_lib):
     import numpy as np
     from paper_2309_04393_b200 import _native as N
     from paper_2309_04393_b200 import Camera, ChannelSettings, RenderConfig, TransferFunction
-    from paper_2309_04393_b200.render import _pack_frame
+    from paper_2309_04393_b200.render import _pack_frame, _pack_frame_py
 
     class _P:  # the layout facts _pack_frame reads
         def __init__(self, k, m):
@@ -294,7 +294,7 @@ def test_c_pack_frame_matches_python_packing(native_lib):
                            lod_reference_distance=float(rng.uniform(0.2, 3.0)),
                            early_term_alpha=0.99, traversal_start_level=int(rng.integers(0, 4)))
         eps = float(rng.choice([0.0, 2.5]))
-        py = _pack_frame(0, _P(k, m), chans, cam, cfg, depth, eps)
+        py = _pack_frame_py(0, _P(k, m), chans, cam, cfg, depth, eps)
         cd = N.CameraDesc((C.c_double * 3)(*cam.position), (C.c_double * 3)(*cam.target),
                           (C.c_double * 3)(*cam.up), cam.fov_deg)
         rc = N.RenderConfigDesc(cfg.image_dims[0], cfg.image_dims[1], cfg.base_step,
@@ -312,3 +312,4 @@ def test_c_pack_frame_matches_python_packing(native_lib):
         N.check(native_lib.ro_pack_frame(k, m, depth, 0, C.byref(cd), C.byref(rc), descs, n_ch,
                                          eps, C.byref(out)))
         assert bytes(out) == bytes(py), trial
+        assert bytes(_pack_frame(0, _P(k, m), chans, cam, cfg, depth, eps)) == bytes(py), trial
