@@ -449,9 +449,9 @@ def run_ours(args):
         # ---- e2e through the public API (host buffers) ----
         e2e = e2e_multi
         if world == 1 and not args.no_e2e:
-            for _ in range(2):
+            for _ in range(3):
                 out = render_frame(eng.paging, eng.octree, scn.channels, scn.camera, cfg)
-            n_e2e = max(3, args.steps // 2)
+            n_e2e = max(10, args.steps)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             for _ in range(n_e2e):

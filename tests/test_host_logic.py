@@ -313,3 +313,28 @@ def test_c_pack_frame_matches_python_packing(native_lib):
                                          eps, C.byref(out)))
         assert bytes(out) == bytes(py), trial
         assert bytes(_pack_frame(0, _P(k, m), chans, cam, cfg, depth, eps)) == bytes(py), trial
+
+
+def test_host_result_pool_recycles_only_dropped_buffers():
+    """render._pinned: a frame's host buffer is reused only after every
+    array view of the previous FrameOutput that used it is gone."""
+    import torch
+    from paper_2309_04393_b200 import render as R
+
+    def frame():
+        t = R._pinned((8, 4), torch.float32, pin=False)
+        return t.numpy().reshape(32)[3:], t.data_ptr()
+
+    o1, p1 = frame()
+    o2, p2 = frame()
+    assert p1 != p2                  # o1 still alive: a second buffer
+    held = torch.from_numpy(o2)      # a torch view of a numpy view keeps it alive too
+    del o1
+    o3, p3 = frame()
+    assert p3 == p1                  # recycled
+    o4, p4 = frame()
+    assert p4 not in (p1, p2)
+    del o2
+    o5, p5 = frame()
+    assert p5 not in (p1, p2, p4)    # `held` still references buffer 2
+    del held, o3, o4, o5
