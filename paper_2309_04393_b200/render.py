@@ -460,8 +460,8 @@ def _run(mode, paging, channels, camera, config, octree=None,
     hist = sm[:nh].reshape(buf.hist.shape).copy()
     counters = sm[nh:nh + N.RO_NUM_COUNTERS]
     fb = sm[nh + N.RO_NUM_COUNTERS:].reshape(4, -1)
-    bricks = [int(v) for v in fb[1][:nb]]
-    metas = [(int(v) // m, int(v) % m) for v in fb[3][:nm]]
+    bricks = fb[1][:nb].tolist()
+    metas = [divmod(v, m) for v in fb[3][:nm].tolist()]
     required = req.numpy()
     nreq = int(required.sum())
     sx, sy, sz = paging.config.brick_size

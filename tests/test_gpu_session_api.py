@@ -166,3 +166,33 @@ def test_png_roundtrip():
     back = rows[:, 1:].reshape(h, w, 4)
     assert back.shape == (16, 24, 4)
     assert np.array_equal(back, np.clip(np.rint(img * 255), 0, 255).astype(np.uint8))
+
+
+def test_held_frame_outputs_are_never_overwritten():
+    """render_frame recycles its pinned result buffers only once every array
+    of an earlier FrameOutput is dropped: outputs a caller keeps (the
+    session history does) stay intact across later frames."""
+    from paper_2309_04393_b200 import (ChannelSettings, methods, orbit_pose, render_frame,
+                                       grayscale_ramp_tf)
+    from paper_2309_04393_b200.render import RenderConfig
+    st = scenes.store("shell64")
+    eng = methods.prepare_engine(st, {0: 0}, methods.full_engine_config(st, 1, 3))
+    chans = [ChannelSettings(slot=0, tf=grayscale_ramp_tf(40.0))]
+    cfg = RenderConfig(image_dims=(64, 48), base_step=1.0 / 64.0)
+    outs, snaps = [], []
+    for a in (0.0, 1.0, 2.0, 3.0, 4.0, 5.0, 0.5):
+        o = render_frame(eng.paging, eng.octree, chans, orbit_pose(a), cfg)
+        outs.append(o)
+        snaps.append((o.image.copy(), o.required_mask.copy(), o.pixel_required.copy()))
+    for o, (img, req, pix) in zip(outs, snaps):
+        assert np.array_equal(o.image, img)
+        assert np.array_equal(o.required_mask, req)
+        assert np.array_equal(o.pixel_required, pix)
+    assert not np.array_equal(snaps[0][0], snaps[3][0])   # poses differ
+    # dropped outputs are recycled: the steady state allocates nothing new
+    from paper_2309_04393_b200 import render as R
+    del outs, o
+    before = {k: len(v) for k, v in R._HOST_POOL.items()}
+    for _ in range(5):
+        render_frame(eng.paging, eng.octree, chans, orbit_pose(0.2), cfg)
+    assert {k: len(v) for k, v in R._HOST_POOL.items()} == before
