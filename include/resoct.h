@@ -162,7 +162,11 @@ typedef struct ro_frame {
        row, and ro_render does not clear required / hist / counters (the
        owner clears them once per frame before any part renders). */
     int32_t shared_outputs;
-    int32_t _pad1;
+    /* > 0: every ray resolves at most this many samples through the cursor
+       (a skippable sample still runs its skip loop) -- the single-sample
+       probe behind traverse_sample() (render_units hand traces); residency
+       mode only, 0 = unlimited (the product setting) */
+    int32_t max_samples;
     ro_channel ch[RO_MAX_CH];
 } ro_frame;
 

@@ -15,9 +15,9 @@ from .octree import (INVALID_WORD, NodeAddress, OctreeConfig,  # noqa: F401
 from .paging import (EMPTY, MAPPED, UNMAPPED, MultiChannelPaging,  # noqa: F401
                      PagingConfig, PagingError, decode_brick_id, encode_brick_id)
 from .render import (ChannelSettings, ClassicMetadata, FrameOutput,  # noqa: F401
-                     FrameStats, RenderConfig, RenderError, render_classic_octree,
-                     render_frame, render_frame_part, render_pagetable_only,
-                     render_reference)
+                     FrameStats, RenderConfig, RenderError, SampleProbe, probe_sample,
+                     render_classic_octree, render_frame, render_frame_part,
+                     render_pagetable_only, render_reference)
 from .session import FrameRecord, Session  # noqa: F401
 from .transfer import (TransferFunction, grayscale_ramp_tf,  # noqa: F401
                        transparent_tf)

@@ -80,7 +80,7 @@ class Frame(C.Structure):
                 ("dt_tab", _i32 * RO_MAX_LEVELS),
                 ("n_parts", _i32), ("part", _i32), ("tile_rows", _i32),
                 ("cls_depth", _i32), ("ref_pt", _p), ("ref_cache", _p),
-                ("cls_min", _p), ("cls_max", _p), ("shared_outputs", _i32), ("_pad1", _i32),
+                ("cls_min", _p), ("cls_max", _p), ("shared_outputs", _i32), ("max_samples", _i32),
                 ("ch", Channel * RO_MAX_CH)]
 
 

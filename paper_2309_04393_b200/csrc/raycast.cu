@@ -535,6 +535,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
     int stall = 0;
     uint32_t ev = 0;  // request event index within this pixel
     int32_t pixreq = 0;
+    [[maybe_unused]] int n_probe = 0;  // CHECK: cursor-resolved samples (max_samples)
 
     // Warp-uniform sample loop: lanes whose ray ended idle until the whole
     // packet is done, so the warp reconverges once per sample.
@@ -911,7 +912,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                         c_eval += 1;
                     } else {
                         c_skip += 1;
-                        if (CHECK && zero_mask) {
+                        if (CHECK && F.check_skips && zero_mask) {
                             double qx = ox + t * dx, qy = oy + t * dy, qz = oz + t * dz;
                             if (qx < 0.0) qx = 0.0;
                             if (qy < 0.0) qy = 0.0;
@@ -949,7 +950,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                 }
             } else {
                 stall = 0;
-                if (CHECK && zero_mask) {  // kernels.py:644-655
+                if (CHECK && F.check_skips && zero_mask) {  // kernels.py:644-655
                     for (int ci = 0; ci < n_ch; ++ci) {
                         if (!((zero_mask >> ci) & 1u)) continue;
                         const int lev = clampi(raw, CH_LO(ci), CH_HI(ci));
@@ -977,6 +978,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                 prev_depth = end_depth;
             }
             alive = alive && t < tfar && accA < F.early_alpha;
+            if (CHECK && F.max_samples > 0 && ++n_probe >= F.max_samples) alive = false;
         }
     }
     if (active) {
@@ -1069,6 +1071,8 @@ int render(ro_ctx *c, const ro_frame *F, const ro_state *st,
         return fail(RO_EINVAL, "unknown render mode");
     if (F->check_skips && (F->ref_pt == nullptr || F->ref_cache == nullptr))
         return fail(RO_EINVAL, "check_skips needs reference paging");
+    if (F->max_samples < 0 || (F->max_samples > 0 && F->mode != RO_MODE_RESIDENCY))
+        return fail(RO_EINVAL, "max_samples: >= 0, residency mode only");
     if (F->check_skips && F->mode != RO_MODE_RESIDENCY)
         return fail(RO_EINVAL, "the skip audit runs in residency mode only");
     if (F->mode == RO_MODE_CLASSIC) {
@@ -1141,7 +1145,7 @@ int render(ro_ctx *c, const ro_frame *F, const ro_state *st,
         e = launch<RO_MODE_PAGETABLE, false>(*F, A, s);
     } else if (F->mode == RO_MODE_CLASSIC) {
         e = launch<RO_MODE_CLASSIC, false>(*F, A, s);
-    } else if (F->check_skips) {
+    } else if (F->check_skips || F->max_samples > 0) {  // audit / probe instantiation
         e = launch<RO_MODE_RESIDENCY, true>(*F, A, s);
     } else {
         e = launch<RO_MODE_RESIDENCY, false>(*F, A, s);

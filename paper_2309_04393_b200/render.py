@@ -338,7 +338,8 @@ class FramePass:
 
     def __init__(self, mode, paging: MultiChannelPaging, octree: ResidencyOctree | None,
                  channels, camera: Camera, config: RenderConfig, reference_paging=None,
-                 partition=(1, 0, 8), bricks_first: bool = True, classic=None):
+                 partition=(1, 0, 8), bricks_first: bool = True, classic=None,
+                 max_samples: int = 0):
         N.require_cuda()
         if mode == MODE_RESIDENCY:
             if octree is None:
@@ -360,6 +361,7 @@ class FramePass:
         self.classic = classic  # keeps the metadata buffers alive
         self.frame = _pack_frame(mode, paging, channels, camera, config, depth, eps_h,
                                  reference_paging, partition, classic)
+        self.frame.max_samples = int(max_samples)
         w, h = config.image_dims
         self.local_rows = N.lib().ro_local_rows(h, *partition)
         self.buf = _buffers(paging, len(channels), self.local_rows * w,
@@ -429,10 +431,11 @@ def _pinned(shape, dtype, pin: bool = True) -> torch.Tensor:
 
 
 def _run(mode, paging, channels, camera, config, octree=None,
-         reference_paging=None, classic=None, partition=(1, 0, 8)) -> FrameOutput:
+         reference_paging=None, classic=None, partition=(1, 0, 8),
+         max_samples: int = 0) -> FrameOutput:
     start = time.perf_counter()
     fp = FramePass(mode, paging, octree, channels, camera, config, reference_paging,
-                   partition=partition, classic=classic)
+                   partition=partition, classic=classic, max_samples=max_samples)
     buf = fp.buf
     # Zero-copy image: the ray caster stores each pixel's RGBA and brick
     # count straight into pinned host memory (UVA-mapped), so the 20 B/pixel
@@ -497,6 +500,53 @@ def render_frame_part(paging: MultiChannelPaging, octree: ResidencyOctree, chann
     capacity-mode Session (distributed.gather_image assembles the frame)."""
     return _run(MODE_RESIDENCY, paging, channels, camera, config, octree=octree,
                 partition=tuple(partition))
+
+
+@dataclass
+class SampleProbe:
+    """What one sample resolved through the shared residency cursor leaves
+    behind -- the observable part of the reference's TraversalResult
+    (render.py traverse_sample, checked by tests/test_render_units.py:194-269)."""
+    steps: int                 # octree node visits over all channels
+    brick_requests: list       # BrickIDs in first-seen order
+    metadata_requests: list    # (node index, slot) in first-seen order
+    sampled_levels: list       # per channel: the level sampled, None if none
+    skippable: bool            # resolved ZERO / CONST / MISSU for every channel
+    rgba: tuple                # the sample composited over nothing
+    output: FrameOutput
+
+
+def probe_sample(paging: MultiChannelPaging, octree: ResidencyOctree, channels,
+                 position, levels, depth: int, start_depth: int = 0,
+                 direction=(1.0, 0.0, 0.0)) -> SampleProbe:
+    """Resolve ONE sample at ``position`` on the GPU, the way the ray caster
+    resolves every sample (kernels.py:431-558): a 1x1 frame whose ray starts
+    inside the volume at ``position`` (t = 0), with channel i's desired level
+    pinned to ``levels[i]``, the traversal depth to ``depth`` (step
+    2^-depth) and the cursor starting at ``start_depth``; the ray stops after
+    that sample (ro_frame.max_samples = 1; a skippable sample still runs its
+    skip loop, which is how ``skippable`` is observed: skipped samples, or
+    more than one constant-composited sample, and so the skip region must
+    span more than one step for a CONST outcome to read as skippable)."""
+    if len(levels) != len(channels):
+        raise RenderError("one desired level per channel")
+    chans = [ChannelSettings(slot=c.slot, tf=c.tf, level_range=(int(lv), int(lv)))
+             for c, lv in zip(channels, levels)]
+    base = 2.0 ** -int(depth) / (1 << max(int(v) for v in levels))
+    cfg = RenderConfig(image_dims=(1, 1), base_step=base, max_requests_per_frame=4096,
+                       traversal_start_level=int(start_depth) + 1)
+    pos = tuple(float(v) for v in position)
+    cam = Camera(position=pos, target=tuple(p + float(d) for p, d in zip(pos, direction)),
+                 up=(0.0, 1.0, 0.0) if abs(direction[1]) < 0.9 else (1.0, 0.0, 0.0))
+    out = _run(MODE_RESIDENCY, paging, chans, cam, cfg, octree=octree, max_samples=1)
+    st = out.stats
+    hist = out.level_histogram
+    sampled = [int(np.flatnonzero(hist[i])[0]) if hist[i].any() else None
+               for i in range(len(chans))]
+    return SampleProbe(steps=st.traversal_steps, brick_requests=list(out.brick_requests),
+                       metadata_requests=list(out.metadata_requests), sampled_levels=sampled,
+                       skippable=st.samples_skipped > 0 or st.samples_evaluated > 1,
+                       rgba=tuple(float(v) for v in out.image[0, 0]), output=out)
 
 
 def render_reference(paging: MultiChannelPaging, channels, camera: Camera,
