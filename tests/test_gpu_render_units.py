@@ -297,3 +297,89 @@ def test_probe_matches_oracle_first_sample():
     assert full.stats.traversal_steps == r.steps
     assert full.brick_requests == r.brick_requests
     assert math.isclose(r.rgba[3], 1.0)
+
+
+# -- sampling helpers (test_kernels.py:11-38, 122-145) -------------------------
+
+def _value_scene(payload, coord=(1, 1, 1)):
+    """One level-0 brick; TF alpha 1 everywhere with red = value / 255, so a
+    single composited sample returns its interpolated value in the red
+    channel."""
+    from paper_2309_04393_b200 import ChannelSettings, TransferFunction
+    octree, paging = make_octree(m=1)
+    set_meta_all(octree, 0, 0, 255)
+    bid = paging.encode(0, 0, coord)
+    paging.insert_brick(bid, payload, 1)
+    octree.on_brick_inserted(bid)
+    tf = TransferFunction(points=((0.0, (0.0, 0.0, 0.0, 1.0)), (255.0, (1.0, 1.0, 1.0, 1.0))))
+    return octree, paging, [ChannelSettings(slot=0, tf=tf)]
+
+
+def _trilinear(brick, l):
+    """kernels.py:137-180 restated: voxel centres at +0.5, clamped to the
+    brick interior, x fastest."""
+    B = brick.shape[0]
+    f = [min(max(c - 0.5, 0.0), B - 1.0) for c in l]
+    i0 = [int(v) for v in f]
+    i1 = [min(v + 1, B - 1) for v in i0]
+    t = [f[a] - i0[a] for a in range(3)]
+
+    def lerp(a, b, w):
+        return a + (b - a) * w
+
+    def at(z, y, x):
+        return float(brick[z, y, x])
+    c00 = lerp(at(i0[2], i0[1], i0[0]), at(i0[2], i0[1], i1[0]), t[0])
+    c10 = lerp(at(i0[2], i1[1], i0[0]), at(i0[2], i1[1], i1[0]), t[0])
+    c01 = lerp(at(i1[2], i0[1], i0[0]), at(i1[2], i0[1], i1[0]), t[0])
+    c11 = lerp(at(i1[2], i1[1], i0[0]), at(i1[2], i1[1], i1[0]), t[0])
+    return lerp(lerp(c00, c10, t[1]), lerp(c01, c11, t[1]), t[2])
+
+
+def test_trilinear_constant_brick_exact():
+    """test_kernels.py:26-38: a constant brick samples to its value exactly
+    anywhere, the brick faces included."""
+    from paper_2309_04393_b200 import probe_sample
+    octree, paging, chans = _value_scene(np.full((16, 16, 16), 173, np.uint8))
+    for pos in ((0.25, 0.25, 0.25), (0.3, 0.4, 0.49), (0.499, 0.251, 0.37)):
+        r = probe_sample(paging, octree, chans, pos, [0], 3, start_depth=0)
+        assert r.sampled_levels == [0]
+        assert r.rgba[0] == float(np.float32(173.0 / 255.0)) and r.rgba[3] == 1.0
+
+
+def test_trilinear_matches_python_sampler():
+    """test_kernels.py:11-23: the sampled value equals a plain-Python
+    trilinear sampler at random positions inside the brick (read back
+    through the f32 image, hence the 1e-6 tolerance)."""
+    from paper_2309_04393_b200 import probe_sample
+    rng = np.random.default_rng(5)
+    brick = rng.integers(0, 256, size=(16, 16, 16), dtype=np.uint8)
+    octree, paging, chans = _value_scene(brick)
+    for _ in range(24):
+        pos = tuple(float(v) for v in rng.uniform(0.25, 0.4999, 3))
+        r = probe_sample(paging, octree, chans, pos, [0], 3, start_depth=0)
+        want = _trilinear(brick, [p * 64.0 - 16.0 for p in pos]) / 255.0
+        assert r.rgba[0] == pytest.approx(want, rel=1e-6, abs=1e-7), pos
+
+
+def test_brick_coordinates_and_entries_match_paging():
+    """test_kernels.py:122-145: the brick the kernel uses for a position is
+    paging.brick_coord_of (clamped to the grid) and its usage-mask entry is
+    paging's entry index, for every level."""
+    from paper_2309_04393_b200 import ChannelSettings, probe_sample
+    octree, paging = make_octree(m=1, k=3, cache=(4, 4, 4))
+    set_meta_all(octree, 0, 0, 255)
+    rng = np.random.default_rng(9)
+    tf = _tf40()
+    for lev in range(3):
+        for _ in range(6):
+            pos = tuple(float(v) for v in rng.uniform(0.0, 0.9999, 3))
+            coord = paging.brick_coord_of(lev, pos)
+            bid = paging.encode(0, lev, coord)
+            if paging.resident_slot(bid) is None:
+                paging.insert_brick(bid, np.full((16, 16, 16), 120, np.uint8), 1)
+                octree.on_brick_inserted(bid)
+            r = probe_sample(paging, octree, [ChannelSettings(0, tf)], pos, [lev], 3)
+            assert r.sampled_levels == [lev]
+            used = np.flatnonzero(r.output.required_mask)
+            assert list(used) == [paging._entry_index(0, lev, coord)]
