@@ -246,3 +246,55 @@ def test_gpu_pyramid_and_bricks_match_store():
                     for x in range(gx):
                         assert np.array_equal(bricks[i], st.brick(c, lev, (x, y, z)))
                         i += 1
+
+
+# -- known answers of the reference's ingest / lz4io tests ---------------------
+
+def test_gpu_normalize_known_answers():
+    """test_ingest.py:13-31: full [0, 255] range, order kept, constant
+    volume -> 0, and the midpoint rounds half up (1 of [0, 2] -> 128)."""
+    import torch
+    from paper_2309_04393_b200 import ingest
+    raw = np.array([[[10, 20], [30, 40]], [[50, 60], [70, 90]]], dtype=np.uint16)
+    out = ingest.normalize_to_u8(torch.from_numpy(raw).cuda()).cpu().numpy()
+    assert out.dtype == np.uint8 and out.min() == 0 and out.max() == 255
+    assert np.array_equal(np.argsort(raw.ravel()), np.argsort(out.ravel()))
+    mid = np.array([0, 1, 2], dtype=np.float32).reshape(1, 1, 3)
+    assert ingest.normalize_to_u8(torch.from_numpy(mid).cuda()).cpu().numpy().ravel() \
+        .tolist() == [0, 128, 255]
+
+
+def test_gpu_edge_bricks_replicate_the_nearest_voxel():
+    """test_ingest.py:74-84: interior bricks are plain crops, edge bricks
+    repeat the last in-volume voxel along each clipped axis."""
+    import torch
+    from paper_2309_04393_b200 import ingest
+    data = np.arange(5 * 6 * 7, dtype=np.uint8).reshape(5, 6, 7)
+    bricks = ingest.extract_bricks(torch.from_numpy(data).cuda(), (4, 4, 4)).cpu().numpy()
+    assert bricks.shape == (2 * 2 * 2, 4, 4, 4)
+    assert np.array_equal(bricks[0], data[:4, :4, :4])
+    edge = bricks[7]                                   # grid (1, 1, 1): origin (4, 4, 4)
+    assert edge[0, 0, 0] == data[4, 4, 4] and edge[1, 0, 0] == data[4, 4, 4]
+    assert edge[0, 0, 2] == data[4, 4, 6] and edge[0, 0, 3] == data[4, 4, 6]
+    want = data[np.minimum(np.arange(4, 8), 4)][:, np.minimum(np.arange(4, 8), 5)][
+        :, :, np.minimum(np.arange(4, 8), 6)]
+    assert np.array_equal(edge, want)
+
+
+def test_gpu_lz4_error_known_answers():
+    """test_lz4io.py:24-52: a zero brick compresses below 1 %; a size
+    mismatch, a truncated or corrupted frame, garbage and an empty input are
+    all rejected (per frame, the others in the batch still decode)."""
+    from paper_2309_04393_b200 import ingest
+    zero = ingest.compress(bytes(32 ** 3))
+    assert len(zero) < 32 ** 3 // 100
+    good = ingest.compress(bytes(range(256)) * 16)           # 4096 bytes = 16^3
+    corrupt = bytearray(good)
+    corrupt[4] ^= 0xFF
+    frames = [good, ingest.compress(b"abcdef"), good[:len(good) // 2], bytes(corrupt),
+              b"not lz4 data at all", b"", good]
+    out, st = ingest.decompress_bricks(frames, (16, 16, 16), raise_on_error=False)
+    assert st[0] == 0 and st[-1] == 0 and all(st[1:-1] != 0)
+    assert bytes(out[0].cpu().numpy().tobytes()) == bytes(range(256)) * 16
+    with pytest.raises(ingest.IngestError):
+        ingest.decompress_bricks(frames[1:2], (16, 16, 16))
