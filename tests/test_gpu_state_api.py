@@ -285,3 +285,75 @@ def test_metadata_box_dilation_and_prefill_overflow():
     small = _engine(cache=(2, 2, 2))
     with pytest.raises(EngineError):
         small.prefill(lambda s, lev, c: _brick(), slots=[0])
+
+
+# -- engine metadata fill / prefill (test_engine.py:118-194) -------------------
+
+def test_fill_metadata_equals_per_node_scan_and_keeps_masks():
+    """test_engine.py:118-141: every node's (min, max) after the device fill
+    equals the per-node local scan, other slots stay INVALID, and the fill
+    leaves residency bits alone."""
+    from paper_2309_04393_b200.octree import NodeAddress
+    from paper_2309_04393_b200.volume import shell_volume
+    eng = _engine(depth=2, cache=(5, 5, 5))
+    bid = eng.paging.encode(0, 0, (0, 0, 0))
+    eng.apply_brick(bid, _brick(3))
+    mask = eng.octree.residency_mask(NodeAddress(2, 0, 0, 0), 0)
+    assert mask != 0
+    vol = shell_volume(64)
+    eng.fill_metadata_from_volumes({0: vol})
+    for d in range(3):
+        s = 1 << d
+        for z in range(s):
+            for y in range(s):
+                for x in range(s):
+                    a = NodeAddress(d, x, y, z)
+                    assert eng.octree.metadata(a, 0) == eng.compute_metadata_local(a, 0, vol)
+    assert eng.octree.metadata(NodeAddress(0, 0, 0, 0), 1) is None
+    assert eng.octree.residency_mask(NodeAddress(2, 0, 0, 0), 0) == mask
+
+
+def test_prefill_all_levels_and_overflow():
+    """test_engine.py:144-160: prefill makes 4^3 + 2^3 + 1 bricks resident;
+    a cache too small for that raises."""
+    from paper_2309_04393_b200 import EngineError
+    eng = _engine(depth=2, cache=(5, 5, 5), m=1)
+    eng.prefill(lambda slot, level, coord: _brick(level), slots=[0])
+    assert eng.paging.occupied_slot_count() == 73
+    for lev, g in [(0, 4), (1, 2), (2, 1)]:
+        for z in range(g):
+            assert eng.paging.resident_slot(eng.paging.encode(0, lev, (z, 0, 0))) is not None
+    with pytest.raises(EngineError):
+        _engine(depth=2, cache=(2, 2, 2), m=1).prefill(
+            lambda slot, level, coord: _brick(level), slots=[0])
+
+
+def test_metadata_bounds_samples_of_every_level():
+    """test_engine.py:163-194: the dilated node (min, max) bounds the
+    trilinear sample of every level's brick at random points."""
+    from paper_2309_04393_b200.octree import NodeAddress
+    from paper_2309_04393_b200.volume import build_pyramid, shell_volume
+    eng = _engine(depth=2, cache=(6, 6, 6), m=1)
+    vol = shell_volume(64)
+    pyr = build_pyramid(vol, eng.manifest.levels)
+
+    def fetch(slot, level, coord):
+        x, y, z = coord
+        out = np.zeros((16, 16, 16), np.uint8)
+        part = pyr[level][z * 16:(z + 1) * 16, y * 16:(y + 1) * 16, x * 16:(x + 1) * 16]
+        out[:part.shape[0], :part.shape[1], :part.shape[2]] = part
+        return out
+
+    eng.prefill(fetch, slots=[0])
+    eng.fill_metadata_from_volumes({0: vol})
+    rng = np.random.default_rng(7)
+    for _ in range(200):
+        p = rng.uniform(0.0, 1.0, 3)
+        mn, mx = eng.octree.metadata(NodeAddress(2, *(min(int(v * 4), 3) for v in p)), 0)
+        for lev in range(3):
+            coord = eng.paging.brick_coord_of(lev, tuple(p))
+            lin = eng.paging.resident_slot(eng.paging.encode(0, lev, coord))
+            dims = eng.paging.level_dims[lev]
+            local = tuple(float(p[a] * dims[a] - coord[a] * 16) for a in range(3))
+            v = eng.paging.sample(eng.paging.slot_triple(lin), local)
+            assert mn - 1e-9 <= v <= mx + 1e-9, (p, lev, v, mn, mx)
