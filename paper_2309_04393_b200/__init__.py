@@ -19,6 +19,7 @@ from .render import (ChannelSettings, ClassicMetadata, FrameOutput,  # noqa: F40
                      render_classic_octree, render_frame, render_frame_part,
                      render_pagetable_only, render_reference)
 from .session import FrameRecord, Session  # noqa: F401
+from .viewer import ProtocolError, SessionDriver  # noqa: F401
 from .transfer import (TransferFunction, grayscale_ramp_tf,  # noqa: F401
                        transparent_tf)
 from .volume import LocalTransport, VolumeStore  # noqa: F401
