@@ -22,11 +22,15 @@ constexpr unsigned kScanBlocks = 148 * 4;
 
 // compact (key, entry) of every touched entry, reset the key; warp-aggregated
 // slot allocation
+// (also the largest pixel and event index among the touched keys, so the
+// sort only has to order the bits those need)
 __global__ void __launch_bounds__(256) k_compact(unsigned long long *__restrict__ keys,
                                                  int64_t n,
                                                  unsigned long long *__restrict__ out_keys,
                                                  int32_t *__restrict__ out_vals,
-                                                 int32_t *__restrict__ count) {
+                                                 int32_t *__restrict__ count,
+                                                 unsigned *__restrict__ maxes) {
+    unsigned mpix = 0, mev = 0;
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -43,6 +47,8 @@ __global__ void __launch_bounds__(256) k_compact(unsigned long long *__restrict_
             k0 = keys[base];
         }
         const bool t0 = k0 != ~0ull, t1 = k1 != ~0ull;
+        if (t0) { mpix = max(mpix, (unsigned)(k0 >> 32)); mev = max(mev, (unsigned)k0); }
+        if (t1) { mpix = max(mpix, (unsigned)(k1 >> 32)); mev = max(mev, (unsigned)k1); }
         const int mine = (int)t0 + (int)t1;
         int incl = mine;
 #pragma unroll
@@ -67,26 +73,48 @@ __global__ void __launch_bounds__(256) k_compact(unsigned long long *__restrict_
             keys[base + 1] = ~0ull;
         }
     }
+    mpix = __reduce_max_sync(0xffffffffu, mpix);
+    mev = __reduce_max_sync(0xffffffffu, mev);
+    if (lane == 0 && (mpix | mev)) {
+        atomicMax(&maxes[0], mpix);
+        atomicMax(&maxes[1], mev);
+    }
+}
+
+// (pixel << 32 | event) -> (pixel << ev_bits | event): order-preserving and
+// injective while pixel < 2^pix_bits and event < 2^ev_bits
+__global__ void k_pack_keys(const unsigned long long *__restrict__ in, int32_t n, int ev_bits,
+                            uint32_t *__restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const unsigned long long k = in[i];
+    out[i] = ((uint32_t)(k >> 32) << ev_bits) | (uint32_t)k;
+}
+
+__device__ __forceinline__ unsigned long long unpack_key(uint32_t k, int ev_bits) {
+    return ((unsigned long long)(k >> ev_bits) << 32) | (k & ((1u << ev_bits) - 1u));
 }
 
 __global__ void k_emit_bricks(const DevLayout L,
                               const unsigned long long *__restrict__ keys,
+                              const uint32_t *__restrict__ keys32, int ev_bits,
                               const int32_t *__restrict__ vals, int32_t n,
                               int64_t *__restrict__ out_keys,
                               int64_t *__restrict__ out_ids) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    out_keys[i] = (int64_t)keys[i];
+    out_keys[i] = (int64_t)(keys32 ? unpack_key(keys32[i], ev_bits) : keys[i]);
     out_ids[i] = entry_to_id(L, vals[i]);
 }
 
 __global__ void k_emit_metas(const unsigned long long *__restrict__ keys,
+                             const uint32_t *__restrict__ keys32, int ev_bits,
                              const int32_t *__restrict__ vals, int32_t n,
                              int64_t *__restrict__ out_keys,
                              int64_t *__restrict__ out_ids) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    out_keys[i] = (int64_t)keys[i];
+    out_keys[i] = (int64_t)(keys32 ? unpack_key(keys32[i], ev_bits) : keys[i]);
     out_ids[i] = vals[i];
 }
 
@@ -110,29 +138,53 @@ inline unsigned scan_blocks(int64_t n) {
     return (unsigned)b;
 }
 
-// sort the n compacted (key, entry) pairs and emit the first `keep`
+inline int bit_length(unsigned v) { return v ? 32 - __builtin_clz(v) : 0; }
+
+// sort the n compacted (key, entry) pairs and emit the first `keep`.  Only
+// the key bits in use are ordered: (pixel, event) packed into 32 bits when
+// they fit (4 radix passes instead of 8), else the 64-bit key up to the top
+// pixel bit.
 int sort_and_emit(ro_ctx *c, unsigned long long *k_in, int32_t *v_in, int32_t n,
-                  int32_t keep, bool bricks, int64_t *out_keys, int64_t *out_ids,
-                  cudaStream_t s) {
+                  int32_t keep, bool bricks, int pix_bits, int ev_bits,
+                  int64_t *out_keys, int64_t *out_ids, cudaStream_t s) {
     if (n <= 0 || keep <= 0) return RO_OK;
     void *p1, *p3, *tmp;
     int rc;
-    if ((rc = scratch(c, 1, sizeof(unsigned long long) * n, &p1))) return rc;
     if ((rc = scratch(c, 3, sizeof(int32_t) * n, &p3))) return rc;
-    auto *k_out = (unsigned long long *)p1;
     auto *v_out = (int32_t *)p3;
-    // keys are (pixel << 32 | event): only the bits up to the top pixel matter
     size_t tmp_bytes = 0;
-    RO_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k_in, k_out, v_in, v_out, n,
-                                            0, 64, s));
-    if ((rc = scratch(c, 4, tmp_bytes, &tmp))) return rc;
-    RO_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, k_in, k_out, v_in, v_out, n, 0,
-                                            64, s));
+    const unsigned long long *k64 = nullptr;
+    const uint32_t *k32 = nullptr;
+    if (pix_bits + ev_bits <= 32) {
+        void *p5, *p6;
+        if ((rc = scratch(c, 5, sizeof(uint32_t) * n, &p5))) return rc;
+        if ((rc = scratch(c, 6, sizeof(uint32_t) * n, &p6))) return rc;
+        auto *q_in = (uint32_t *)p5, *q_out = (uint32_t *)p6;
+        k_pack_keys<<<(n + 255) / 256, 256, 0, s>>>(k_in, n, ev_bits, q_in);
+        const int end_bit = pix_bits + ev_bits > 0 ? pix_bits + ev_bits : 1;
+        RO_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, q_in, q_out, v_in, v_out, n,
+                                                0, end_bit, s));
+        if ((rc = scratch(c, 4, tmp_bytes, &tmp))) return rc;
+        RO_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, q_in, q_out, v_in, v_out, n, 0,
+                                                end_bit, s));
+        k32 = q_out;
+    } else {
+        if ((rc = scratch(c, 1, sizeof(unsigned long long) * n, &p1))) return rc;
+        auto *k_out = (unsigned long long *)p1;
+        const int end_bit = 32 + pix_bits;
+        RO_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k_in, k_out, v_in, v_out, n,
+                                                0, end_bit, s));
+        if ((rc = scratch(c, 4, tmp_bytes, &tmp))) return rc;
+        RO_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, k_in, k_out, v_in, v_out, n, 0,
+                                                end_bit, s));
+        k64 = k_out;
+    }
     if (bricks)
-        k_emit_bricks<<<(keep + 255) / 256, 256, 0, s>>>(c->dl, k_out, v_out, keep, out_keys,
-                                                          out_ids);
+        k_emit_bricks<<<(keep + 255) / 256, 256, 0, s>>>(c->dl, k64, k32, ev_bits, v_out, keep,
+                                                          out_keys, out_ids);
     else
-        k_emit_metas<<<(keep + 255) / 256, 256, 0, s>>>(k_out, v_out, keep, out_keys, out_ids);
+        k_emit_metas<<<(keep + 255) / 256, 256, 0, s>>>(k64, k32, ev_bits, v_out, keep, out_keys,
+                                                         out_ids);
     RO_CUDA(cudaGetLastError());
     return RO_OK;
 }
@@ -150,22 +202,28 @@ int feedback_collect(ro_ctx *c, int64_t budget, int32_t bricks_first,
     if ((rc = scratch(c, 2, sizeof(int32_t) * (c->E + n_meta), &p2))) return rc;
     auto *ck = (unsigned long long *)p0;
     auto *cv = (int32_t *)p2;
-    RO_CUDA(cudaMemsetAsync(c->touched_n, 0, 2 * sizeof(int32_t), s));
-    k_compact<<<scan_blocks(c->E), 256, 0, s>>>(brick_keys(c), c->E, ck, cv, c->touched_n);
+    // touched_n: [0] bricks, [1] metas, [2] max pixel, [3] max event
+    RO_CUDA(cudaMemsetAsync(c->touched_n, 0, 4 * sizeof(int32_t), s));
+    auto *maxes = reinterpret_cast<unsigned *>(c->touched_n + 2);
+    k_compact<<<scan_blocks(c->E), 256, 0, s>>>(brick_keys(c), c->E, ck, cv, c->touched_n,
+                                                maxes);
     if (n_meta)
         k_compact<<<scan_blocks(n_meta), 256, 0, s>>>(meta_keys(c), n_meta, ck + c->E,
-                                                      cv + c->E, c->touched_n + 1);
+                                                      cv + c->E, c->touched_n + 1, maxes);
     RO_CUDA(cudaGetLastError());
     int32_t *hn = reinterpret_cast<int32_t *>(c->pinned_small);
-    RO_CUDA(cudaMemcpyAsync(hn, c->touched_n, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    RO_CUDA(cudaMemcpyAsync(hn, c->touched_n, 4 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     RO_CUDA(cudaStreamSynchronize(s));
     const int32_t nb = hn[0], nm = hn[1];
+    const int pix_bits = bit_length((unsigned)hn[2]), ev_bits = bit_length((unsigned)hn[3]);
     const int32_t kb = (int32_t)(nb < budget ? nb : budget);
     const int64_t rest = bricks_first ? budget - kb : budget;
     const int32_t km = (int32_t)(nm < rest ? nm : rest);
-    rc = sort_and_emit(c, ck, cv, nb, kb, true, fb->brick_keys, fb->brick_ids, s);
+    rc = sort_and_emit(c, ck, cv, nb, kb, true, pix_bits, ev_bits, fb->brick_keys,
+                       fb->brick_ids, s);
     if (rc) return rc;
-    rc = sort_and_emit(c, ck + c->E, cv + c->E, nm, km, false, fb->meta_keys, fb->meta_ids, s);
+    rc = sort_and_emit(c, ck + c->E, cv + c->E, nm, km, false, pix_bits, ev_bits,
+                       fb->meta_keys, fb->meta_ids, s);
     if (rc) return rc;
     fb->counts[0] = nb;
     fb->counts[1] = nm;
