@@ -313,3 +313,91 @@ def reference_state(scn: Scenario):
     return dict(m=m, k=k, brick_size=tuple(man.brick_size), level_dims=dims,
                 level_grids=grids, pt_offsets=pt_off, pt_status=pt_status,
                 pt_slot=pt_slot, cache=cache, words=words, depth=D, eps_h=0.0)
+
+
+# ---------------------------------------------------------------------------
+# config 4: out-of-core procedural volume
+# ---------------------------------------------------------------------------
+
+class ProceduralStore:
+    """Config 4 of BASELINE.json: 60 channels x 8192x8192x256 u8 (k = 9,
+    grids 256^2x8 ... 1, 599,381 bricks per channel, ~1.18 TB of bricks)
+    that never exists in full: every brick is generated on request from a
+    deterministic per-(channel, level, brick) hash, the way a brick server
+    would read it from disk (service.py:130-136 serves a stored brick).
+
+    Content: per channel a seeded occupancy grid of ``cell``-voxel columns
+    (cell x cell in x/y, the full z extent); an occupied column holds noise in
+    [16, 255] (one of ``pool`` seeded noise bricks, picked by the brick hash),
+    an empty one holds 0.  A level-l voxel takes the occupancy of the column
+    under its centre.  ``fetch_metadata`` (service.py:102-115's
+    region_min_max) answers from the occupancy grid: (0, 0) when the box
+    touches no occupied column, else a conservative (16 or 0, 255) -- exact
+    for the empty test the ray caster runs, never tighter than the data.
+
+    Transport interface of volume.LocalTransport (manifest, fetch_brick,
+    fetch_metadata), so Session streams it like any other server."""
+
+    metadata_supported = True
+
+    def __init__(self, dims=(8192, 8192, 256), channels=60, brick=32, cell=256,
+                 occupancy=0.3, pool=64, seed=4242):
+        nx, ny, nz = dims
+        b = (brick, brick, brick)
+        k = 1
+        while True:
+            lv = plan_levels(dims, b, k, (2, 2, 2))
+            if lv[-1].brick_grid_dims[0] == 1 and lv[-1].brick_grid_dims[1] == 1:
+                break
+            k += 1
+        self.manifest = VolumeManifest(name=f"procedural{nx}x{ny}x{nz}",
+                                       channel_count=channels, brick_size=b,
+                                       levels=plan_levels(dims, b, k, (2, 2, 2)))
+        self.manifest.validate()
+        self.dims = dims
+        self.brick_edge = brick
+        self.cell = cell
+        gx, gy = -(-nx // cell), -(-ny // cell)
+        self.occ = np.stack([np.random.default_rng(seed + 1 + c).random((gy, gx)) < occupancy
+                             for c in range(channels)])
+        rng = np.random.default_rng(seed)
+        self.pool = rng.integers(16, 256, size=(pool, brick, brick, brick), dtype=np.uint8)
+        self.bytes_served = 0
+
+    @property
+    def brick_count(self) -> int:
+        return self.manifest.channel_count * sum(
+            int(np.prod(l.brick_grid_dims)) for l in self.manifest.levels)
+
+    def fetch_brick(self, c, l, coord):
+        x, y, z = coord
+        B = self.brick_edge
+        i = np.arange(B)
+        # column of each level-l voxel centre, in level-0 voxels
+        cx = np.minimum((((x * B + i) << 1) + 1) << l >> 1, self.dims[0] - 1) // self.cell
+        cy = np.minimum((((y * B + i) << 1) + 1) << l >> 1, self.dims[1] - 1) // self.cell
+        mask = self.occ[c][cy[:, None], cx[None, :]]
+        h = (c * 73856093) ^ (l * 19349663) ^ (x * 83492791) ^ (y * 2654435761) ^ (z * 97)
+        out = self.pool[h % len(self.pool)] * mask[None, :, :]
+        self.bytes_served += out.nbytes
+        return out
+
+    def fetch_metadata(self, c, l, box):
+        x0, y0, _, x1, y1, _ = box
+        if x1 <= x0 or y1 <= y0:
+            return 0, 0
+        part = self.occ[c][y0 // self.cell:(y1 - 1) // self.cell + 1,
+                           x0 // self.cell:(x1 - 1) // self.cell + 1]
+        if not part.any():
+            return 0, 0
+        return (16 if part.all() else 0), 255
+
+    def close(self):
+        pass
+
+    # VolumeStore-style names (service.py:71-115 semantics) for in-process users
+    def brick(self, c, l, coord):
+        return self.fetch_brick(c, l, coord)
+
+    def region_min_max(self, c, l, box):
+        return self.fetch_metadata(c, l, box)

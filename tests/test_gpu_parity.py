@@ -802,3 +802,49 @@ def test_gpu_deep_octree_matches_oracle(depth):
         assert np.array_equal(out.required_mask, want.required_mask)
         assert [out.stats.traversal_steps, out.stats.samples_evaluated,
                 out.stats.samples_skipped] == list(want.counters[:3])
+
+
+def test_gpu_out_of_core_procedural_session_matches_oracle():
+    """Config 4 (scaled): the procedural out-of-core store streamed through a
+    Session whose cache holds a fraction of the working set (LRU evictions
+    every frame) along a moving orbit, with a mid-sequence channel swap;
+    every frame's image, ordered requests, usage mask and the full state
+    equal the oracle session fed by the same store."""
+    from oracle.session import OracleSession, state_hashes
+    from paper_2309_04393_b200 import (ChannelSettings, EngineConfig, RenderConfig, Session,
+                                       orbit_path)
+    from paper_2309_04393_b200.scenarios import COLORS, ProceduralStore
+    from paper_2309_04393_b200.transfer import colored_ramp_tf
+    from oracle import raycast as orc
+    store = ProceduralStore(dims=(512, 512, 64), channels=12, brick=16, cell=64,
+                            occupancy=0.3, pool=8, seed=99)
+    chans = [ChannelSettings(slot=s, tf=colored_ramp_tf(40.0, COLORS[s], 0.3))
+             for s in range(4)]
+    rconf = RenderConfig(image_dims=(64, 48), base_step=1 / 128, max_requests_per_frame=48)
+    econf = EngineConfig(octree_depth=4, cache_slots=(6, 6, 5), channel_slots=4)
+    sess = Session(store, econf, rconf, chans)
+    och = [orc.OracleChannel(slot=c.slot, points=c.tf.points, level_range=c.level_range)
+           for c in chans]
+    ora = OracleSession(store, 4, 4, (6, 6, 5), och,
+                        dict(image_dims=(64, 48), base_step=1 / 128, budget=48),
+                        sess.engine.metadata_pad)
+    for s, c in enumerate((0, 3, 6, 9)):
+        sess.swap_channel(s, c)
+        ora.swap_channel(s, c)
+    evicting = False
+    for i, pose in enumerate(orbit_path(14)):
+        if i == 7:
+            for s in range(4):
+                sess.swap_channel(s, 1 + 3 * s)
+                ora.swap_channel(s, 1 + 3 * s)
+        r = sess.step_frame(pose)
+        o = ora.step_frame(cam_tuple(pose))
+        assert np.array_equal(r.output.image, o.image), i
+        assert r.output.brick_requests == o.brick_requests, i
+        assert r.output.metadata_requests == o.metadata_requests, i
+        assert np.array_equal(r.output.required_mask, o.required_mask), i
+        d = diff_hashes(device_state_hashes(sess.engine), state_hashes(ora.st))
+        assert not d, (i, d)
+        evicting |= len(ora.st.free) == 0
+    assert evicting
+    sess.close()

@@ -1,0 +1,166 @@
+"""Config 4 of BASELINE.json: out-of-core 60-channel 8192x8192x256 u8 (~1.18
+TB of bricks), m = 4 visible, a 16 GiB brick cache (524,288 slots) per GPU
+streamed from pinned host memory.
+
+    python tools/bench_config4.py [--cold-frames 40 --orbit-frames 24]
+
+The volume is scenarios.ProceduralStore (bricks generated on request from a
+per-brick hash, metadata from a per-channel occupancy grid), served through
+the Session transport interface.  Each frame runs the Session.step_frame
+sequence (session.py:65-103) with every phase timed on its own:
+
+  render        render_frame (ray cast + feedback ordering, outputs to host)
+  note_sampled  usage mask -> slot_last_used (kernel 3b)
+  fetch         the transport generating the requested bricks (the "server";
+                host numpy, reported but not part of the renderer)
+  apply_bricks  ordered batch: pinned staging -> cudaMemcpyAsync on the side
+                stream -> LRU slot assignment -> octree insert/evict pass
+  metadata      request lookups + apply_metadata_batch
+
+Phase 1 starts cold at orbit_pose(0.6) and runs until the Session's
+convergence rule holds (or --cold-frames); phase 2 moves the camera along an
+orbit, streaming what each new view needs.  Prints one JSON line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--cold-frames", type=int, default=40)
+    ap.add_argument("--orbit-frames", type=int, default=24)
+    ap.add_argument("--image", type=int, nargs=2, default=[1920, 1080])
+    ap.add_argument("--budget", type=int, default=4096)
+    ap.add_argument("--cache-gib", type=float, default=16.0)
+    ap.add_argument("--depth", type=int, default=7)
+    ap.add_argument("--channels", type=int, nargs=4, default=[0, 17, 34, 51])
+    args = ap.parse_args()
+    torch.cuda.set_device(0)
+    from paper_2309_04393_b200 import orbit_path, orbit_pose
+    from paper_2309_04393_b200.engine import Engine, EngineConfig
+    from paper_2309_04393_b200.octree import node_from_index
+    from paper_2309_04393_b200.render import ChannelSettings, RenderConfig, render_frame
+    from paper_2309_04393_b200.scenarios import COLORS, ProceduralStore
+    from paper_2309_04393_b200.transfer import colored_ramp_tf
+
+    store = ProceduralStore()
+    man = store.manifest
+    slots = int(args.cache_gib * (1 << 30)) // (32 ** 3)
+    shape = (128, 64, slots // (128 * 64))
+    t0 = time.perf_counter()
+    eng = Engine(man, EngineConfig(octree_depth=args.depth, cache_slots=shape,
+                                   channel_slots=4))
+    for s, c in enumerate(args.channels):
+        eng.paging.channel_mapping[s] = c
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t0
+    channels = [ChannelSettings(slot=s, tf=colored_ramp_tf(40.0, COLORS[s], 0.3))
+                for s in range(4)]
+    cfg = RenderConfig(image_dims=tuple(args.image), base_step=1.0 / 512.0,
+                       max_requests_per_frame=args.budget, traversal_start_level=2)
+    pool = ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 4))
+
+    def timed(fn):
+        torch.cuda.synchronize()
+        a = time.perf_counter()
+        r = fn()
+        torch.cuda.synchronize()
+        return r, (time.perf_counter() - a) * 1e3
+
+    frames = []
+    streak, last = 0, None
+
+    def step(cam, phase):
+        nonlocal streak, last
+        eng.advance_frame()
+        out, t_render = timed(lambda: render_frame(eng.paging, eng.octree, channels, cam, cfg))
+        _, t_note = timed(lambda: eng.note_sampled(out.required_mask_device))
+        a = time.perf_counter()
+        ids = list(out.brick_requests)
+        def fetch(bid):
+            slot, level, coord = eng.paging.decode(bid)
+            return store.fetch_brick(eng.paging.channel_mapping[slot], level, coord)
+        pays = list(pool.map(fetch, ids))
+        payload = np.stack(pays) if ids else None
+        t_fetch = (time.perf_counter() - a) * 1e3
+        t_apply = 0.0
+        if ids:
+            _, t_apply = timed(lambda: eng.apply_bricks(ids, payload))
+        a = time.perf_counter()
+        metas = list(out.metadata_requests)
+        if metas:
+            nodes, sl, mins, maxs = [], [], [], []
+            for n, s in metas:
+                lo, hi = eng.metadata_box(node_from_index(n))
+                mn, mx = store.fetch_metadata(eng.paging.channel_mapping[s], 0,
+                                              (*lo, *hi))
+                nodes.append(n), sl.append(s), mins.append(mn), maxs.append(mx)
+            eng.apply_metadata_batch(nodes, sl, mins, maxs)
+            torch.cuda.synchronize()
+        t_meta = (time.perf_counter() - a) * 1e3
+        digest = hash(out.image.tobytes())
+        if out.stats.requests_issued == 0:
+            streak = streak + 1 if digest == last else 1
+        else:
+            streak = 0
+        last = digest
+        rec = {"phase": phase, "frame": eng.frame, "render_ms": round(t_render, 3),
+               "note_ms": round(t_note, 3), "fetch_ms": round(t_fetch, 3),
+               "apply_ms": round(t_apply, 3), "meta_ms": round(t_meta, 3),
+               "bricks": len(ids), "metas": len(metas),
+               "requests_issued": int(out.stats.requests_issued),
+               "upload_gbs": round(len(ids) * 32768 / (t_apply * 1e6), 2) if ids else None,
+               "resident": eng.paging.num_slots - int(eng.paging.free_count.item())}
+        frames.append(rec)
+        print(json.dumps(rec), file=sys.stderr, flush=True)
+
+    cam0 = orbit_pose(0.6)
+    for _ in range(args.cold_frames):
+        step(cam0, "cold")
+        if streak >= 2:
+            break
+    converged_at = frames[-1]["frame"] if streak >= 2 else None
+    for cam in orbit_path(args.orbit_frames):
+        step(cam, "orbit")
+
+    def agg(sel):
+        rs = [f for f in frames if f["phase"] == sel]
+        br = sum(f["bricks"] for f in rs)
+        ap_ms = sum(f["apply_ms"] for f in rs)
+        return {"frames": len(rs), "bricks_uploaded": br,
+                "upload_bytes": br * 32768,
+                "upload_gbs": round(br * 32768 / (ap_ms * 1e6), 2) if ap_ms else None,
+                "apply_ms_per_brick": round(ap_ms / br, 5) if br else None,
+                "render_ms_median": float(np.median([f["render_ms"] for f in rs])) if rs else None,
+                "apply_ms_total": round(ap_ms, 2),
+                "frame_ms_median_excl_fetch": float(np.median(
+                    [f["render_ms"] + f["note_ms"] + f["apply_ms"] + f["meta_ms"]
+                     for f in rs])) if rs else None}
+
+    line = {"workload": "config 4: out-of-core 60 ch x 8192x8192x256 u8 (procedural, "
+                        f"{store.brick_count} bricks, {store.brick_count * 32768 / 1e12:.2f} TB), "
+                        f"m=4 channels {args.channels}, {args.cache_gib:g} GiB cache "
+                        f"({int(np.prod(shape))} slots), octree D={args.depth}, "
+                        f"{args.image[0]}x{args.image[1]}, step 1/512, budget {args.budget}",
+            "setup_s": round(setup_s, 2), "converged_at_frame": converged_at,
+            "cold": agg("cold"), "orbit": agg("orbit"),
+            "bytes_generated": store.bytes_served,
+            "device_mem_gib": round(torch.cuda.max_memory_allocated() / 2 ** 30, 2)}
+    print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    main()
