@@ -338,3 +338,33 @@ def test_host_result_pool_recycles_only_dropped_buffers():
     o5, p5 = frame()
     assert p5 not in (p1, p2, p4)    # `held` still references buffer 2
     del held, o3, o4, o5
+
+
+def test_procedural_store_metadata_is_conservative():
+    """Config-4 procedural store: the occupancy-grid metadata answer bounds
+    the real level-0 voxels of every queried box ((0, 0) only where every
+    voxel is 0), and bricks are deterministic per (channel, level, brick)."""
+    from paper_2309_04393_b200.scenarios import ProceduralStore
+    st = ProceduralStore(dims=(256, 256, 32), channels=3, brick=16, cell=32,
+                         occupancy=0.3, pool=4, seed=5)
+    man = st.manifest
+    gx, gy, gz = man.levels[0].brick_grid_dims
+    rng = np.random.default_rng(0)
+    for c in range(3):
+        vol = np.zeros((32, 256, 256), dtype=np.uint8)
+        for z in range(gz):
+            for y in range(gy):
+                for x in range(gx):
+                    vol[z * 16:(z + 1) * 16, y * 16:(y + 1) * 16,
+                        x * 16:(x + 1) * 16] = st.fetch_brick(c, 0, (x, y, z))
+        for _ in range(200):
+            lo = rng.integers(0, [256, 256, 32])
+            hi = lo + rng.integers(1, [120, 120, 32])
+            box = (*lo.tolist(), *np.minimum(hi, [256, 256, 32]).tolist())
+            part = vol[box[2]:box[5], box[1]:box[4], box[0]:box[3]]
+            mn, mx = st.region_min_max(c, 0, box)
+            if (mn, mx) == (0, 0):
+                assert part.max() == 0
+            else:
+                assert mn <= part.min() and mx >= part.max()
+        assert np.array_equal(st.fetch_brick(c, 2, (1, 0, 0)), st.fetch_brick(c, 2, (1, 0, 0)))
