@@ -245,7 +245,10 @@ int ro_note_sampled(ro_ctx *ctx, const ro_state *state,
                     const uint8_t *required, int64_t frame, void *stream);
 
 /* Insert n bricks in order.  ids: HOST array.  payloads: n*brick bytes on the
-   host (payload_on_device=0) or device (=1).  update_octree=0 for paging-only
+   host (payload_on_device=0) or device (=1).  Host payloads in page-locked
+   memory (cudaHostAlloc / torch pin_memory) are DMA'd straight from the
+   caller's buffer on the upload stream, finished before the call returns;
+   pageable ones go through the handle's pinned staging buffer.  update_octree=0 for paging-only
    inserts.  slots_out / evicted_out: optional HOST arrays of n.  Synchronises
    the stream. */
 int ro_apply_bricks(ro_ctx *ctx, const ro_state *state, const int64_t *ids,

@@ -584,6 +584,13 @@ int apply_bricks(ro_ctx *c, const ro_state *st, const int64_t *ids_h, int64_t n6
 
     // payload upload on the side stream (overlaps the checks)
     const uint8_t *d_payload = nullptr;
+    bool caller_pinned = false;
+    // a DMA from the caller's pinned buffer completes before any return
+    struct UploadWait {
+        ro_ctx *c;
+        const bool *on;
+        ~UploadWait() { if (*on) cudaEventSynchronize(c->upload_done); }
+    } upload_wait{c, &caller_pinned};
     if (payloads) {
         if (on_device) {
             d_payload = (const uint8_t *)payloads;
@@ -591,19 +598,32 @@ int apply_bricks(ro_ctx *c, const ro_state *st, const int64_t *ids_h, int64_t n6
             void *dp;
             if ((rc = scratch(c, 2, (size_t)bvox * n, &dp))) return rc;
             size_t bytes = (size_t)bvox * n;
-            if (c->staging_bytes < bytes) {
-                if (c->staging) cudaFreeHost(c->staging);
-                c->staging = nullptr;
-                c->staging_bytes = 0;
-                RO_CUDA(cudaMallocHost(&c->staging, bytes));
-                c->staging_bytes = bytes;
+            // payloads already in pinned memory are DMA'd straight from the
+            // caller's buffer (waited for before returning); pageable ones go
+            // through the handle's pinned staging buffer
+            cudaPointerAttributes pa;
+            if (cudaPointerGetAttributes(&pa, payloads) != cudaSuccess) {
+                cudaGetLastError();
+                pa.type = cudaMemoryTypeUnregistered;
             }
-            // the previous upload must have finished before we overwrite staging
-            RO_CUDA(cudaEventSynchronize(c->upload_done));
-            if (payloads != c->staging) memcpy(c->staging, payloads, bytes);
+            caller_pinned = pa.type == cudaMemoryTypeHost;
+            const void *src = payloads;
+            if (!caller_pinned) {
+                if (c->staging_bytes < bytes) {
+                    if (c->staging) cudaFreeHost(c->staging);
+                    c->staging = nullptr;
+                    c->staging_bytes = 0;
+                    RO_CUDA(cudaMallocHost(&c->staging, bytes));
+                    c->staging_bytes = bytes;
+                }
+                // the previous upload must have finished before we overwrite staging
+                RO_CUDA(cudaEventSynchronize(c->upload_done));
+                if (payloads != c->staging) memcpy(c->staging, payloads, bytes);
+                src = c->staging;
+            }
             RO_CUDA(cudaEventRecord(c->host_done, s));
             RO_CUDA(cudaStreamWaitEvent(c->upload, c->host_done, 0));
-            RO_CUDA(cudaMemcpyAsync(dp, c->staging, bytes, cudaMemcpyHostToDevice, c->upload));
+            RO_CUDA(cudaMemcpyAsync(dp, src, bytes, cudaMemcpyHostToDevice, c->upload));
             RO_CUDA(cudaEventRecord(c->upload_done, c->upload));
             d_payload = (const uint8_t *)dp;
         }

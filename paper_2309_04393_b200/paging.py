@@ -89,6 +89,31 @@ class Translation:
         return _STATUS_NAMES[self.status]
 
 
+class PinnedBrickBuffer:
+    """Recycled page-locked host buffer that a frame's fetched bricks are
+    stacked into, so ro_apply_bricks DMAs them straight to the device on its
+    upload stream (no second host copy through the staging buffer).  The
+    returned view is valid until the next ``stack`` call; apply_bricks has
+    finished reading it when it returns."""
+
+    def __init__(self, brick_shape_zyx):
+        self.brick_shape = tuple(brick_shape_zyx)
+        self._buf = None
+
+    def stack(self, payloads):
+        n = len(payloads)
+        if any(np.shape(p) != self.brick_shape or np.asarray(p).dtype != np.uint8
+               for p in payloads):
+            return np.stack(payloads)   # insert_bricks reports the bad payload
+        need = n * math.prod(self.brick_shape)
+        if self._buf is None or self._buf.numel() < need:
+            cap = max(need, 2 * (0 if self._buf is None else self._buf.numel()))
+            self._buf = torch.empty(cap, dtype=torch.uint8, pin_memory=True)
+        view = self._buf[:need].view(n, *self.brick_shape)
+        np.stack(payloads, out=view.numpy())
+        return view
+
+
 class MultiChannelPaging:
     """m channel slots x k levels of page tables over one device brick cache.
 

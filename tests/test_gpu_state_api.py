@@ -357,3 +357,34 @@ def test_metadata_bounds_samples_of_every_level():
             local = tuple(float(p[a] * dims[a] - coord[a] * 16) for a in range(3))
             v = eng.paging.sample(eng.paging.slot_triple(lin), local)
             assert mn - 1e-9 <= v <= mx + 1e-9, (p, lev, v, mn, mx)
+
+
+def test_pinned_payloads_upload_like_pageable():
+    """ro_apply_bricks with payloads in page-locked memory (direct DMA from
+    the caller's buffer) leaves the same cache / page table / LRU / octree
+    as the pageable staging path, batch after batch with evictions, and the
+    recycled PinnedBrickBuffer can be refilled right after each call."""
+    import torch
+    from paper_2309_04393_b200.paging import PinnedBrickBuffer
+    a, b = _engine(cache=(2, 2, 2)), _engine(cache=(2, 2, 2))
+    pinned = PinnedBrickBuffer((16, 16, 16))
+    rng = np.random.default_rng(3)
+    for frame in range(1, 7):
+        a.advance_frame(), b.advance_frame()
+        ids, seen = [], set()
+        while len(ids) < 5:
+            slot, level = int(rng.integers(2)), int(rng.integers(3))
+            grid = [int(v) for v in a.paging.level_grids[level]]
+            bid = a.paging.encode(slot, level, tuple(int(rng.integers(g)) for g in grid))
+            if bid not in seen:
+                seen.add(bid)
+                ids.append(bid)
+        pays = [rng.integers(0, 256, (16, 16, 16), dtype=np.uint8) for _ in ids]
+        a.apply_bricks(ids, np.stack(pays))
+        view = pinned.stack(pays)
+        assert isinstance(view, torch.Tensor) and view.is_pinned()
+        b.apply_bricks(ids, view)
+        torch.cuda.synchronize()
+        for name in ("pt_status", "pt_slot", "slot_brick", "slot_last_used", "cache"):
+            assert np.array_equal(getattr(a.paging, name), getattr(b.paging, name)), name
+        assert np.array_equal(a.octree.words, b.octree.words)
