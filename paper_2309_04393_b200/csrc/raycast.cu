@@ -1019,6 +1019,9 @@ cudaError_t launch_b(const ro_frame &F, const RayArgs &A, cudaStream_t s) {
         cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev);
     }
     size_t dyn = (size_t)F.n_ch * kBlock * 4 * 3 + (size_t)F.n_ch * A.L.k * kBlock * 4;
+#ifdef RO_EXTRA_SMEM
+    dyn += RO_EXTRA_SMEM;  // experiment knob: shared-memory / L1 split sensitivity
+#endif
     auto kern = k_raycast<MODE, CHECK, BX, BY>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)dyn);
