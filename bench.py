@@ -482,6 +482,10 @@ def run_ours(args):
             cpu = {"value": cfps, "unit": "frames/s", "cores": threads, "kind": "port",
                    "sample": f"{len(bands)} strided 4-row bands ({rows}/{h} rows) of the "
                              f"same frame, {cdt:.1f} s, extrapolated"}
+        # compulsory bytes (the reference's FrameStats.required_bytes,
+        # render.py:224): every distinct brick the frame sampled, read once
+        req_bricks = int(fp.buf.required.to(torch.int64).sum().item())
+        compulsory = req_bricks * 32768
         result = {
             "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
@@ -507,7 +511,10 @@ def run_ours(args):
                          "traffic_source": "profiles/ncu_raycast_summary.json (ncu --set full)",
                          "peak_kind": peak_kind,
                          "algorithmic_bytes_per_launch": part_bytes,
-                         "model": "13*F + 4*S + 16*P bytes (SURVEY 8d), /ray-cast kernel time"},
+                         "model": "13*F + 4*S + 16*P bytes (SURVEY 8d), /ray-cast kernel time",
+                         "compulsory_bytes": compulsory,
+                         "compulsory_gbs": compulsory / (kern_ms / 1e3) / 1e9,
+                         "required_bricks": req_bricks},
             "e2e": e2e, "gpu_launches": launches, "clocks": clk,
             "cpu_baseline": cpu, "parity_sampled_rows": parity,
             "setup_s": setup_s,
