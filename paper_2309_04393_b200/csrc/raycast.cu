@@ -340,6 +340,25 @@ __device__ __forceinline__ double trilerp(const int v[8], const Taps &tp) {
     return lerp(lerp(c00, c10, tp.ty), lerp(c01, c11, tp.ty), tp.tz);
 }
 
+#ifndef RO_TAP_HINT
+#define RO_TAP_HINT 0
+#endif
+// experiment knob: L1 eviction priority of the trilinear tap loads
+// (0: plain ld.global.nc; 1: L1::evict_first; 2: L1::no_allocate)
+__device__ __forceinline__ uint8_t ld_tap(const uint8_t *p) {
+#if RO_TAP_HINT == 1
+    unsigned short v;
+    asm("ld.global.nc.L1::evict_first.u8 %0, [%1];" : "=h"(v) : "l"(p));
+    return (uint8_t)v;
+#elif RO_TAP_HINT == 2
+    unsigned short v;
+    asm("ld.global.nc.L1::no_allocate.u8 %0, [%1];" : "=h"(v) : "l"(p));
+    return (uint8_t)v;
+#else
+    return __ldg(p);
+#endif
+}
+
 // BX/BY = compile-time brick extent (0: runtime) so the eight tap offsets
 // become load immediates off one base address
 template <int BX, int BY>
@@ -347,14 +366,14 @@ __device__ __forceinline__ void load_taps(int v[8], const uint8_t *__restrict__ 
                                           int bxy) {
     const int sx = BX ? BX : bx;
     const int sxy = BX ? BX * BY : bxy;
-    v[0] = __ldg(p);
-    v[1] = __ldg(p + 1);
-    v[2] = __ldg(p + sx);
-    v[3] = __ldg(p + sx + 1);
-    v[4] = __ldg(p + sxy);
-    v[5] = __ldg(p + sxy + 1);
-    v[6] = __ldg(p + sxy + sx);
-    v[7] = __ldg(p + sxy + sx + 1);
+    v[0] = ld_tap(p);
+    v[1] = ld_tap(p + 1);
+    v[2] = ld_tap(p + sx);
+    v[3] = ld_tap(p + sx + 1);
+    v[4] = ld_tap(p + sxy);
+    v[5] = ld_tap(p + sxy + 1);
+    v[6] = ld_tap(p + sxy + sx);
+    v[7] = ld_tap(p + sxy + sx + 1);
 }
 
 // audit value from the fully resident reference paging (kernels.py:707-723)
