@@ -84,8 +84,13 @@ constexpr int kWarps = RO_WARPS;
 constexpr int kBlock = 32 * kWarps;  // default 4 warps on a 16x8 pixel tile
 constexpr int kTileW = RO_TILE_W;
 constexpr int kTileH = RO_TILE_H;
-constexpr int kPPT = (kTileW / 8) * (kTileH / 4);  // 8x4 packets per tile
-static_assert(kTileW % 8 == 0 && kTileH % 4 == 0 && kPPT % kWarps == 0, "tile shape");
+#ifndef RO_PACK_W
+#define RO_PACK_W 8
+#endif
+constexpr int kPackW = RO_PACK_W, kPackH = 32 / RO_PACK_W;  // warp packet (8x4)
+constexpr int kPPT = (kTileW / kPackW) * (kTileH / kPackH);  // packets per tile
+static_assert(kTileW % kPackW == 0 && kTileH % kPackH == 0 && kPPT % kWarps == 0,
+              "tile shape");
 constexpr int kFastDepth = 6;  // longest channel-0 descent handled in parallel
 constexpr double kClampHi = 1.0 - 1e-9;
 constexpr double kTwo52 = 4503599627370496.0;
@@ -509,9 +514,11 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
         last_mreq[i * kBlock + tid] = -1;
     }
 
-    // ---- pixel of this thread: warp = 8x4 packet ----
-    const int x = (tile % tiles_x) * kTileW + (wsub % (kTileW / 8)) * 8 + (lane & 7);
-    const int ly = (tile / tiles_x) * kTileH + (wsub / (kTileW / 8)) * 4 + (lane >> 3);
+    // ---- pixel of this thread: warp = kPackW x kPackH packet ----
+    const int x = (tile % tiles_x) * kTileW + (wsub % (kTileW / kPackW)) * kPackW +
+                  (lane % kPackW);
+    const int ly = (tile / tiles_x) * kTileH + (wsub / (kTileW / kPackW)) * kPackH +
+                   lane / kPackW;
     const int tr = F.tile_rows;
     const int gy = ((ly / tr) * F.n_parts + F.part) * tr + (ly % tr);
     const bool active = x < F.width && ly < A.local_rows && gy < F.height;
