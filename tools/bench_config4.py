@@ -22,6 +22,11 @@ sequence (session.py:65-103) with every phase timed on its own:
 Phase 1 starts cold at orbit_pose(0.6) and runs until the Session's
 convergence rule holds (or --cold-frames); phase 2 moves the camera along an
 orbit, streaming what each new view needs.  Prints one JSON line.
+
+``--partition N PART`` runs what one GPU of an N-GPU capacity-mode job does
+(each GPU renders, requests and caches only its own 8-row
+blocks, with no feedback exchange), so the per-GPU cost at N GPUs is
+measured on one GPU without stand-in ranks.
 """
 
 from __future__ import annotations
@@ -49,6 +54,9 @@ def main():
     ap.add_argument("--cache-gib", type=float, default=16.0)
     ap.add_argument("--depth", type=int, default=7)
     ap.add_argument("--channels", type=int, nargs=4, default=[0, 17, 34, 51])
+    ap.add_argument("--partition", type=int, nargs=2, default=None, metavar=("N", "PART"),
+                    help="capacity mode: render, request and cache only part PART of N "
+                         "sort-first row-block parts (what one GPU of N does; no exchange)")
     ap.add_argument("--pageable", action="store_true",
                     help="hand apply_bricks pageable payloads (staging-copy path)")
     args = ap.parse_args()
@@ -57,7 +65,8 @@ def main():
     from paper_2309_04393_b200.engine import Engine, EngineConfig
     from paper_2309_04393_b200.octree import node_from_index
     from paper_2309_04393_b200.paging import PinnedBrickBuffer
-    from paper_2309_04393_b200.render import ChannelSettings, RenderConfig, render_frame
+    from paper_2309_04393_b200.render import (ChannelSettings, RenderConfig, render_frame,
+                                              render_frame_part)
     from paper_2309_04393_b200.scenarios import COLORS, ProceduralStore
     from paper_2309_04393_b200.transfer import colored_ramp_tf
 
@@ -92,7 +101,13 @@ def main():
     def step(cam, phase):
         nonlocal streak, last
         eng.advance_frame()
-        out, t_render = timed(lambda: render_frame(eng.paging, eng.octree, channels, cam, cfg))
+        if args.partition:
+            part = (args.partition[0], args.partition[1], 8)
+            out, t_render = timed(lambda: render_frame_part(eng.paging, eng.octree, channels,
+                                                            cam, cfg, part))
+        else:
+            out, t_render = timed(lambda: render_frame(eng.paging, eng.octree, channels, cam,
+                                                       cfg))
         _, t_note = timed(lambda: eng.note_sampled(out.required_mask_device))
         a = time.perf_counter()
         ids = list(out.brick_requests)
@@ -127,6 +142,9 @@ def main():
                "note_ms": round(t_note, 3), "fetch_ms": round(t_fetch, 3),
                "apply_ms": round(t_apply, 3), "meta_ms": round(t_meta, 3),
                "bricks": len(ids), "metas": len(metas),
+               "samples": int(out.stats.samples_evaluated + out.stats.samples_skipped),
+               "fetches": int(out.level_histogram.sum()),
+               "steps": int(out.stats.traversal_steps),
                "requests_issued": int(out.stats.requests_issued),
                "upload_gbs": round(len(ids) * 32768 / (t_apply * 1e6), 2) if ids else None,
                "resident": eng.paging.num_slots - int(eng.paging.free_count.item())}
@@ -158,6 +176,8 @@ def main():
                 "upload_gbs": round(br * 32768 / (ap_ms * 1e6), 2) if ap_ms else None,
                 "apply_ms_per_brick": round(ap_ms / br, 5) if br else None,
                 "render_ms_median": float(np.median([f["render_ms"] for f in rs])) if rs else None,
+                "samples_median": float(np.median([f["samples"] for f in rs])) if rs else None,
+                "fetches_median": float(np.median([f["fetches"] for f in rs])) if rs else None,
                 "apply_ms_total": round(ap_ms, 2),
                 "frame_ms_median_excl_fetch": float(np.median(
                     [f["render_ms"] + f["note_ms"] + f["apply_ms"] + f["meta_ms"]
@@ -170,6 +190,8 @@ def main():
                         f"{args.image[0]}x{args.image[1]}, step 1/512, budget {args.budget}",
             "setup_s": round(setup_s, 2), "converged_at_frame": converged_at,
             "cold": agg("cold"), "orbit": agg("orbit"),
+            "partition": (f"capacity mode, part {args.partition[1]} of {args.partition[0]} "
+                          "(8-row blocks)") if args.partition else "whole frame",
             "first_frames_ms": [round(f["render_ms"] + f["apply_ms"], 1) for f in frames[:5]],
             "payloads": "pageable (staging copy)" if args.pageable else
                         "page-locked PinnedBrickBuffer (direct DMA)",
