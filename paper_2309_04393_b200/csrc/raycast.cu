@@ -279,6 +279,30 @@ __device__ __forceinline__ void level_pos(LevelPos &lp, int lev, double px, doub
     lp.sub = (((sb[2] << max(lby - RO_SUB_LOG, 0)) + sb[1]) << max(lbx - RO_SUB_LOG, 0)) + sb[0];
 }
 
+#ifndef RO_META_HINT
+#define RO_META_HINT 0
+#endif
+// experiment knob: L1::evict_last on octree-word and page-table loads
+__device__ __forceinline__ int ld_meta(const int32_t *p) {
+#if RO_META_HINT
+    int v;
+    asm("ld.global.nc.L1::evict_last.s32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+#else
+    return __ldg(p);
+#endif
+}
+__device__ __forceinline__ uint4 ld_meta4(const uint4 *p) {
+#if RO_META_HINT
+    uint4 v;
+    asm("ld.global.nc.L1::evict_last.v4.u32 {%0, %1, %2, %3}, [%4];"
+        : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    return v;
+#else
+    return __ldg(p);
+#endif
+}
+
 // kernels.py:518-549: nearest resident level in the node's mask, coarser
 // first on ties; returns (level, cache slot) or level -1.  The position of
 // the chosen level is left in `lp2` (a one-entry cache across channels).
@@ -298,7 +322,7 @@ __device__ __forceinline__ int2 substitute(const int32_t *__restrict__ pt, const
         const int cand = da <= db ? lev + da : lev - db;
         if (lp2.lev != cand) level_pos(lp2, cand, px, py, pz, S, lbx, lby, lbz);
         RO_ASSERT(cand >= 0 && cand < RO_MAX_LEVELS && lp2.local >= 0);
-        const int pv2 = __ldg(pt + S.ptoff[ci][cand] + lp2.local);
+        const int pv2 = ld_meta(pt + S.ptoff[ci][cand] + lp2.local);
         if (pv2 >= 0) return make_int2(cand, pv2);
         mk &= ~(1u << cand);
     }
@@ -677,7 +701,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                     if (sc.lp.lev != lev) level_pos(sc.lp, lev, px, py, pz, S, lbx, lby, lbz);
                     const int32_t e = S.ptoff[ci][lev] + sc.lp.local;
                     RO_ASSERT(e >= 0 && e < A.L.E);
-                    const int pv = __ldg(A.pt + e);
+                    const int pv = ld_meta(A.pt + e);
                     if (pv >= 0) {
                         all_empty = false;
                         sample(ci, lev, pv);
@@ -734,7 +758,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                         const int32_t e = S.ptoff[ci][lev_d] + local;  // grid 2^d per axis
                         A.required[e] = 1;
                         RO_ASSERT(e >= 0 && e < A.L.E);
-                    const int pv = __ldg(A.pt + e);
+                    const int pv = ld_meta(A.pt + e);
                         if (pv < 0) {
                             const unsigned long long key = key_hi | ev++;
                             int32_t &lb = last_breq[ci * kBlock + tid];
@@ -835,7 +859,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                         if (vec4) {
                             if (nidx != cur_node) {
                                 RO_ASSERT(nidx >= 0 && nidx < A.L.num_nodes);
-                                wv = __ldg(reinterpret_cast<const uint4 *>(A.words) + nidx);
+                                wv = ld_meta4(reinterpret_cast<const uint4 *>(A.words) + nidx);
                                 cur_node = nidx;
                             }
                             w = slot == 0 ? wv.x : slot == 1 ? wv.y : slot == 2 ? wv.z : wv.w;
@@ -891,7 +915,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                         if (sc.lp.lev != lev) level_pos(sc.lp, lev, px, py, pz, S, lbx, lby, lbz);
                         const int32_t e = S.ptoff[ci][lev] + sc.lp.local;
                         RO_ASSERT(e >= 0 && e < A.L.E);
-                    const int pv = __ldg(A.pt + e);
+                    const int pv = ld_meta(A.pt + e);
                         if (pv >= 0) {
                             sample(ci, lev, pv);
                             break;
