@@ -102,3 +102,35 @@ def test_gpu_abi_rejects_bad_arguments():
     out = render_frame(p, eng.octree, chans, orbit_pose(0.5), cfg)
     assert out.image.shape == (12, 16, 4)
     p.check_bijection()
+
+
+def test_gpu_abi_pinned_payload_error_leaves_context_usable():
+    """ro_apply_bricks with page-locked payloads (direct DMA from the
+    caller's buffer) and a brick id outside the layout: error code +
+    message, nothing inserted, and the same pinned buffer then uploads a
+    valid batch correctly."""
+    import torch
+    from paper_2309_04393_b200 import Engine, EngineConfig
+    from paper_2309_04393_b200 import _native as N
+    lib = N.lib()
+    st = scenes.store("mc64")
+    eng = Engine(st.manifest, EngineConfig(octree_depth=3, cache_slots=(4, 4, 4),
+                                           channel_slots=2))
+    p = eng.paging
+    state = p.state()
+    s = N.stream_ptr()
+    pay = torch.empty((2, 16, 16, 16), dtype=torch.uint8, pin_memory=True)
+    pay.copy_(torch.arange(2 * 16 ** 3, dtype=torch.int64).remainder(251).to(torch.uint8)
+              .view(2, 16, 16, 16))
+    good = p.encode(0, 0, (0, 0, 0))
+    ids = np.array([good, (1 << 32) + 5], dtype=np.int64)
+    assert _err(lib.ro_apply_bricks(p.ctx, C.byref(state), ids.ctypes.data, 2,
+                                    pay.data_ptr(), 0, 1, 1, None, None, s))
+    assert p.resident_slot(good) is None
+    ids = np.array([good, p.encode(1, 0, (1, 0, 0))], dtype=np.int64)
+    eng.advance_frame()
+    eng.apply_bricks(ids, pay)
+    for i, bid in enumerate(ids):
+        slot = p.resident_slot(int(bid))
+        assert slot is not None
+        assert np.array_equal(p.cache[slot], pay[i].numpy())
