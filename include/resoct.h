@@ -128,6 +128,11 @@ typedef struct ro_channel {
     /* interval emptiness (kernels.py:201-206): metadata (mn, mx) is
        transparent iff mx < empty_below[mn] */
     uint16_t empty_below[256];
+    /* largest integer scalar v with opacity 0 on [0, v] (-1: none) */
+    int32_t zero_upto;
+    int32_t _pad;
+    /* per integer scalar j: first knot segment i with x[i+1] >= j */
+    uint8_t tf_seg[256];
 } ro_channel;
 
 /* Per-frame constants, filled on the host. */
@@ -223,6 +228,25 @@ int ro_pack_frame(int32_t k, int32_t m, int32_t depth, int32_t mode,
                   const ro_camera *camera, const ro_render_config *config,
                   const ro_channel_desc *channels, int32_t n_ch, double eps_h,
                   ro_frame *frame);
+
+/* ---- transfer-function queries (host, no CUDA; transfer.py:38-120) ----
+   n knots x[n] (strictly increasing), rgba[n][4]; the host mirror
+   (transfer.TransferFunction) answers every query through these. */
+int ro_tf_evaluate(int32_t n, const double *x, const double *rgba, double v,
+                   double *out4);
+/* inf{x >= a : opacity(x) > 0}, +inf when none */
+int ro_tf_first_support(int32_t n, const double *x, const double *rgba, double a,
+                        double *out);
+/* maximal opaque intervals as (start, end, end_closed) triples, out[3*(n-1)] */
+int ro_tf_support_intervals(int32_t n, const double *x, const double *rgba,
+                            double *out, int32_t *n_out);
+int ro_tf_interval_max_opacity(int32_t n, const double *x, const double *rgba,
+                               double lo, double hi, double *out);
+/* per integer scalar: first support (+inf stored as 1e30), opacity, the
+   emptiness threshold (ro_channel.empty_below) and zero_upto; any output
+   may be NULL */
+int ro_tf_tables(int32_t n, const double *x, const double *rgba, double *first_support,
+                 double *opacity, uint16_t *empty_below, int32_t *zero_upto);
 
 int ro_create(const ro_layout *layout, ro_ctx **out);
 int ro_destroy(ro_ctx *ctx);

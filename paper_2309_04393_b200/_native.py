@@ -65,7 +65,8 @@ class Channel(C.Structure):
     _fields_ = [("slot", _i32), ("lo", _i32), ("hi", _i32), ("npoints", _i32),
                 ("tf_x", _d * RO_MAX_TF_POINTS),
                 ("tf_rgba", (_d * 4) * RO_MAX_TF_POINTS),
-                ("empty_below", C.c_uint16 * 256)]
+                ("empty_below", C.c_uint16 * 256), ("zero_upto", _i32), ("_pad", _i32),
+                ("tf_seg", C.c_uint8 * 256)]
 
 
 class Frame(C.Structure):
@@ -134,6 +135,11 @@ _SIGS = {
     "ro_pack_frame": ([_i32, _i32, _i32, _i32, C.POINTER(CameraDesc),
                        C.POINTER(RenderConfigDesc), C.POINTER(ChannelDesc), _i32, _d,
                        C.POINTER(Frame)], _i32),
+    "ro_tf_evaluate": ([_i32, _p, _p, _d, _p], _i32),
+    "ro_tf_first_support": ([_i32, _p, _p, _d, _p], _i32),
+    "ro_tf_support_intervals": ([_i32, _p, _p, _p, _p], _i32),
+    "ro_tf_interval_max_opacity": ([_i32, _p, _p, _d, _d, _p], _i32),
+    "ro_tf_tables": ([_i32, _p, _p, _p, _p, _p, _p], _i32),
     "ro_upload_state": ([_p, C.POINTER(HostState), C.POINTER(State), _p], _i32),
     "ro_download_state": ([_p, C.POINTER(State), _p, _p, _p, _p, _p, _p, _p, _p, _p], _i32),
     "ro_apply_bricks_lz4": ([_p, C.POINTER(State), _p, _i64, _p, _p, _i32, _i64, _i32, _p,

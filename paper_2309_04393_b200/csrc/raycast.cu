@@ -455,9 +455,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
     for (int i = tid; i < n_ch * 256; i += kBlock) {
         const int c = i / 256, j = i % 256;
         S.empty_below[c][j] = F.ch[c].empty_below[j];
-        int sg = 0;
-        while (sg < F.ch[c].npoints - 2 && F.ch[c].tf_x[sg + 1] < (double)j) ++sg;
-        S.tf_seg[c][j] = (uint8_t)sg;
+        S.tf_seg[c][j] = F.ch[c].tf_seg[j];
     }
     for (int i = tid; i < n_ch * RO_MAX_LEVELS; i += kBlock) {
         const int c = i / RO_MAX_LEVELS, l = i % RO_MAX_LEVELS;
@@ -481,16 +479,8 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
         S.lo[tid] = F.ch[tid].lo;
         S.hi[tid] = F.ch[tid].hi;
         S.np[tid] = F.ch[tid].npoints;
-        // leading zero-opacity range of the piecewise-linear TF (kernels.py:119-133):
-        // below x[0] the TF is transparent; a segment whose two knots have alpha 0
-        // evaluates to 0 + (0 - 0) * t = 0 exactly
-        const ro_channel &c = F.ch[tid];
-        int z = 255;
-        for (int i = 0; i + 1 < c.npoints; ++i) {
-            if (c.tf_rgba[i][3] > 0.0) { z = (int)ceil(c.tf_x[i]) - 1; break; }
-            if (c.tf_rgba[i + 1][3] > 0.0) { z = (int)floor(c.tf_x[i]); break; }
-        }
-        S.zero_upto[tid] = z;  // (a single-knot TF evaluates to 0 everywhere)
+        // leading zero-opacity range of the TF (ro_pack_frame)
+        S.zero_upto[tid] = F.ch[tid].zero_upto;
     }
     if (tid < RO_NUM_COUNTERS) S.red[tid] = 0;
     if (tid == 0) {

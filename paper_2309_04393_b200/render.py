@@ -164,6 +164,12 @@ def _channel_block(slot: int, lo: int, hi: int, tf: TransferFunction) -> N.Chann
     C.memmove(ch.tf_rgba, rgba.ctypes.data, rgba.nbytes)
     eb = np.ascontiguousarray(tf.empty_below(), dtype=np.uint16)
     C.memmove(ch.empty_below, eb.ctypes.data, eb.nbytes)
+    ch.zero_upto = tf.zero_upto()
+    # kernel TF search start: first segment whose right knot is >= j
+    n = len(tf.points)
+    seg = np.searchsorted(xs[1:max(n - 1, 1)], np.arange(256, dtype=np.float64), side="left")
+    seg = np.minimum(seg, max(n - 2, 0)).astype(np.uint8)
+    C.memmove(ch.tf_seg, seg.ctypes.data, seg.nbytes)
     return ch
 
 

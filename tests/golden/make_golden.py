@@ -469,6 +469,58 @@ def lz4_frames():
     return {"items": items, "volume": {"kind": "vessel", "n": 128, "seed": 7}}, rec
 
 
+def tf_queries():
+    """TransferFunction queries answered by the reference's transfer.py
+    (transfer.py:38-120): evaluate at knots / in between / outside, first
+    support at integer and fractional scalars, support intervals, interval
+    emptiness and max opacity, the support table -- on edge-case and seeded
+    random knot sets.  Pins the native TF code (csrc/pack.cu) behind
+    paper_2309_04393_b200.transfer."""
+    rng = np.random.default_rng(2309)
+    tfs = [grayscale_ramp_tf(40.0), grayscale_ramp_tf(0.0, 0.5),
+           TransferFunction(points=((10.0, (1, 0, 0, 0)), (20.0, (0, 1, 0, 0.7)),
+                                    (30.0, (0, 0, 1, 0.2)))),
+           TransferFunction(points=((0.0, (0, 0, 0, 0)), (100.0, (1, 1, 0, 0.9)),
+                                    (101.0, (0, 0, 0, 0)), (255.0, (0, 0, 0, 0)))),
+           TransferFunction(points=((0.0, (0, 0, 0, 0)), (255.0, (0, 0, 0, 0)))),
+           TransferFunction(points=((0.0, (0, 0, 0, 0.3)), (57.5, (0, 0, 0, 0)),
+                                    (200.25, (0, 0, 0, 0)), (255.0, (1, 1, 1, 1)))),
+           TransferFunction(points=((30.0, (0, 0, 0, 0)), (40.0, (0, 0, 0, 1)),
+                                    (50.0, (0, 0, 0, 0)), (180.0, (0, 0, 0, 0)),
+                                    (190.0, (1, 1, 1, 1)))),
+           TransferFunction(points=((12.5, (0.2, 0.3, 0.4, 0.5)), (12.75, (0.9, 0.1, 0.0, 0.0)),
+                                    (13.0, (0.0, 0.0, 0.0, 0.6))))]
+    for _ in range(40):
+        n = int(rng.integers(2, 9))
+        xs = np.sort(rng.choice(np.arange(0, 256 * 4), size=n, replace=False)) / 4.0
+        pts = []
+        for x in xs:
+            a = float(rng.choice([0.0, 0.0, 0.25, 0.6, 1.0]))
+            pts.append((float(x), (float(rng.random()), float(rng.random()),
+                                   float(rng.random()), a)))
+        tfs.append(TransferFunction(points=tuple(pts)))
+    probes = np.concatenate([np.arange(-1.0, 257.0, 0.5), rng.uniform(0, 255, 200)])
+    pairs = rng.integers(0, 256, size=(300, 2))
+    rec, items = {}, []
+    for i, tf in enumerate(tfs):
+        rec[f"x{i}"] = np.array([p[0] for p in tf.points], dtype=np.float64)
+        rec[f"rgba{i}"] = np.array([p[1] for p in tf.points], dtype=np.float64)
+        rec[f"eval{i}"] = np.array([tf.evaluate(float(v)) for v in probes], dtype=np.float64)
+        rec[f"fs{i}"] = np.array([tf.first_support_at_or_after(float(v)) for v in probes],
+                                 dtype=np.float64)
+        f, op = tf.support_table()
+        rec[f"table_f{i}"], rec[f"table_op{i}"] = f, op
+        lo, hi = pairs.min(axis=1), pairs.max(axis=1)
+        rec[f"empty{i}"] = np.array([tf.interval_is_empty(int(a), int(b))
+                                     for a, b in zip(lo, hi)], dtype=np.bool_)
+        rec[f"maxop{i}"] = np.array([tf.interval_max_opacity(float(a), float(b))
+                                     for a, b in pairs], dtype=np.float64)
+        items.append({"support_intervals": [list(iv) for iv in tf.support_intervals()]})
+    rec["probes"] = probes
+    rec["pairs"] = pairs
+    return {"tfs": items}, rec
+
+
 def main():
     tmp = tempfile.mkdtemp()
     only = set(sys.argv[1:])
@@ -478,7 +530,8 @@ def main():
                      ("lru_replay", lru_replay),
                      ("baselines_sparse256x4", lambda: baselines_sparse256x4(tmp)),
                      ("baselines_vessel256", baselines_vessel256),
-                     ("lz4_frames", lz4_frames)):
+                     ("lz4_frames", lz4_frames),
+                     ("tf_queries", tf_queries)):
         if only and name not in only:
             continue
         print("generating", name, flush=True)
