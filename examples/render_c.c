@@ -170,6 +170,7 @@ int main(int argc, char **argv) {
     CUDA(cudaMalloc((void **)&fb.meta_keys, sizeof(int64_t) * BUDGET));
     CUDA(cudaMalloc((void **)&fb.meta_ids, sizeof(int64_t) * BUDGET));
     fb.counts = counts;
+    fb.counts_dev = NULL;
     CHECK(ro_feedback_collect(ctx, BUDGET, 1, &fb, NULL));
     CHECK(ro_sync(ctx, NULL));
 

@@ -191,8 +191,10 @@ typedef struct ro_outputs {
 typedef struct ro_feedback {
     int64_t *brick_keys, *brick_ids; /* [budget] device */
     int64_t *meta_keys, *meta_ids;   /* [budget] device; meta id = node*m+slot */
-    int64_t *counts;                 /* [4] HOST: unique bricks, unique metas,
-                                        bricks emitted, metas emitted */
+    int64_t *counts;                 /* [4] HOST (or NULL): unique bricks, unique
+                                        metas, bricks emitted, metas emitted */
+    int64_t *counts_dev;             /* [4] DEVICE (or NULL): the same counts,
+                                        written on the stream */
 } ro_feedback;
 
 typedef struct ro_ctx ro_ctx;
@@ -261,7 +263,10 @@ int ro_render(ro_ctx *ctx, const ro_frame *frame, const ro_state *state,
 /* Order the frame's first-seen requests and truncate them: with
    bricks_first=1 metas get budget-(bricks emitted) (render.py:210-215),
    otherwise each list is cut to `budget` independently (per-part lists of a
-   sort-first frame, merged later).  Synchronises the stream. */
+   sort-first frame, merged later).  Everything runs on the device (one
+   kernel, no library call).  With fb->counts (host) set the call
+   synchronises the stream once at the end to fill it; with only
+   fb->counts_dev set it is fully asynchronous. */
 int ro_feedback_collect(ro_ctx *ctx, int64_t budget, int32_t bricks_first,
                         const ro_feedback *fb, void *stream);
 

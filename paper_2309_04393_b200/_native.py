@@ -107,7 +107,7 @@ class Outputs(C.Structure):
 
 class Feedback(C.Structure):
     _fields_ = [("brick_keys", _p), ("brick_ids", _p), ("meta_keys", _p),
-                ("meta_ids", _p), ("counts", _p)]
+                ("meta_ids", _p), ("counts", _p), ("counts_dev", _p)]
 
 
 _LIB = None

@@ -182,6 +182,7 @@ int ro_create(const ro_layout *layout, ro_ctx **out) {
     TRY(cudaMalloc(&c->claim, sizeof(uint32_t) * c->E));
     TRY(cudaMemset(c->claim, 0, sizeof(uint32_t) * c->E));
     TRY(cudaMallocHost(&c->pinned_small, sizeof(int64_t) * 64));
+    if (L.depth <= 9) TRY(cudaMalloc(&c->node_class, (size_t)c->num_nodes));
     TRY(cudaStreamCreateWithFlags(&c->upload, cudaStreamNonBlocking));
     TRY(cudaEventCreateWithFlags(&c->upload_done, cudaEventDisableTiming));
     TRY(cudaEventCreateWithFlags(&c->host_done, cudaEventDisableTiming));
@@ -200,6 +201,7 @@ int ro_destroy(ro_ctx *c) {
     cudaFree(c->meta_touched);
     cudaFree(c->touched_n);
     cudaFree(c->claim);
+    cudaFree(c->node_class);
     for (int i = 0; i < 12; ++i) cudaFree(c->scratch[i]);
     if (c->pinned_small) cudaFreeHost(c->pinned_small);
     if (c->staging) cudaFreeHost(c->staging);
@@ -222,7 +224,7 @@ int ro_render(ro_ctx *c, const ro_frame *frame, const ro_state *st, const ro_out
 
 int ro_feedback_collect(ro_ctx *c, int64_t budget, int32_t bricks_first,
                         const ro_feedback *fb, void *stream) {
-    if (!c || !fb || !fb->counts) return fail(RO_EINVAL, "null argument");
+    if (!c || !fb || (!fb->counts && !fb->counts_dev)) return fail(RO_EINVAL, "null argument");
     if (budget > 0 && (!fb->brick_keys || !fb->brick_ids || !fb->meta_keys || !fb->meta_ids))
         return fail(RO_EINVAL, "null feedback buffer");
     return feedback_collect(c, budget, bricks_first, fb, (cudaStream_t)stream);

@@ -2,42 +2,75 @@
 //
 // The ray caster leaves, per touched brick / metadata entry, the smallest
 // (pixel << 32 | event) key of any request for it (raycast.cu, RED.MIN).
-// Sorting the touched entries by that key reproduces the reference's
+// Ordering the touched entries by that key reproduces the reference's
 // single-threaded first-seen append order (kernels.py:457-517, seen_brick /
 // seen_meta); the bricks-first budget is render.py:210-215.
 //
-// Touched entries are found by one streaming pass over the key arrays
-// (E u64 for bricks, N*m u64 for metadata: 0.6 MB + 9.6 MB at config 2),
-// which also resets them for the next frame -- cheaper than making every
-// request wait for an atomic's return value in the ray caster.
-#include <cub/cub.cuh>
+// One cooperative kernel (k_feedback) does the whole frame's ordering, with
+// no host round trip and no library call:
+//   A. a streaming pass over both key arrays compacts the touched (key,
+//      entry) pairs and resets the keys for the next frame (warp-aggregated
+//      appends), and finds the largest pixel and event index;       grid sync
+//   B. keys are repacked order-preservingly as q = pixel << ev_bits | event;
+//      only the `keep` smallest survive the budget, so instead of sorting
+//      every touched entry the kernel radix-SELECTS the keep-th smallest q
+//      (8-bit digits from the top, one histogram pass per digit over the
+//      candidates, grid sync per digit) -- skipped when everything survives;
+//   C. the survivors (q <= threshold) are gathered into the output range and
+//      one CTA sorts them in shared memory (bitonic, <= kChunk pairs) and
+//      writes the unpacked keys and the decoded BrickIDs.
+// Budgets above kChunk are cut into consecutive rank chunks, each selected
+// and sorted the same way.  Nothing synchronises the host: the counts land
+// in device memory (and, for the synchronous API, in host memory after one
+// final copy).
+#include <cooperative_groups.h>
 
 #include "internal.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace ro {
 
 namespace {
 
-constexpr unsigned kScanBlocks = 148 * 4;
+constexpr int kFbThreads = 1024;
+constexpr int kChunk = 8192;  // pairs sorted per CTA in shared memory (96 KB)
+constexpr size_t kFbSmem = (size_t)kChunk * (sizeof(unsigned long long) + sizeof(int32_t));
 
-// compact (key, entry) of every touched entry, reset the key; warp-aggregated
-// slot allocation
-// (also the largest pixel and event index among the touched keys, so the
-// sort only has to order the bits those need)
-__global__ void __launch_bounds__(256) k_compact(unsigned long long *__restrict__ keys,
-                                                 int64_t n,
-                                                 unsigned long long *__restrict__ out_keys,
-                                                 int32_t *__restrict__ out_vals,
-                                                 int32_t *__restrict__ count,
-                                                 unsigned *__restrict__ maxes) {
-    unsigned mpix = 0, mev = 0;
+// ctl block (u32, zeroed before the launch):
+//   [0] touched bricks  [1] touched metas  [2] max pixel  [3] max event
+//   [8 ..)          gather counters, one per chunk
+//   [kHistOff ..)   3 x 256 digit histograms (a ring, see select())
+constexpr int kMaxChunks = 1024;
+constexpr int kHistOff = 8 + kMaxChunks;
+constexpr int kCtlWords = kHistOff + 3 * 256;
+
+struct FbArgs {
+    DevLayout L;
+    unsigned long long *bkeys;  // [E] first-seen keys (~0 = untouched)
+    int64_t nbk;
+    unsigned long long *mkeys;  // [n_meta] (may be null)
+    int64_t nmk;
+    unsigned long long *cand_k;  // [E + n_meta] compacted keys (bricks, then metas at +E)
+    int32_t *cand_v;             // [E + n_meta] entries
+    uint32_t *ctl;
+    int64_t budget;
+    int32_t bricks_first;
+    int64_t *out_bkeys, *out_bids, *out_mkeys, *out_mids;  // [budget] each
+    int64_t *counts;  // [4] device: touched bricks, touched metas, emitted, emitted
+};
+
+__device__ __forceinline__ int bit_len(unsigned v) { return v ? 32 - __clz(v) : 0; }
+
+// phase A: one list's key array -> compacted candidates
+__device__ void compact(unsigned long long *__restrict__ keys, int64_t n,
+                        unsigned long long *__restrict__ out_k, int32_t *__restrict__ out_v,
+                        uint32_t *count, unsigned &mpix, unsigned &mev) {
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    // warp-uniform trip count (the shuffles need all 32 lanes)
-    for (int64_t wb = warp * 64; wb < n; wb += nwarps * 64) {
+    for (int64_t wb = warp * 64; wb < n; wb += nwarps * 64) {  // warp-uniform trip count
         const int64_t base = wb + 2 * lane;
-        // two entries per lane: 16-byte loads
         unsigned long long k0 = ~0ull, k1 = ~0ull;
         if (base + 1 < n) {
             const ulonglong2 v = *reinterpret_cast<const ulonglong2 *>(keys + base);
@@ -49,73 +82,211 @@ __global__ void __launch_bounds__(256) k_compact(unsigned long long *__restrict_
         const bool t0 = k0 != ~0ull, t1 = k1 != ~0ull;
         if (t0) { mpix = max(mpix, (unsigned)(k0 >> 32)); mev = max(mev, (unsigned)k0); }
         if (t1) { mpix = max(mpix, (unsigned)(k1 >> 32)); mev = max(mev, (unsigned)k1); }
-        const int mine = (int)t0 + (int)t1;
-        int incl = mine;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
-        }
-        const int total = __shfl_sync(0xffffffffu, incl, 31);
-        int basepos = 0;
-        if (lane == 31 && total) basepos = atomicAdd(count, total);
-        basepos = __shfl_sync(0xffffffffu, basepos, 31);
-        int pos = basepos + incl - mine;
+        const unsigned b0 = __ballot_sync(0xffffffffu, t0), b1 = __ballot_sync(0xffffffffu, t1);
+        const int total = __popc(b0) + __popc(b1);
+        if (total == 0) continue;
+        uint32_t basepos = 0;
+        if (lane == 0) basepos = atomicAdd(count, (uint32_t)total);
+        basepos = __shfl_sync(0xffffffffu, basepos, 0);
+        const unsigned below = (1u << lane) - 1u;
+        uint32_t pos = basepos + __popc(b0 & below) + __popc(b1 & below);
         if (t0) {
-            out_keys[pos] = k0;
-            out_vals[pos] = (int32_t)base;
+            out_k[pos] = k0;
+            out_v[pos] = (int32_t)base;
             keys[base] = ~0ull;
             ++pos;
         }
         if (t1) {
-            out_keys[pos] = k1;
-            out_vals[pos] = (int32_t)(base + 1);
+            out_k[pos] = k1;
+            out_v[pos] = (int32_t)(base + 1);
             keys[base + 1] = ~0ull;
         }
     }
+}
+
+__device__ __forceinline__ unsigned long long pack(unsigned long long k, int ev_bits) {
+    return ((k >> 32) << ev_bits) | (k & 0xFFFFFFFFull);
+}
+__device__ __forceinline__ unsigned long long unpack(unsigned long long q, int ev_bits) {
+    return ((q >> ev_bits) << 32) | (q & ((1ull << ev_bits) - 1ull));
+}
+
+// Exact `need`-th smallest packed key among the candidates with q > lo (lo
+// ignored when !has_lo).  Histogram ring H[g % 3]: step g accumulates into
+// H[g%3] before the grid sync; after it, every CTA reads H[g%3] and CTA 0
+// clears H[(g+2)%3] (read by nobody after the previous sync).
+__device__ unsigned long long select(cg::grid_group &grid, const unsigned long long *cand,
+                                     int64_t n, int ev_bits, bool has_lo,
+                                     unsigned long long lo, int64_t need, int top_shift,
+                                     uint32_t *ctl, uint32_t &g, uint32_t *s_hist) {
+    unsigned long long prefix = 0;
+    for (int shift = top_shift; shift >= 0; shift -= 8) {
+        uint32_t *H = ctl + kHistOff + 256 * (g % 3);
+        for (int i = threadIdx.x; i < 256; i += blockDim.x) s_hist[i] = 0;
+        __syncthreads();
+        const int hs = shift + 8;
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+             i += (int64_t)gridDim.x * blockDim.x) {
+            const unsigned long long q = pack(__ldcg(cand + i), ev_bits);
+            if (has_lo && q <= lo) continue;
+            if (hs < 64 && (q >> hs) != (prefix >> hs)) continue;
+            atomicAdd(&s_hist[(q >> shift) & 255], 1u);
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < 256; i += blockDim.x)
+            if (s_hist[i]) atomicAdd(&H[i], s_hist[i]);
+        grid.sync();
+        // every CTA finds the digit where the running count reaches `need`
+        __shared__ uint32_t s_sel[2];
+        if (threadIdx.x < 32) {
+            uint32_t c[8];
+            uint32_t run = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                c[j] = __ldcg(&H[threadIdx.x * 8 + j]);
+                run += c[j];
+            }
+            uint32_t incl = run;
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if ((int)threadIdx.x >= o) incl += y;
+            }
+            uint32_t before = incl - run;  // candidates in lower digit groups
+            if ((int64_t)before < need && need <= (int64_t)incl) {
+                for (int j = 0; j < 8; ++j) {
+                    if (need <= (int64_t)(before + c[j])) {
+                        s_sel[0] = threadIdx.x * 8 + j;
+                        s_sel[1] = before;
+                        break;
+                    }
+                    before += c[j];
+                }
+            }
+        }
+        if (blockIdx.x == 0) {
+            uint32_t *Hz = ctl + kHistOff + 256 * ((g + 2) % 3);
+            for (int i = threadIdx.x; i < 256; i += blockDim.x) Hz[i] = 0;
+        }
+        __syncthreads();
+        prefix |= (unsigned long long)s_sel[0] << shift;
+        need -= s_sel[1];
+        ++g;
+        __syncthreads();
+    }
+    return prefix;
+}
+
+// one CTA: sort the gathered [base, base+w) (q in okeys, entry in oids) and
+// write the unpacked keys / decoded ids back
+__device__ void sort_emit(const DevLayout &L, bool bricks, int64_t *okeys, int64_t *oids,
+                          int64_t w, int ev_bits, unsigned char *smem) {
+    auto *sk = reinterpret_cast<unsigned long long *>(smem);
+    auto *sv = reinterpret_cast<int32_t *>(sk + kChunk);
+    int np = 1;
+    while (np < w) np <<= 1;
+    for (int i = threadIdx.x; i < np; i += blockDim.x) {
+        if (i < w) {
+            sk[i] = (unsigned long long)__ldcg(okeys + i);
+            sv[i] = (int32_t)__ldcg(oids + i);
+        } else {
+            sk[i] = ~0ull;
+            sv[i] = -1;
+        }
+    }
+    __syncthreads();
+    for (int size = 2; size <= np; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int i = threadIdx.x; i < np / 2; i += blockDim.x) {
+                const int lo = 2 * i - (i & (stride - 1));
+                const int hi = lo + stride;
+                const bool up = (lo & size) == 0;
+                const unsigned long long a = sk[lo], b = sk[hi];
+                if ((a > b) == up) {
+                    sk[lo] = b;
+                    sk[hi] = a;
+                    const int32_t t = sv[lo];
+                    sv[lo] = sv[hi];
+                    sv[hi] = t;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (int i = threadIdx.x; i < w; i += blockDim.x) {
+        okeys[i] = (int64_t)unpack(sk[i], ev_bits);
+        oids[i] = bricks ? entry_to_id(L, sv[i]) : (int64_t)sv[i];
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kFbThreads, 1) k_feedback(const __grid_constant__ FbArgs A) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ uint32_t s_hist[256];
+    cg::grid_group grid = cg::this_grid();
+    uint32_t *ctl = A.ctl;
+
+    // ---- A: compaction ----
+    unsigned mpix = 0, mev = 0;
+    compact(A.bkeys, A.nbk, A.cand_k, A.cand_v, &ctl[0], mpix, mev);
+    if (A.mkeys) compact(A.mkeys, A.nmk, A.cand_k + A.nbk, A.cand_v + A.nbk, &ctl[1], mpix, mev);
     mpix = __reduce_max_sync(0xffffffffu, mpix);
     mev = __reduce_max_sync(0xffffffffu, mev);
-    if (lane == 0 && (mpix | mev)) {
-        atomicMax(&maxes[0], mpix);
-        atomicMax(&maxes[1], mev);
+    if ((threadIdx.x & 31) == 0 && (mpix | mev)) {
+        atomicMax(&ctl[2], mpix);
+        atomicMax(&ctl[3], mev);
     }
-}
+    grid.sync();
 
-// (pixel << 32 | event) -> (pixel << ev_bits | event): order-preserving and
-// injective while pixel < 2^pix_bits and event < 2^ev_bits
-__global__ void k_pack_keys(const unsigned long long *__restrict__ in, int32_t n, int ev_bits,
-                            uint32_t *__restrict__ out) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const unsigned long long k = in[i];
-    out[i] = ((uint32_t)(k >> 32) << ev_bits) | (uint32_t)k;
-}
+    const int64_t nb = __ldcg(&ctl[0]), nm = __ldcg(&ctl[1]);
+    const int ev_bits = bit_len(__ldcg(&ctl[3]));
+    const int tb = bit_len(__ldcg(&ctl[2])) + ev_bits;
+    const int top_shift = tb > 8 ? ((tb + 7) / 8 - 1) * 8 : 0;
+    const int64_t kb = nb < A.budget ? nb : A.budget;
+    const int64_t rest = A.bricks_first ? A.budget - kb : A.budget;
+    const int64_t km = nm < rest ? nm : rest;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        A.counts[0] = nb;
+        A.counts[1] = nm;
+        A.counts[2] = kb;
+        A.counts[3] = km;
+    }
 
-__device__ __forceinline__ unsigned long long unpack_key(uint32_t k, int ev_bits) {
-    return ((unsigned long long)(k >> ev_bits) << 32) | (k & ((1u << ev_bits) - 1u));
-}
-
-__global__ void k_emit_bricks(const DevLayout L,
-                              const unsigned long long *__restrict__ keys,
-                              const uint32_t *__restrict__ keys32, int ev_bits,
-                              const int32_t *__restrict__ vals, int32_t n,
-                              int64_t *__restrict__ out_keys,
-                              int64_t *__restrict__ out_ids) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    out_keys[i] = (int64_t)(keys32 ? unpack_key(keys32[i], ev_bits) : keys[i]);
-    out_ids[i] = entry_to_id(L, vals[i]);
-}
-
-__global__ void k_emit_metas(const unsigned long long *__restrict__ keys,
-                             const uint32_t *__restrict__ keys32, int ev_bits,
-                             const int32_t *__restrict__ vals, int32_t n,
-                             int64_t *__restrict__ out_keys,
-                             int64_t *__restrict__ out_ids) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    out_keys[i] = (int64_t)(keys32 ? unpack_key(keys32[i], ev_bits) : keys[i]);
-    out_ids[i] = vals[i];
+    // ---- B + C per list, in rank chunks ----
+    uint32_t g = 0;   // histogram ring step (identical in every CTA)
+    int chunk = 0;    // gather counter index (identical in every CTA)
+    for (int list = 0; list < 2; ++list) {
+        const bool bricks = list == 0;
+        const int64_t n = bricks ? nb : nm;
+        const int64_t keep = bricks ? kb : km;
+        const unsigned long long *cand = A.cand_k + (bricks ? 0 : A.nbk);
+        const int32_t *candv = A.cand_v + (bricks ? 0 : A.nbk);
+        int64_t *okeys = bricks ? A.out_bkeys : A.out_mkeys;
+        int64_t *oids = bricks ? A.out_bids : A.out_mids;
+        bool has_lo = false;
+        unsigned long long lo = 0;
+        for (int64_t done = 0; done < keep; done += kChunk, ++chunk) {
+            const int64_t w = keep - done < kChunk ? keep - done : kChunk;
+            // threshold: the w-th smallest above lo, or everything left
+            unsigned long long hi = ~0ull;
+            if (done + w < n)
+                hi = select(grid, cand, n, ev_bits, has_lo, lo, w, top_shift, ctl, g, s_hist);
+            uint32_t *cnt = &ctl[8 + (chunk % kMaxChunks)];
+            for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+                 i += (int64_t)gridDim.x * blockDim.x) {
+                const unsigned long long q = pack(__ldcg(cand + i), ev_bits);
+                if ((has_lo && q <= lo) || q > hi) continue;
+                const uint32_t pos = atomicAdd(cnt, 1u);
+                okeys[done + pos] = (int64_t)q;
+                oids[done + pos] = __ldcg(candv + i);
+            }
+            grid.sync();
+            // one CTA per chunk sorts it; the others go on selecting
+            if (blockIdx.x == (unsigned)(chunk % gridDim.x))
+                sort_emit(A.L, bricks, okeys + done, oids + done, w, ev_bits, smem);
+            has_lo = true;
+            lo = hi;
+        }
+    }
 }
 
 // engine.py:72-81: every sampled entry that is MAPPED stamps its slot
@@ -131,104 +302,63 @@ __global__ void k_note_sampled(const uint8_t *__restrict__ required,
     }
 }
 
-inline unsigned scan_blocks(int64_t n) {
-    int64_t b = (n + 511) / 512;
-    if (b < 1) b = 1;
-    if (b > kScanBlocks) b = kScanBlocks;
-    return (unsigned)b;
-}
-
-inline int bit_length(unsigned v) { return v ? 32 - __builtin_clz(v) : 0; }
-
-// sort the n compacted (key, entry) pairs and emit the first `keep`.  Only
-// the key bits in use are ordered: (pixel, event) packed into 32 bits when
-// they fit (4 radix passes instead of 8), else the 64-bit key up to the top
-// pixel bit.
-int sort_and_emit(ro_ctx *c, unsigned long long *k_in, int32_t *v_in, int32_t n,
-                  int32_t keep, bool bricks, int pix_bits, int ev_bits,
-                  int64_t *out_keys, int64_t *out_ids, cudaStream_t s) {
-    if (n <= 0 || keep <= 0) return RO_OK;
-    void *p1, *p3, *tmp;
-    int rc;
-    if ((rc = scratch(c, 3, sizeof(int32_t) * n, &p3))) return rc;
-    auto *v_out = (int32_t *)p3;
-    size_t tmp_bytes = 0;
-    const unsigned long long *k64 = nullptr;
-    const uint32_t *k32 = nullptr;
-    if (pix_bits + ev_bits <= 32) {
-        void *p5, *p6;
-        if ((rc = scratch(c, 5, sizeof(uint32_t) * n, &p5))) return rc;
-        if ((rc = scratch(c, 6, sizeof(uint32_t) * n, &p6))) return rc;
-        auto *q_in = (uint32_t *)p5, *q_out = (uint32_t *)p6;
-        k_pack_keys<<<(n + 255) / 256, 256, 0, s>>>(k_in, n, ev_bits, q_in);
-        const int end_bit = pix_bits + ev_bits > 0 ? pix_bits + ev_bits : 1;
-        RO_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, q_in, q_out, v_in, v_out, n,
-                                                0, end_bit, s));
-        if ((rc = scratch(c, 4, tmp_bytes, &tmp))) return rc;
-        RO_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, q_in, q_out, v_in, v_out, n, 0,
-                                                end_bit, s));
-        k32 = q_out;
-    } else {
-        if ((rc = scratch(c, 1, sizeof(unsigned long long) * n, &p1))) return rc;
-        auto *k_out = (unsigned long long *)p1;
-        const int end_bit = 32 + pix_bits;
-        RO_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k_in, k_out, v_in, v_out, n,
-                                                0, end_bit, s));
-        if ((rc = scratch(c, 4, tmp_bytes, &tmp))) return rc;
-        RO_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, k_in, k_out, v_in, v_out, n, 0,
-                                                end_bit, s));
-        k64 = k_out;
-    }
-    if (bricks)
-        k_emit_bricks<<<(keep + 255) / 256, 256, 0, s>>>(c->dl, k64, k32, ev_bits, v_out, keep,
-                                                          out_keys, out_ids);
-    else
-        k_emit_metas<<<(keep + 255) / 256, 256, 0, s>>>(k64, k32, ev_bits, v_out, keep, out_keys,
-                                                         out_ids);
-    RO_CUDA(cudaGetLastError());
-    return RO_OK;
-}
-
 }  // namespace
 
 int feedback_collect(ro_ctx *c, int64_t budget, int32_t bricks_first,
                      const ro_feedback *fb, cudaStream_t s) {
     if (budget < 0) return fail(RO_EINVAL, "negative budget");
+    if (budget > (int64_t)kChunk * (kMaxChunks / 2 - 1))
+        return fail(RO_EINVAL, "request budget above 4M entries");
     const int64_t n_meta = meta_keys(c) ? c->n_meta : 0;
-    void *p0, *p2;
+    void *p0, *p2, *pc;
     int rc;
-    // compacted arrays: bricks at [0, E), metas at [E, E + n_meta)
+    // compacted candidates: bricks at [0, E), metas at [E, E + n_meta)
     if ((rc = scratch(c, 0, sizeof(unsigned long long) * (c->E + n_meta), &p0))) return rc;
     if ((rc = scratch(c, 2, sizeof(int32_t) * (c->E + n_meta), &p2))) return rc;
-    auto *ck = (unsigned long long *)p0;
-    auto *cv = (int32_t *)p2;
-    // touched_n: [0] bricks, [1] metas, [2] max pixel, [3] max event
-    RO_CUDA(cudaMemsetAsync(c->touched_n, 0, 4 * sizeof(int32_t), s));
-    auto *maxes = reinterpret_cast<unsigned *>(c->touched_n + 2);
-    k_compact<<<scan_blocks(c->E), 256, 0, s>>>(brick_keys(c), c->E, ck, cv, c->touched_n,
-                                                maxes);
-    if (n_meta)
-        k_compact<<<scan_blocks(n_meta), 256, 0, s>>>(meta_keys(c), n_meta, ck + c->E,
-                                                      cv + c->E, c->touched_n + 1, maxes);
-    RO_CUDA(cudaGetLastError());
-    int32_t *hn = reinterpret_cast<int32_t *>(c->pinned_small);
-    RO_CUDA(cudaMemcpyAsync(hn, c->touched_n, 4 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    RO_CUDA(cudaStreamSynchronize(s));
-    const int32_t nb = hn[0], nm = hn[1];
-    const int pix_bits = bit_length((unsigned)hn[2]), ev_bits = bit_length((unsigned)hn[3]);
-    const int32_t kb = (int32_t)(nb < budget ? nb : budget);
-    const int64_t rest = bricks_first ? budget - kb : budget;
-    const int32_t km = (int32_t)(nm < rest ? nm : rest);
-    rc = sort_and_emit(c, ck, cv, nb, kb, true, pix_bits, ev_bits, fb->brick_keys,
-                       fb->brick_ids, s);
-    if (rc) return rc;
-    rc = sort_and_emit(c, ck + c->E, cv + c->E, nm, km, false, pix_bits, ev_bits,
-                       fb->meta_keys, fb->meta_ids, s);
-    if (rc) return rc;
-    fb->counts[0] = nb;
-    fb->counts[1] = nm;
-    fb->counts[2] = kb;
-    fb->counts[3] = km;
+    if ((rc = scratch(c, 11, sizeof(uint32_t) * kCtlWords + sizeof(int64_t) * 8, &pc))) return rc;
+    auto *ctl = (uint32_t *)pc;
+    auto *dcounts = fb->counts_dev ? fb->counts_dev
+                                   : reinterpret_cast<int64_t *>(ctl + kCtlWords + (kCtlWords & 1));
+    static int64_t dummy[1];
+    FbArgs A;
+    A.L = c->dl;
+    A.bkeys = brick_keys(c);
+    A.nbk = c->E;
+    A.mkeys = n_meta ? meta_keys(c) : nullptr;
+    A.nmk = n_meta;
+    A.cand_k = (unsigned long long *)p0;
+    A.cand_v = (int32_t *)p2;
+    A.ctl = ctl;
+    A.budget = budget;
+    A.bricks_first = bricks_first;
+    // outputs may be null with budget 0 (nothing is written then)
+    A.out_bkeys = fb->brick_keys ? fb->brick_keys : dummy;
+    A.out_bids = fb->brick_ids ? fb->brick_ids : dummy;
+    A.out_mkeys = fb->meta_keys ? fb->meta_keys : dummy;
+    A.out_mids = fb->meta_ids ? fb->meta_ids : dummy;
+    A.counts = dcounts;
+    static int grid = 0;
+    if (grid == 0) {
+        RO_CUDA(cudaFuncSetAttribute(k_feedback, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)kFbSmem));
+        int dev = 0, sms = 0, per_sm = 0;
+        RO_CUDA(cudaGetDevice(&dev));
+        RO_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        RO_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_feedback, kFbThreads,
+                                                              kFbSmem));
+        if (per_sm < 1) return fail(RO_ECUDA, "feedback kernel cannot be resident");
+        grid = sms;  // one CTA per SM
+    }
+    RO_CUDA(cudaMemsetAsync(ctl, 0, sizeof(uint32_t) * kCtlWords, s));
+    void *args[] = {&A};
+    RO_CUDA(cudaLaunchCooperativeKernel((const void *)k_feedback, dim3(grid), dim3(kFbThreads),
+                                        args, kFbSmem, s));
+    if (fb->counts) {  // synchronous form: counts on the host when the call returns
+        int64_t *h = c->pinned_small + 8;
+        RO_CUDA(cudaMemcpyAsync(h, dcounts, 4 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        RO_CUDA(cudaStreamSynchronize(s));
+        for (int i = 0; i < 4; ++i) fb->counts[i] = h[i];
+    }
     return RO_OK;
 }
 

@@ -192,6 +192,9 @@ struct ro_ctx {
     unsigned long long *brick_key_ext = nullptr;
     unsigned long long *meta_key_ext = nullptr;
     uint32_t epoch = 0;
+    // per-frame node classes of the ray caster's residency walk (raycast.cu
+    // k_classify_nodes): [num_nodes] bytes, allocated with the context
+    uint8_t *node_class = nullptr;
 };
 
 namespace ro {

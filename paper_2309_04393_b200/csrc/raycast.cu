@@ -144,6 +144,7 @@ struct RayArgs {
     int32_t *tile_counter;   // persistent-CTA work counter (zeroed per launch)
     const uint8_t *sub_max;  // [S*nsb] dilated 8^3 sub-block maxima (optional)
     int32_t nsb;             // sub-blocks per slot
+    const uint8_t *node_class;  // [num_nodes] k_classify_nodes output (optional)
 };
 
 __device__ __forceinline__ double lerp(double a, double b, double t) {
@@ -428,6 +429,56 @@ struct SampleCtx {
     int tp_lev;
     LevelPos lp2;  // the last substitute level (kernels.py:518-549)
 };
+
+// Per-frame node classes for the residency walk (kernels.py:444-517).
+// A node is "plain" for channel ci when the reference's walk would just step
+// through it: valid metadata, not transparent under ci's TF (_is_empty_meta),
+// not homogeneous, and some level resident (mask != 0).  node_class[x] = 1 iff
+// x is plain for every visible channel AND x and all its ancestors are plain
+// for channel 0.  The ray caster takes a sample whose depth-dt node is class 1
+// straight to the page-table probes at dt: channel 0 walks d0..dt through
+// plain nodes, every later channel visits only the (plain) dt node -- exactly
+// dt - d0 + n_ch node visits and no request events, as the reference's walk.
+// One thread per node; ancestors are re-read (L1/L2 hits, ~0.3 M nodes at D=6).
+__global__ void __launch_bounds__(256) k_classify_nodes(const __grid_constant__ ro_frame F,
+                                                        const uint32_t *__restrict__ words,
+                                                        int m, int D, int64_t n_nodes,
+                                                        uint8_t *__restrict__ out) {
+    __shared__ uint16_t eb[RO_MAX_CH][256];
+    const int n_ch = F.n_ch;
+    for (int i = threadIdx.x; i < n_ch * 256; i += blockDim.x)
+        eb[i >> 8][i & 255] = F.ch[i >> 8].empty_below[i & 255];
+    __syncthreads();
+    const int eps_i = F.eps_h >= 255.0 ? 255 : (F.eps_h < 0.0 ? -1 : (int)F.eps_h);
+    auto plain = [&](int64_t node, int ci) -> bool {
+        const uint32_t w = __ldg(words + node * m + F.ch[ci].slot);
+        const int mn = (w >> 16) & 0xFF, mx = (int)(w >> 24);
+        if (mn == 255 && mx == 0) return false;        // INVALID: metadata request
+        if (mx < (int)eb[ci][mn]) return false;         // K_ZERO
+        if (mx - mn <= eps_i) return false;             // K_CONST
+        return (w & 0xFFFFu) != 0;                      // else K_MISSU
+    };
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n_nodes; x += stride) {
+        int d = 0;
+        while (d < D && level_offset(d + 1) <= x) ++d;
+        bool ok = true;
+        for (int ci = 0; ci < n_ch && ok; ++ci) ok = plain(x, ci);
+        if (ok && d > 0) {
+            const int64_t local = x - level_offset(d);
+            const int side_mask = (1 << d) - 1;
+            const int nx = (int)(local & side_mask), ny = (int)((local >> d) & side_mask),
+                      nz = (int)(local >> (2 * d));
+            for (int a = d - 1; a >= 0 && ok; --a) {
+                const int sh = d - a;
+                const int64_t anc = level_offset(a) +
+                                    ((((int64_t)(nz >> sh) << a) + (ny >> sh)) << a) + (nx >> sh);
+                ok = plain(anc, 0);
+            }
+        }
+        out[x] = ok ? 1 : 0;
+    }
+}
 
 template <int MODE, bool CHECK, int BX, int BY>
 __global__ void __launch_bounds__(kBlock, RO_MINB * 4 / kWarps)
@@ -796,6 +847,29 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                 int cur_node = -1;
                 uint4 wv = make_uint4(0, 0, 0, 0);
                 const int d0 = d;
+                // pre-classified depth-dt node (k_classify_nodes): every
+                // channel reaches dt through plain nodes and probes there
+                bool fast = false;
+                if (A.node_class != nullptr) {
+                    const int sh = D - dt_;
+                    const int lx = qx >> sh, lyy = qy >> sh, lz = qz >> sh;
+                    const int leaf = S.lvl_off[dt_] + (((lz << dt_) + lyy) << dt_) + lx;
+                    RO_ASSERT(leaf >= 0 && leaf < A.L.num_nodes);
+                    fast = __ldg(A.node_class + leaf) != 0;
+                    if (fast) {
+                        c_steps += dt_ - d0 + n_ch;
+                        d = dt_;
+                        ix = lx;
+                        iy = lyy;
+                        iz = lz;
+                        if (vec4) {
+                            wv = ld_meta4(reinterpret_cast<const uint4 *>(A.words) + leaf);
+                            cur_node = leaf;
+                        } else {
+                            cur_node = leaf;
+                        }
+                    }
+                }
 #if RO_FAST_DESCENT
                 // Channel 0 walks d0 -> dt through nodes known up front (the
                 // ancestors of the sample position).  Load its word at every depth
@@ -804,7 +878,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                 // resident); the generic loop below resumes exactly there.  Any
                 // INVALID ancestor (it would issue a metadata request) stops the
                 // fast walk at that node, so requests stay in program order.
-                if (dt_ - d0 >= 1 && dt_ - d0 <= kFastDepth) {
+                if (!fast && dt_ - d0 >= 1 && dt_ - d0 <= kFastDepth) {
                     const int slot0 = CH_SLOT(0);
                     uint32_t pw[kFastDepth];
 #pragma unroll
@@ -838,6 +912,12 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
 #pragma unroll 1
                 for (int ci = 0; ci < n_ch; ++ci) {
                     const int slot = CH_SLOT(ci);
+                    uint32_t mask;
+                    if (fast) {
+                        mask = (vec4 ? (slot == 0 ? wv.x : slot == 1 ? wv.y : slot == 2 ? wv.z : wv.w)
+                                     : __ldg(A.words + cur_node * m + slot)) & 0xFFFFu;
+                    } else {
+                    bool probe = false;
                     while (true) {
                         const int sh = D - d;
                         ix = qx >> sh;
@@ -858,7 +938,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                             w = __ldg(A.words + nidx * m + slot);
                         }
                         const int mn = (w >> 16) & 0xFF, mx = (w >> 24) & 0xFF;
-                        const uint32_t mask = w & 0xFFFF;
+                        mask = w & 0xFFFF;
                         if (mn == 255 && mx == 0) {  // INVALID: metadata request
                             const int32_t mid = nidx * m + slot;
                             const unsigned long long key = key_hi | ev++;
@@ -900,15 +980,22 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                             d += 1;
                             continue;
                         }
-                        // at traversal depth: probe the desired brick
+                        probe = true;
+                        break;
+                    }
+                    if (!probe) continue;
+                    }
+                    // at traversal depth: probe the desired brick
+                    {
                         all_cz = false;
+                        const int lev = clampi(raw, CH_LO(ci), CH_HI(ci));
                         if (sc.lp.lev != lev) level_pos(sc.lp, lev, px, py, pz, S, lbx, lby, lbz);
                         const int32_t e = S.ptoff[ci][lev] + sc.lp.local;
                         RO_ASSERT(e >= 0 && e < A.L.E);
-                    const int pv = ld_meta(A.pt + e);
+                        const int pv = ld_meta(A.pt + e);
                         if (pv >= 0) {
                             sample(ci, lev, pv);
-                            break;
+                            continue;
                         }
                         {
                             const unsigned long long key = key_hi | ev++;
@@ -922,7 +1009,6 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                         const int2 sub = substitute(A.pt, S, ci, lev, k, mask, px, py, pz,
                                                     lbx, lby, lbz, sc.lp2);
                         if (sub.x >= 0) sample2(ci, sub.x, sub.y);
-                        break;
                     }
                 }
                 end_depth = d;
@@ -1173,6 +1259,7 @@ int render(ro_ctx *c, const ro_frame *F, const ro_state *st,
     A.sub_max = sub_ok ? st->sub_max : nullptr;
     A.nsb = sub_ok ? (c->layout.brick[0] >> RO_SUB_LOG) * (c->layout.brick[1] >> RO_SUB_LOG) *
                          (c->layout.brick[2] >> RO_SUB_LOG) : 0;
+    A.node_class = nullptr;
     A.local_rows = (int32_t)ro_local_rows(F->height, F->n_parts, F->part, F->tile_rows);
     if (!F->shared_outputs) {  // shared outputs are cleared once by their owner
         RO_CUDA(cudaMemsetAsync(out->required, 0, (size_t)c->E, s));
@@ -1181,6 +1268,15 @@ int render(ro_ctx *c, const ro_frame *F, const ro_state *st,
     }
     if (A.local_rows == 0) return RO_OK;
     RO_CUDA(cudaMemsetAsync(A.tile_counter, 0, sizeof(int32_t), s));
+    if (F->mode == RO_MODE_RESIDENCY && c->node_class != nullptr && st->words != nullptr) {
+        int64_t blocks = (c->num_nodes + 255) / 256;
+        if (blocks > 148 * 8) blocks = 148 * 8;
+        k_classify_nodes<<<(unsigned)blocks, 256, 0, s>>>(*F, st->words, c->layout.m,
+                                                           c->layout.depth, c->num_nodes,
+                                                           c->node_class);
+        RO_CUDA(cudaGetLastError());
+        A.node_class = c->node_class;
+    }
     cudaError_t e;
     if (F->mode == RO_MODE_REFERENCE) {
         e = launch<RO_MODE_REFERENCE, false>(*F, A, s);

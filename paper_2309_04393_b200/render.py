@@ -300,21 +300,26 @@ class DeviceFrame:
         self.image = torch.empty((npix_local, 4), dtype=torch.float32, device=dev)
         self.required = torch.empty(paging.total_entries, dtype=torch.uint8, device=dev)
         self.pix_required = torch.empty(npix_local, dtype=torch.int32, device=dev)
-        # histogram, counters and the four feedback lists share one int64
-        # block so a frame's small results come back in one copy
+        # histogram, counters, the four feedback lists and the feedback counts
+        # share one int64 block so a frame's small results come back in one copy
         nh, nc, nb = n_ch * k, N.RO_NUM_COUNTERS, max(budget, 1)
-        self.small = torch.empty(nh + nc + 4 * nb, dtype=torch.int64, device=dev)
+        self.small = torch.empty(nh + nc + 4 * nb + 4, dtype=torch.int64, device=dev)
         self.hist = self.small[:nh].view(n_ch, k)
         self.counters = self.small[nh:nh + nc]
-        self.fb = self.small[nh + nc:].view(4, nb)
+        self.fb = self.small[nh + nc:nh + nc + 4 * nb].view(4, nb)
+        self.counts_dev = self.small[nh + nc + 4 * nb:]
         self.budget = budget
         self.counts = np.zeros(4, dtype=np.int64)
         self.outputs = N.Outputs(self.image.data_ptr(), self.required.data_ptr(),
                                  self.pix_required.data_ptr(), self.hist.data_ptr(),
                                  self.counters.data_ptr())
+        # synchronous form (host counts) and the asynchronous one (device counts only)
         self.feedback = N.Feedback(self.fb[0].data_ptr(), self.fb[1].data_ptr(),
                                    self.fb[2].data_ptr(), self.fb[3].data_ptr(),
-                                   self.counts.ctypes.data)
+                                   self.counts.ctypes.data, self.counts_dev.data_ptr())
+        self.feedback_async = N.Feedback(self.fb[0].data_ptr(), self.fb[1].data_ptr(),
+                                         self.fb[2].data_ptr(), self.fb[3].data_ptr(),
+                                         None, self.counts_dev.data_ptr())
 
     @property
     def n_bricks(self) -> int:
@@ -379,11 +384,15 @@ class FramePass:
         N.check(N.lib().ro_render(self.paging.ctx, C.byref(self.frame), C.byref(self.state),
                                   C.byref(out), N.stream_ptr()))
 
-    def collect(self):
+    def collect(self, asynchronous: bool = False):
+        """Order + truncate the requests on the device.  Synchronous: the
+        counts are in ``buf.counts`` on return.  Asynchronous: nothing waits;
+        the counts are in ``buf.counts_dev`` (part of ``buf.small``)."""
+        fb = self.buf.feedback_async if asynchronous else self.buf.feedback
         N.check(N.lib().ro_feedback_collect(self.paging.ctx,
                                             self.config.max_requests_per_frame,
                                             1 if self.bricks_first else 0,
-                                            C.byref(self.buf.feedback), N.stream_ptr()))
+                                            C.byref(fb), N.stream_ptr()))
 
 
 def render_frame_device(mode, paging: MultiChannelPaging, octree: ResidencyOctree | None,
@@ -455,20 +464,22 @@ def _run(mode, paging, channels, camera, config, octree=None,
     small = _pinned(buf.small.shape, torch.int64)
     fp.render(N.Outputs(img.data_ptr(), buf.required.data_ptr(), pixr.data_ptr(),
                         buf.hist.data_ptr(), buf.counters.data_ptr()))
-    fp.collect()  # synchronises once on the request counts (the kernel's host stores included)
-    # usage mask (E bytes) and the histogram / counters / ordered requests
-    # block: two copies behind request ordering, one synchronisation
+    fp.collect(asynchronous=True)
+    # usage mask (E bytes) and the histogram / counters / ordered requests /
+    # counts block: two copies behind the request ordering, one
+    # synchronisation for the whole frame (the kernel's host stores included)
     main = torch.cuda.current_stream()
     req.copy_(buf.required, non_blocking=True)
     small.copy_(buf.small, non_blocking=True)
     main.synchronize()
     m = paging.config.m
+    sm = small.numpy()
+    buf.counts[:] = sm[-4:]
     nb, nm = buf.n_bricks, buf.n_metas
     elapsed_ms = (time.perf_counter() - start) * 1000.0
-    sm = small.numpy()
     hist = sm[:nh].reshape(buf.hist.shape).copy()
     counters = sm[nh:nh + N.RO_NUM_COUNTERS]
-    fb = sm[nh + N.RO_NUM_COUNTERS:].reshape(4, -1)
+    fb = sm[nh + N.RO_NUM_COUNTERS:-4].reshape(4, -1)
     bricks = fb[1][:nb].tolist()
     metas = [divmod(v, m) for v in fb[3][:nm].tolist()]
     required = req.numpy()
