@@ -3,16 +3,18 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 One step = one frame of the hot path over a state already resident in HBM:
-ray-cast (kernel 1) + request ordering / bricks-first budget (kernel 3a),
-i.e. what render_frame computes.  `value` is frames/s from CUDA events on
-the launching stream (max over ranks); `e2e` is the same frame through the
-public API render_frame() with the host copies of image / usage mask /
-requests inside the timed region.  With torchrun (N > 1) frames are split
-sort-first over the GPUs and tiles + feedback are exchanged over NCCL.
+node classification + ray cast (kernel 1) + request ordering / bricks-first
+budget (kernel 3a), i.e. what render_frame computes.  The K timed frames
+walk the reference's benchmark orbit (camera.orbit_path(K), as
+bench.run_orbit does, bench.py:98-145 of the reference): no frame repeats.
+`value` is frames/s from CUDA events on the launching stream (max over
+ranks); `e2e` is the same orbit through the public API render_frame() with
+the host copies of image / usage mask / requests inside the timed region.
+With torchrun (N > 1) frames are split sort-first over the GPUs.
 
 --impl reference times the reference algorithm's CPU implementation (the
 C restatement in oracle/, pinned bit-exact to the reference) on all host
-cores over a bounded, strided sample of the same frame's rows.
+cores over a bounded, strided sample of the same orbit frames' rows.
 """
 
 from __future__ import annotations
@@ -32,6 +34,32 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "frames/s & Gsamples/s, 1080p m=4 ch, 1/2/4/8 B200 vs CPU ref; HBM GB/s"
+
+
+def bench_config(scn, world: int, exchange_kind: str = "single") -> dict:
+    """The `config` object of the JSON line -- identical in both arms."""
+    w, h = scn.render.image_dims
+    return {"workload": "config 2: CyCIF-like 4-of-16 ch, 2048x2048x128 u16->u8, 32^3 bricks, "
+                        "1920x1080, partial residency (levels>=2 + 50% of L0/L1), "
+                        "coarser-LOD fallback",
+            "image": [w, h], "channels": len(scn.channels), "octree_depth": scn.depth,
+            "resident_bricks": int(len(scn.brick_ids)),
+            "cache_bytes": int(len(scn.brick_ids)) * 32768,
+            "camera": "orbit_path(steps): radius 2.2, elevation 0.35, fov 45 (reference "
+                      "bench.run_orbit); step i renders pose i",
+            "l2_policy": "inputs larger than L2 (brick cache 1.25 GB > 126 MB); no pose repeats",
+            "parallelism": (f"sort-first x{world}" if world > 1 else "1 GPU")}
+
+
+def host_cores() -> dict:
+    """Threads used by the CPU legs and the physical core count behind them."""
+    logical = os.cpu_count() or 1
+    try:
+        import psutil
+        physical = psutil.cpu_count(logical=False) or logical
+    except Exception:
+        physical = logical
+    return {"threads": logical, "physical": physical}
 
 
 def _peaks():
@@ -139,13 +167,17 @@ class ClockSampler:
 
 
 def _ncu_traffic(world):
-    """dram read+write bytes per ray-cast launch from the committed ncu
-    capture (profiles/ncu_raycast_summary.json), scaled to this part."""
+    """(dram read+write bytes per ray-cast launch, provenance) from the
+    committed ncu --set full capture (profiles/ncu_raycast_summary.json: its
+    commit, camera and kernel time are recorded there), scaled to this part."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_raycast_summary.json")) as f:
-            return json.load(f)["dram_bytes_per_launch"] / world
+            d = json.load(f)
+        src = (f"profiles/ncu_raycast_summary.json: ncu --set full of k_raycast at commit "
+               f"{d.get('commit', '?')}, {d.get('camera', 'orbit_pose(0.6)')}")
+        return d["dram_bytes_per_launch"] / world, src
     except Exception:
-        return None
+        return None, "no ncu summary"
 
 
 def _hang_guard():
@@ -188,10 +220,11 @@ def _sample_rows(h, frac):
     return bands
 
 
-def cpu_frame_rate(ref_state, scn, bands, threads):
-    """Oracle (reference algorithm, C) over the sampled row bands."""
+def cpu_frame_rate(ref_state, scn, bands, threads, cams=None):
+    """Oracle (reference algorithm, C) over the sampled row bands; band i
+    of the list is rendered from camera cams[i % len(cams)] (the orbit)."""
     from oracle import raycast as orc
-    cam = scn.camera
+    cams = cams or [scn.camera]
     och = [orc.OracleChannel(slot=c.slot, points=c.tf.points, level_range=c.level_range)
            for c in scn.channels]
     cfg = scn.render
@@ -199,14 +232,15 @@ def cpu_frame_rate(ref_state, scn, bands, threads):
     rows = sum(b - a for a, b in bands)
     t0 = time.perf_counter()
     images = {}
-    for a, b in bands:
+    for i, (a, b) in enumerate(bands):
+        cam = cams[i % len(cams)]
         out = orc.render(ref_state, och, (cam.position, cam.target, cam.up, cam.fov_deg),
                          cfg.image_dims, cfg.base_step, t0=cfg.lod_reference_distance,
                          early_alpha=cfg.early_term_alpha,
                          budget=cfg.max_requests_per_frame,
                          start_level=cfg.traversal_start_level, rows=(a, b),
                          threads=threads)
-        images[(a, b)] = out.image[a:b]
+        images[(i % len(cams), a, b)] = out.image[a:b]
     dt = time.perf_counter() - t0
     return (rows / h) / dt, dt, rows, images
 
@@ -221,35 +255,40 @@ def run_reference(args):
     dev = "cuda" if torch.cuda.is_available() else "cpu"
     scn = scenarios.cycif(device=dev)
     from oracle.raycast import OracleState
+    from paper_2309_04393_b200.camera import orbit_path
     ref = OracleState(**scenarios.reference_state(scn))
-    threads = os.cpu_count() or 1
+    cores = host_cores()
+    threads = cores["threads"]
     w, h = scn.render.image_dims
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    cams = orbit_path(max(args.steps, 1))
     # size each step so the whole run stays within ~2-3 minutes: calibrate on
     # a small strided sample, then aim at args.cpu_budget_s over all steps
-    cal_fps, cal_dt, cal_rows, _ = cpu_frame_rate(ref, scn, _sample_rows(h, 0.01), threads)
+    cal_fps, cal_dt, cal_rows, _ = cpu_frame_rate(ref, scn, _sample_rows(h, 0.01), threads,
+                                                  cams[:1])
     sec_per_row = cal_dt / max(cal_rows, 1)
     per_step = args.cpu_budget_s / max(args.steps + 0.25 * args.warmup, 1)
     frac = min(1.0, max(4.0 / h, per_step / sec_per_row / h))
-    for _ in range(args.warmup):
-        cpu_frame_rate(ref, scn, _sample_rows(h, frac / 4), threads)
+    for i in range(args.warmup):
+        cpu_frame_rate(ref, scn, _sample_rows(h, frac / 4), threads, [cams[i % len(cams)]])
     rates, secs, rows_total = [], 0.0, 0
-    for _ in range(args.steps):
-        fps, dt, rows, _ = cpu_frame_rate(ref, scn, _sample_rows(h, frac), threads)
+    for i in range(args.steps):  # step i: rows of orbit pose i (the GPU arm's frame i)
+        fps, dt, rows, _ = cpu_frame_rate(ref, scn, _sample_rows(h, frac), threads, [cams[i]])
         rates.append(fps)
         secs += dt
         rows_total += rows
-    fps = float(np.mean(rates))
+    # whole-orbit frames/s: total frames over total time
+    fps = float(args.steps / sum(1.0 / r for r in rates))
     sample = (f"{len(_sample_rows(h, frac))} strided 4-row bands = {rows_total // args.steps} "
-              f"of {h} rows per step, {w}x{h} frame, extrapolated to whole frames")
+              f"of {h} rows of orbit pose i per step i, {w}x{h}, extrapolated to whole frames")
     line = {"impl": "reference", "metric": METRIC, "value": fps, "unit": "frames/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1000.0 * secs / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic CyCIF-like volume (seeded), no network",
-            "config": {"workload": "config 2: CyCIF-like 4-of-16 ch, 2048x2048x128 u16->u8, "
-                                   "32^3 bricks, 1920x1080, partial residency",
-                       "image": [w, h], "channels": 4, "octree_depth": scn.depth},
+            "config": bench_config(scn, world),
             "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": threads,
+                             "physical_cores": cores["physical"],
                              "kind": "port", "sample": sample},
             "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
@@ -305,11 +344,17 @@ def run_ours(args):
                     peer.close()
                     peer = None
                 exchange_kind = "nccl"
-    fp = FramePass(mode, eng.paging, eng.octree, scn.channels, scn.camera, cfg,
-                   partition=(world, rank, 8),
-                   bricks_first=(world == 1 or exchange_kind == "peer"))
+    from paper_2309_04393_b200.camera import orbit_path
+    cams = orbit_path(max(args.steps, 1))
+    # one packed frame per orbit pose (all bound to the same output buffers),
+    # packed before the timed region
+    passes = [FramePass(mode, eng.paging, eng.octree, scn.channels, cam, cfg,
+                        partition=(world, rank, 8),
+                        bricks_first=(world == 1 or exchange_kind == "peer")) for cam in cams]
+    fp = passes[0]
 
-    def step(events=None):
+    def step(events=None, i=0):
+        fp = passes[i % len(passes)]
         if peer is not None:
             return peer.frame(fp, cfg.max_requests_per_frame, m, events)
         if events:
@@ -327,8 +372,8 @@ def run_ours(args):
                             cfg.image_dims, 8, cfg.max_requests_per_frame, m)
         return None
 
-    for _ in range(args.warmup):
-        step()
+    for i in range(args.warmup):
+        step(i=i)
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
@@ -346,7 +391,7 @@ def run_ours(args):
     torch.cuda.profiler.start()
     t_start.record(stream)
     for i in range(args.steps):
-        step(ev[i])
+        step(ev[i], i)
         ev[i][2].record(stream)
     t_end.record(stream)
     torch.cuda.synchronize()
@@ -362,23 +407,32 @@ def run_ours(args):
     ms_per_step = total_ms / args.steps
     fps = 1000.0 / ms_per_step
 
-    # work counters of the full frame (sum over parts)
-    if peer is not None:   # the shared accumulators already hold the full frame
-        counters = peer.bufs["counters"].clone()
-        hist = peer.bufs["hist"].clone()
-    else:
-        counters = fp.buf.counters.clone()
-        hist = fp.buf.hist.clone()
-        if world > 1:
-            torch.distributed.all_reduce(counters)
-            torch.distributed.all_reduce(hist)
-    counters = counters.cpu().numpy()
-    hist = hist.cpu().numpy()
+    # work counters of every timed frame (untimed replay of the orbit; sum
+    # over parts), averaged per frame
+    tot_counters, tot_hist, tot_req = None, None, 0
+    for i in range(args.steps):
+        step(i=i)
+        req_mask = peer.bufs["required"] if peer is not None else passes[i].buf.required
+        tot_req += int(req_mask.to(torch.int64).sum().item())
+        if peer is not None:   # the shared accumulators already hold the full frame
+            counters = peer.bufs["counters"].clone()
+            hist = peer.bufs["hist"].clone()
+        else:
+            counters = passes[i].buf.counters.clone()
+            hist = passes[i].buf.hist.clone()
+            if world > 1:
+                torch.distributed.all_reduce(counters)
+                torch.distributed.all_reduce(hist)
+        c_np, h_np = counters.cpu().numpy(), hist.cpu().numpy()
+        tot_counters = c_np if tot_counters is None else tot_counters + c_np
+        tot_hist = h_np if tot_hist is None else tot_hist + h_np
+    counters = tot_counters / args.steps
+    hist = tot_hist / args.steps
     samples = int(counters[1] + counters[2])
     F = int(hist.sum())
     S = int(counters[0])
     P = w * h
-    alg_bytes = 13 * F + 4 * S + 16 * P          # SURVEY §8(d), u8 bricks
+    alg_bytes = 13 * F + 4 * S + 16 * P          # SURVEY §8(d), u8 bricks, mean frame
     part_bytes = alg_bytes / world
     peak, peak_kind = _peaks()
     achieved = part_bytes / (kern_ms / 1000.0) / 1e9
@@ -391,12 +445,13 @@ def run_ours(args):
         from paper_2309_04393_b200.distributed import exchange as _exchange
         pin_img = torch.empty((h, w, 4), dtype=torch.float32, pin_memory=True)
 
-        def e2e_step():
+        def e2e_step(i):
             if peer is not None:
-                res = step()
+                res = step(i=i)
                 if rank == 0:
                     pin_img.copy_(peer.bufs["image"].reshape(h, w, 4), non_blocking=True)
             else:
+                fp = passes[i % len(passes)]
                 fp.render()
                 fp.collect()
                 b = fp.buf
@@ -408,13 +463,13 @@ def run_ours(args):
                     pin_img.copy_(res["image"], non_blocking=True)
             torch.cuda.synchronize()
             return res
-        for _ in range(2):
-            e2e_step()
+        for i in range(2):
+            e2e_step(i)
         torch.distributed.barrier()
         n_e2e = max(3, args.steps // 2)
         t0 = time.perf_counter()
-        for _ in range(n_e2e):
-            res = e2e_step()
+        for i in range(n_e2e):
+            res = e2e_step(i)
         el = torch.tensor([(time.perf_counter() - t0) / n_e2e], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(el, op=torch.distributed.ReduceOp.MAX)
         e2e_multi = {"value": 1.0 / float(el[0]), "unit": "frames/s",
@@ -449,66 +504,73 @@ def run_ours(args):
         # ---- e2e through the public API (host buffers) ----
         e2e = e2e_multi
         if world == 1 and not args.no_e2e:
-            for _ in range(3):
-                out = render_frame(eng.paging, eng.octree, scn.channels, scn.camera, cfg)
+            for i in range(3):
+                out = render_frame(eng.paging, eng.octree, scn.channels, cams[i % len(cams)],
+                                   cfg)
             n_e2e = max(10, args.steps)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            for _ in range(n_e2e):
-                out = render_frame(eng.paging, eng.octree, scn.channels, scn.camera, cfg)
+            for i in range(n_e2e):   # the same orbit, one pose per call
+                out = render_frame(eng.paging, eng.octree, scn.channels, cams[i % len(cams)],
+                                   cfg)
             e2e_s = (time.perf_counter() - t0) / n_e2e
             d2h = (out.image.nbytes + out.required_mask.nbytes + out.pixel_required.nbytes
                    + 8 * (fp.buf.hist.numel() + N.RO_NUM_COUNTERS + 4 * fp.buf.fb.shape[1]))
             e2e = {"value": 1.0 / e2e_s, "unit": "frames/s",
                    "h2d_bytes_per_step": ctypes.sizeof(N.Frame),
                    "d2h_bytes_per_step": int(d2h),
-                   "note": ("render_frame(): frame params in; image + per-pixel counts stored by "
-                             "the kernel into pinned host memory over PCIe (zero-copy), "
-                             "usage mask / histogram / counters / requests copied after; "
-                             "numpy outputs")}
+                   "note": ("render_frame() over the orbit poses: frame params in; image + "
+                             "per-pixel counts stored by the kernel into pinned host memory "
+                             "over PCIe (zero-copy), usage mask / histogram / counters / "
+                             "requests / counts copied after, one synchronisation; numpy "
+                             "outputs")}
         # ---- CPU baseline (oracle, all cores) + parity of the sampled rows ----
         cpu = None
         parity = None
         if world == 1 and not args.no_cpu_baseline:
             from oracle.raycast import OracleState
             ref = OracleState(**scenarios.reference_state(scn))
-            threads = os.cpu_count() or 1
+            cores = host_cores()
+            threads = cores["threads"]
             bands = _sample_rows(h, args.cpu_fraction)
-            cfps, cdt, rows, images = cpu_frame_rate(ref, scn, bands, threads)
-            img = fp.buf.image.reshape(h, w, 4).cpu().numpy()
-            exact = all(np.array_equal(img[a:b], im) for (a, b), im in images.items())
-            maxdiff = max(float(np.abs(img[a:b] - im).max()) for (a, b), im in images.items())
-            parity = {"rows_checked": rows, "bit_exact": bool(exact), "max_abs_diff": maxdiff}
-            cpu = {"value": cfps, "unit": "frames/s", "cores": threads, "kind": "port",
-                   "sample": f"{len(bands)} strided 4-row bands ({rows}/{h} rows) of the "
-                             f"same frame, {cdt:.1f} s, extrapolated"}
+            n_pose = min(4, len(cams))   # band i comes from orbit pose i % n_pose
+            cfps, cdt, rows, images = cpu_frame_rate(ref, scn, bands, threads, cams[:n_pose])
+            gpu_imgs = []
+            for j in range(n_pose):
+                passes[j].render()
+                passes[j].collect()
+                gpu_imgs.append(passes[j].buf.image.reshape(h, w, 4).cpu().numpy())
+            exact = all(np.array_equal(gpu_imgs[j][a:b], im) for (j, a, b), im in images.items())
+            maxdiff = max(float(np.abs(gpu_imgs[j][a:b] - im).max())
+                          for (j, a, b), im in images.items())
+            parity = {"rows_checked": rows, "poses": n_pose, "bit_exact": bool(exact),
+                      "max_abs_diff": maxdiff}
+            cpu = {"value": cfps, "unit": "frames/s", "cores": threads,
+                   "physical_cores": cores["physical"], "kind": "port",
+                   "sample": f"{len(bands)} strided 4-row bands ({rows}/{h} rows) spread over "
+                             f"orbit poses 0..{n_pose - 1}, {cdt:.1f} s, extrapolated"}
         # compulsory bytes (the reference's FrameStats.required_bytes,
-        # render.py:224): every distinct brick the frame sampled, read once
-        req_bricks = int(fp.buf.required.to(torch.int64).sum().item())
+        # render.py:224): every distinct brick a frame sampled, read once (mean frame)
+        req_bricks = tot_req / args.steps
         compulsory = req_bricks * 32768
         result = {
             "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic CyCIF-like volume (seeded), no network",
-            "config": {"workload": "config 2: CyCIF-like 4-of-16 ch, 2048x2048x128 u16->u8, "
-                                   "32^3 bricks, 1920x1080, partial residency (levels>=2 + "
-                                   "50% of L0/L1), coarser-LOD fallback",
-                       "image": [w, h], "channels": 4, "octree_depth": scn.depth,
-                       "resident_bricks": int(len(scn.brick_ids)),
-                       "cache_bytes": int(len(scn.brick_ids)) * 32768,
-                       "l2_policy": "inputs larger than L2 (brick cache > 126 MB)",
-                       "parallelism": (f"sort-first x{world} ({exchange_kind} exchange)"
-                                       if world > 1 else "1 GPU")},
+            "config": bench_config(scn, world),
+            "exchange": exchange_kind,
             "gsamples_per_s": samples * fps / 1e9,
             # 8 trilinear taps per fetch (SURVEY 8(d) "sampled voxels/s"), whole job
             "sampled_gvoxels_per_s": 8.0 * F / (ms_per_step / 1e3) / 1e9,
-            "frame_work": {"samples": samples, "fetches": F, "traversal_steps": S,
-                           "pixels": P, "livelocked_rays": int(counters[4])},
+            "frame_work": {"per": "mean orbit frame", "samples": samples, "fetches": F,
+                           "traversal_steps": S, "pixels": P,
+                           "livelocked_rays": int(counters[4])},
             "kernel_ms": {"raycast": kern_ms, "feedback": fb_ms},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak,
-                         "unit": "GB/s", "frac": achieved / peak, "traffic": _ncu_traffic(world),
-                         "traffic_source": "profiles/ncu_raycast_summary.json (ncu --set full)",
+                         "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": _ncu_traffic(world)[0],
+                         "traffic_source": _ncu_traffic(world)[1],
                          "peak_kind": peak_kind,
                          "algorithmic_bytes_per_launch": part_bytes,
                          "model": "13*F + 4*S + 16*P bytes (SURVEY 8d), /ray-cast kernel time",

@@ -202,7 +202,7 @@ int ro_destroy(ro_ctx *c) {
     cudaFree(c->touched_n);
     cudaFree(c->claim);
     cudaFree(c->node_class);
-    for (int i = 0; i < 12; ++i) cudaFree(c->scratch[i]);
+    for (int i = 0; i < 16; ++i) cudaFree(c->scratch[i]);
     if (c->pinned_small) cudaFreeHost(c->pinned_small);
     if (c->staging) cudaFreeHost(c->staging);
     if (c->upload) cudaStreamDestroy(c->upload);

@@ -23,9 +23,8 @@
 // and sorted the same way.  Nothing synchronises the host: the counts land
 // in device memory (and, for the synchronous API, in host memory after one
 // final copy).
-#include <cooperative_groups.h>
-
 #include "internal.cuh"
+#include "topk.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -34,13 +33,13 @@ namespace ro {
 namespace {
 
 constexpr int kFbThreads = 1024;
-constexpr int kChunk = 8192;  // pairs sorted per CTA in shared memory (96 KB)
-constexpr size_t kFbSmem = (size_t)kChunk * (sizeof(unsigned long long) + sizeof(int32_t));
+constexpr int kChunk = topk::kChunk;  // pairs sorted per CTA in shared memory (96 KB)
+constexpr size_t kFbSmem = topk::kSortSmem;
 
 // ctl block (u32, zeroed before the launch):
 //   [0] touched bricks  [1] touched metas  [2] max pixel  [3] max event
 //   [8 ..)          gather counters, one per chunk
-//   [kHistOff ..)   3 x 256 digit histograms (a ring, see select())
+//   [kHistOff ..)   3 x 256 digit histograms (a ring, see topk::select_kth)
 constexpr int kMaxChunks = 1024;
 constexpr int kHistOff = 8 + kMaxChunks;
 constexpr int kCtlWords = kHistOff + 3 * 256;
@@ -61,6 +60,8 @@ struct FbArgs {
 };
 
 __device__ __forceinline__ int bit_len(unsigned v) { return v ? 32 - __clz(v) : 0; }
+
+// with ev < 2^ev_bits: order-preserving, injective repack of (pixel << 32 | event)
 
 // phase A: one list's key array -> compacted candidates
 __device__ void compact(unsigned long long *__restrict__ keys, int64_t n,
@@ -111,107 +112,17 @@ __device__ __forceinline__ unsigned long long unpack(unsigned long long q, int e
     return ((q >> ev_bits) << 32) | (q & ((1ull << ev_bits) - 1ull));
 }
 
-// Exact `need`-th smallest packed key among the candidates with q > lo (lo
-// ignored when !has_lo).  Histogram ring H[g % 3]: step g accumulates into
-// H[g%3] before the grid sync; after it, every CTA reads H[g%3] and CTA 0
-// clears H[(g+2)%3] (read by nobody after the previous sync).
-__device__ unsigned long long select(cg::grid_group &grid, const unsigned long long *cand,
-                                     int64_t n, int ev_bits, bool has_lo,
-                                     unsigned long long lo, int64_t need, int top_shift,
-                                     uint32_t *ctl, uint32_t &g, uint32_t *s_hist) {
-    unsigned long long prefix = 0;
-    for (int shift = top_shift; shift >= 0; shift -= 8) {
-        uint32_t *H = ctl + kHistOff + 256 * (g % 3);
-        for (int i = threadIdx.x; i < 256; i += blockDim.x) s_hist[i] = 0;
-        __syncthreads();
-        const int hs = shift + 8;
-        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-             i += (int64_t)gridDim.x * blockDim.x) {
-            const unsigned long long q = pack(__ldcg(cand + i), ev_bits);
-            if (has_lo && q <= lo) continue;
-            if (hs < 64 && (q >> hs) != (prefix >> hs)) continue;
-            atomicAdd(&s_hist[(q >> shift) & 255], 1u);
-        }
-        __syncthreads();
-        for (int i = threadIdx.x; i < 256; i += blockDim.x)
-            if (s_hist[i]) atomicAdd(&H[i], s_hist[i]);
-        grid.sync();
-        // every CTA finds the digit where the running count reaches `need`
-        __shared__ uint32_t s_sel[2];
-        if (threadIdx.x < 32) {
-            uint32_t c[8];
-            uint32_t run = 0;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                c[j] = __ldcg(&H[threadIdx.x * 8 + j]);
-                run += c[j];
-            }
-            uint32_t incl = run;
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-                if ((int)threadIdx.x >= o) incl += y;
-            }
-            uint32_t before = incl - run;  // candidates in lower digit groups
-            if ((int64_t)before < need && need <= (int64_t)incl) {
-                for (int j = 0; j < 8; ++j) {
-                    if (need <= (int64_t)(before + c[j])) {
-                        s_sel[0] = threadIdx.x * 8 + j;
-                        s_sel[1] = before;
-                        break;
-                    }
-                    before += c[j];
-                }
-            }
-        }
-        if (blockIdx.x == 0) {
-            uint32_t *Hz = ctl + kHistOff + 256 * ((g + 2) % 3);
-            for (int i = threadIdx.x; i < 256; i += blockDim.x) Hz[i] = 0;
-        }
-        __syncthreads();
-        prefix |= (unsigned long long)s_sel[0] << shift;
-        need -= s_sel[1];
-        ++g;
-        __syncthreads();
-    }
-    return prefix;
-}
-
-// one CTA: sort the gathered [base, base+w) (q in okeys, entry in oids) and
-// write the unpacked keys / decoded ids back
+// one CTA: sort the gathered [0, w) (q in okeys, entry in oids) and write
+// the unpacked keys / decoded ids back
 __device__ void sort_emit(const DevLayout &L, bool bricks, int64_t *okeys, int64_t *oids,
                           int64_t w, int ev_bits, unsigned char *smem) {
     auto *sk = reinterpret_cast<unsigned long long *>(smem);
     auto *sv = reinterpret_cast<int32_t *>(sk + kChunk);
-    int np = 1;
-    while (np < w) np <<= 1;
-    for (int i = threadIdx.x; i < np; i += blockDim.x) {
-        if (i < w) {
-            sk[i] = (unsigned long long)__ldcg(okeys + i);
-            sv[i] = (int32_t)__ldcg(oids + i);
-        } else {
-            sk[i] = ~0ull;
-            sv[i] = -1;
-        }
+    for (int i = threadIdx.x; i < w; i += blockDim.x) {
+        sk[i] = (unsigned long long)__ldcg(okeys + i);
+        sv[i] = (int32_t)__ldcg(oids + i);
     }
-    __syncthreads();
-    for (int size = 2; size <= np; size <<= 1) {
-        for (int stride = size >> 1; stride > 0; stride >>= 1) {
-            for (int i = threadIdx.x; i < np / 2; i += blockDim.x) {
-                const int lo = 2 * i - (i & (stride - 1));
-                const int hi = lo + stride;
-                const bool up = (lo & size) == 0;
-                const unsigned long long a = sk[lo], b = sk[hi];
-                if ((a > b) == up) {
-                    sk[lo] = b;
-                    sk[hi] = a;
-                    const int32_t t = sv[lo];
-                    sv[lo] = sv[hi];
-                    sv[hi] = t;
-                }
-            }
-            __syncthreads();
-        }
-    }
+    topk::sort_pairs(sk, sv, (int)w);
     for (int i = threadIdx.x; i < w; i += blockDim.x) {
         okeys[i] = (int64_t)unpack(sk[i], ev_bits);
         oids[i] = bricks ? entry_to_id(L, sv[i]) : (int64_t)sv[i];
@@ -268,8 +179,14 @@ __global__ void __launch_bounds__(kFbThreads, 1) k_feedback(const __grid_constan
             const int64_t w = keep - done < kChunk ? keep - done : kChunk;
             // threshold: the w-th smallest above lo, or everything left
             unsigned long long hi = ~0ull;
-            if (done + w < n)
-                hi = select(grid, cand, n, ev_bits, has_lo, lo, w, top_shift, ctl, g, s_hist);
+            if (done + w < n) {
+                auto key_of = [&](int64_t i, unsigned long long &q) {
+                    q = pack(__ldcg(cand + i), ev_bits);
+                    return true;
+                };
+                hi = topk::select_kth(grid, n, key_of, has_lo, lo, w, top_shift,
+                                      ctl + kHistOff, g, s_hist);
+            }
             uint32_t *cnt = &ctl[8 + (chunk % kMaxChunks)];
             for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
                  i += (int64_t)gridDim.x * blockDim.x) {

@@ -178,8 +178,11 @@ struct ro_ctx {
     int64_t *pinned_small = nullptr;          // host pinned scratch [64]
 
     // generic grow-only device scratch
-    void *scratch[12] = {nullptr};
-    size_t scratch_bytes[12] = {0};
+    // 0-7 feedback / octree / ingest / metadata passes, 11 feedback control,
+    // 12 brick-payload upload (its own: a DMA may still be running into it),
+    // 13 LRU control, 14 swap counts
+    void *scratch[16] = {nullptr};
+    size_t scratch_bytes[16] = {0};
     // pinned host staging for payload uploads
     void *staging = nullptr;
     size_t staging_bytes = 0;

@@ -75,6 +75,18 @@
 #ifndef RO_FAST_DESCENT
 #define RO_FAST_DESCENT 1
 #endif
+#ifndef RO_PREFETCH
+#define RO_PREFETCH 0
+#endif
+// brick-run histogram (1) or a histogram increment per fetch (0)
+#ifndef RO_RUNLEN
+#define RO_RUNLEN 0
+#endif
+// per-channel (slot, lo, hi, zero_upto) as one shared-memory int4 (1) or
+// from the kernel-parameter bank (0)
+#ifndef RO_CHI
+#define RO_CHI 0
+#endif
 
 namespace ro {
 
@@ -116,6 +128,7 @@ struct FrameSmem {
     int32_t slot[RO_MAX_CH], lo[RO_MAX_CH], hi[RO_MAX_CH], np[RO_MAX_CH];
     // largest integer value v with opacity(u) == 0 for every u <= v
     int32_t zero_upto[RO_MAX_CH];
+    int4 chi[RO_MAX_CH];  // (slot, lo, hi, zero_upto): one LDS.128 per channel visit
     unsigned long long red[RO_NUM_COUNTERS];
     // frame constants kept out of registers
     double bm1[3];      // brick extent - 1, as fp64 (the reference's B - 1.0)
@@ -250,9 +263,17 @@ __device__ __forceinline__ void request(unsigned long long *keys, int32_t *, int
 
 // Brick coordinates of one level at the current sample position:
 // P = fl(p * dim) (kernels.py:179 numerator), c = int(P / b) = int(P) >> lb.
+#ifndef RO_LP2_LOCAL
+#define RO_LP2_LOCAL 0
+#endif
+#ifndef RO_LP_NOP
+#define RO_LP_NOP 0  // 1: taps recompute P = p * dim (3 DMUL, rare) instead of keeping it live
+#endif
 struct LevelPos {
     int lev;
+#if !RO_LP_NOP
     double P[3];
+#endif
     int cb[3];
     int local;  // (cz*gy + cy)*gx + cx
     int sub;    // 4^3 sub-block of int(P) inside the brick (ro_state.sub_max index)
@@ -267,8 +288,11 @@ __device__ __forceinline__ void level_pos(LevelPos &lp, int lev, double px, doub
     int sb[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-        lp.P[a] = p3[a] * S.dimd[lev][a];
-        const int ip = (int)lp.P[a];
+        const double P = p3[a] * S.dimd[lev][a];
+#if !RO_LP_NOP
+        lp.P[a] = P;
+#endif
+        const int ip = (int)P;
         int c = ip >> lb3[a];
         const int g = S.grids[lev][a];
         lp.cb[a] = c > g - 1 ? g - 1 : c;
@@ -309,7 +333,8 @@ __device__ __forceinline__ uint4 ld_meta4(const uint4 *p) {
 // the chosen level is left in `lp2` (a one-entry cache across channels).
 __device__ __forceinline__ int2 substitute(const int32_t *__restrict__ pt, const FrameSmem &S, int ci,
                                 int lev, int k, uint32_t mask, double px, double py,
-                                double pz, int lbx, int lby, int lbz, LevelPos &lp2) {
+                                double pz, int lbx, int lby, int lbz, LevelPos &lp2,
+                                int32_t &e_out) {
     // Visit the levels present in the mask in the reference's order
     // (distance 1, 2, ...; the coarser one first on a tie) by taking the
     // nearest remaining set bit on either side, instead of scanning every
@@ -323,8 +348,12 @@ __device__ __forceinline__ int2 substitute(const int32_t *__restrict__ pt, const
         const int cand = da <= db ? lev + da : lev - db;
         if (lp2.lev != cand) level_pos(lp2, cand, px, py, pz, S, lbx, lby, lbz);
         RO_ASSERT(cand >= 0 && cand < RO_MAX_LEVELS && lp2.local >= 0);
-        const int pv2 = ld_meta(pt + S.ptoff[ci][cand] + lp2.local);
-        if (pv2 >= 0) return make_int2(cand, pv2);
+        const int32_t e2 = S.ptoff[ci][cand] + lp2.local;
+        const int pv2 = ld_meta(pt + e2);
+        if (pv2 >= 0) {
+            e_out = e2;
+            return make_int2(cand, pv2);
+        }
         mk &= ~(1u << cand);
     }
     return make_int2(-1, -1);
@@ -341,15 +370,21 @@ struct Taps {
 // weight is 0 and lerp(a, b, 0) = a + (b - a) * 0 = a for any finite b.  The
 // read may touch the next row / slice / brick -- the cache carries one brick
 // of tail padding (resoct.h) -- but never changes a result.
-__device__ __forceinline__ void taps_of(Taps &tp, const LevelPos &lp, int bx, int by,
-                                        int bz, const FrameSmem &S) {
+__device__ __forceinline__ void taps_of(Taps &tp, const LevelPos &lp, double px, double py,
+                                        double pz, int bx, int by, int bz, const FrameSmem &S) {
     const int B[3] = {bx, by, bz};
+    const double p3[3] = {px, py, pz};
     int i0[3];
     double tw[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
         // lx = P - c*B exactly; fx = lx - 0.5 exactly; clamped to [0, B-1]
-        double f = (lp.P[a] - i2d(lp.cb[a] * B[a])) - 0.5;
+#if RO_LP_NOP
+        const double P = p3[a] * S.dimd[lp.lev][a];  // the same rounding as level_pos
+#else
+        const double P = lp.P[a];
+#endif
+        double f = (P - i2d(lp.cb[a] * B[a])) - 0.5;
         if (f < 0.0) f = 0.0;
         if (f > S.bm1[a]) f = S.bm1[a];
         const int c0 = (int)f;
@@ -415,7 +450,7 @@ __device__ double ref_value(const ro_frame &F, const FrameSmem &S, int ci, int l
     const int rp = F.ref_pt[S.ptoff[ci][lev] + lp.local];
     if (rp < 0) return -1.0;
     Taps tp;
-    taps_of(tp, lp, bx, by, bz, S);
+    taps_of(tp, lp, qx, qy, qz, bx, by, bz, S);
     int v[8];
     load_taps<0, 0>(v, F.ref_cache + (int64_t)rp * bvox + tp.o, bx, bx * by);
     return trilerp(v, tp);
@@ -532,6 +567,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
         S.np[tid] = F.ch[tid].npoints;
         // leading zero-opacity range of the TF (ro_pack_frame)
         S.zero_upto[tid] = F.ch[tid].zero_upto;
+        S.chi[tid] = make_int4(F.ch[tid].slot, F.ch[tid].lo, F.ch[tid].hi, F.ch[tid].zero_upto);
     }
     if (tid < RO_NUM_COUNTERS) S.red[tid] = 0;
     if (tid == 0) {
@@ -545,8 +581,11 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
     }
     // per-thread arrays: [ci*kBlock + tid]
     const int kChStride = n_ch * kBlock;
-    int32_t *prev_brick = dyn;                        // n_ch
-    int32_t *last_breq = prev_brick + kChStride;      // n_ch
+    // per channel: the current brick run (kernels.py:672-676 prev_brick) as
+    // entry | level << 32 | fetch count << 36; the histogram is credited
+    // when the run ends, not per fetch
+    unsigned long long *run = reinterpret_cast<unsigned long long *>(dyn);  // n_ch
+    int32_t *last_breq = reinterpret_cast<int32_t *>(run + kChStride);    // n_ch
     int32_t *last_mreq = last_breq + kChStride;       // n_ch
     uint32_t *hist_t = reinterpret_cast<uint32_t *>(last_mreq + kChStride);
     for (int i = 0; i < n_ch * k; ++i) hist_t[i * kBlock + tid] = 0;
@@ -574,7 +613,11 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
 #endif
     for (int wsub = warp; wsub < kPPT; wsub += kWarps) {
     for (int i = 0; i < n_ch; ++i) {
-        prev_brick[i * kBlock + tid] = -1;
+#if RO_RUNLEN
+        run[i * kBlock + tid] = 0xFFFFFFFFull;
+#else
+        reinterpret_cast<int32_t *>(run)[i * kBlock + tid] = -1;
+#endif
         last_breq[i * kBlock + tid] = -1;
         last_mreq[i * kBlock + tid] = -1;
     }
@@ -661,9 +704,9 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
 
             // usage mask / histogram / per-pixel brick switches of a sampled
             // channel (kernels.py:670-676)
-            auto account = [&](int ci, int lev, const LevelPos &lp) {
-                const int32_t e = S.ptoff[ci][lev] + lp.local;
-                int32_t &pb = prev_brick[ci * kBlock + tid];
+            auto account = [&](int ci, int lev, int32_t e) {
+#if !RO_RUNLEN
+                int32_t &pb = reinterpret_cast<int32_t *>(run)[ci * kBlock + tid];
                 if (e != pb) {
                     pb = e;
                     pixreq += 1;
@@ -672,6 +715,21 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                 }
                 RO_ASSERT(lev >= 0 && lev < k && ci < n_ch);
                 hist_t[(ci * k + lev) * kBlock + tid] += 1;
+                return;
+#endif
+                unsigned long long &r = run[ci * kBlock + tid];
+                const unsigned long long rv = r;
+                if ((uint32_t)rv == (uint32_t)e) {  // same brick: one more fetch
+                    r = rv + (1ull << 36);
+                    return;
+                }
+                const uint32_t cnt = (uint32_t)(rv >> 36);
+                if (cnt) hist_t[(ci * k + (int)((rv >> 32) & 15)) * kBlock + tid] += cnt;
+                RO_ASSERT(lev >= 0 && lev < k && ci < n_ch);
+                r = (uint32_t)e | ((unsigned long long)lev << 32) | (1ull << 36);
+                pixreq += 1;
+                RO_ASSERT(e >= 0 && e < A.L.E);
+                A.required[e] = 1;
             };
             // Sub-block skip: the taps with non-zero weight lie within one
             // voxel of int(local coordinate), i.e. inside the dilated 8^3
@@ -709,26 +767,33 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                 sB += b * a;
                 trans *= (1.0 - a);
             };
-            // sample at the desired level (sc.lp already holds it)
-            auto sample = [&](int ci, int lev, int slot_lin) {
-                account(ci, lev, sc.lp);
-                if (sub_skip(ci, slot_lin, sc.lp)) return;
-                if (sc.tp_lev != lev) { taps_of(sc.tp, sc.lp, bx, by, bz, S); sc.tp_lev = lev; }
+            // taps + TF of the desired level (sc.lp holds it)
+            auto sample_taps = [&](int ci, int lev, int slot_lin) {
+                if (sc.tp_lev != lev) {
+                    taps_of(sc.tp, sc.lp, px, py, pz, bx, by, bz, S);
+                    sc.tp_lev = lev;
+                }
                 finish(ci, slot_lin, sc.tp);
             };
-            // sample at a substitute level (sc.lp2 holds it)
-            auto sample2 = [&](int ci, int lev, int slot_lin) {
-                account(ci, lev, sc.lp2);
-                if (sub_skip(ci, slot_lin, sc.lp2)) return;
+            // sample at the desired level (sc.lp already holds it; e = its entry)
+            auto sample = [&](int ci, int lev, int slot_lin, int32_t e) {
+                account(ci, lev, e);
+                if (sub_skip(ci, slot_lin, sc.lp)) return;
+                sample_taps(ci, lev, slot_lin);
+            };
+            // sample at a substitute level (lp2 holds it)
+            auto sample2 = [&](int ci, int lev, int slot_lin, int32_t e, const LevelPos &lp2) {
+                account(ci, lev, e);
+                if (sub_skip(ci, slot_lin, lp2)) return;
                 Taps t2;
-                taps_of(t2, sc.lp2, bx, by, bz, S);
+                taps_of(t2, lp2, px, py, pz, bx, by, bz, S);
                 finish(ci, slot_lin, t2);
             };
 
             // sample channel ci from `slot_lin` at level `lev` (any level)
             auto sample_at = [&](int ci, int lev, int slot_lin) {
                 if (sc.lp.lev != lev) level_pos(sc.lp, lev, px, py, pz, S, lbx, lby, lbz);
-                sample(ci, lev, slot_lin);
+                sample(ci, lev, slot_lin, S.ptoff[ci][lev] + sc.lp.local);
             };
 
             if (MODE == RO_MODE_PAGETABLE) {  // kernels.py:316-357
@@ -745,7 +810,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                     const int pv = ld_meta(A.pt + e);
                     if (pv >= 0) {
                         all_empty = false;
-                        sample(ci, lev, pv);
+                        sample(ci, lev, pv, e);
                     } else if (pv == RO_PT_EMPTY) {
                         zero_mask |= 1u << ci;
                         // c*B / float(dim): integer numerator, one IEEE division
@@ -832,8 +897,9 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                 for (int ci = 0; ci < n_ch; ++ci) {
                     const int lev = clampi(raw, CH_LO(ci), CH_HI(ci));
                     if (sc.lp.lev != lev) level_pos(sc.lp, lev, px, py, pz, S, lbx, lby, lbz);
-                    const int pv = __ldg(A.pt + S.ptoff[ci][lev] + sc.lp.local);
-                    if (pv >= 0) sample(ci, lev, pv);
+                    const int32_t e = S.ptoff[ci][lev] + sc.lp.local;
+                    const int pv = __ldg(A.pt + e);
+                    if (pv >= 0) sample(ci, lev, pv, e);
                 }
             } else {
                 // kernels.py:431-558 -- one cursor shared by all channels
@@ -909,9 +975,51 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                     d = d0 + stop;
                 }
 #endif
+                // Fast path, channels 0..3 at channel 0's level: issue their
+                // page-table probes, then the sub-block maxima of the hits, as
+                // independent loads ahead of the in-order channel loop (pure
+                // reads of frame-constant state; every side effect stays in
+                // the loop, in the reference's order)
+                uint32_t pf_done = 0, pf_hit = 0, pf_skip = 0;
+#if RO_PREFETCH
+                if (fast) {
+                    const int4 c0 = S.chi[0];
+                    const int lev0 = clampi(raw, c0.y, c0.z);
+                    level_pos(sc.lp, lev0, px, py, pz, S, lbx, lby, lbz);
+                    int pv[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        pv[j] = -1;
+                        if (j < n_ch) {
+                            const int4 cj = S.chi[j];
+                            if (clampi(raw, cj.y, cj.z) == lev0) {
+                                pf_done |= 1u << j;
+                                pv[j] = ld_meta(A.pt + S.ptoff[j][lev0] + sc.lp.local);
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        if (pv[j] >= 0) {
+                            pf_hit |= 1u << j;
+#if RO_SUBMAX
+                            if (A.sub_max != nullptr &&
+                                (int)__ldg(A.sub_max + (int64_t)pv[j] * A.nsb + sc.lp.sub) <=
+                                    S.chi[j].w)
+                                pf_skip |= 1u << j;
+#endif
+                        }
+                    }
+                }
+#endif
 #pragma unroll 1
                 for (int ci = 0; ci < n_ch; ++ci) {
-                    const int slot = CH_SLOT(ci);
+#if RO_CHI
+                    const int4 chc = S.chi[ci];
+#else
+                    const int4 chc = make_int4(CH_SLOT(ci), CH_LO(ci), CH_HI(ci), 0);
+#endif
+                    const int slot = chc.x;
                     uint32_t mask;
                     if (fast) {
                         mask = (vec4 ? (slot == 0 ? wv.x : slot == 1 ? wv.y : slot == 2 ? wv.z : wv.w)
@@ -988,14 +1096,22 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                     // at traversal depth: probe the desired brick
                     {
                         all_cz = false;
-                        const int lev = clampi(raw, CH_LO(ci), CH_HI(ci));
+                        const int lev = clampi(raw, chc.y, chc.z);
                         if (sc.lp.lev != lev) level_pos(sc.lp, lev, px, py, pz, S, lbx, lby, lbz);
                         const int32_t e = S.ptoff[ci][lev] + sc.lp.local;
                         RO_ASSERT(e >= 0 && e < A.L.E);
-                        const int pv = ld_meta(A.pt + e);
-                        if (pv >= 0) {
-                            sample(ci, lev, pv);
-                            continue;
+                        if ((pf_done >> ci) & 1u) {  // probed ahead
+                            if ((pf_hit >> ci) & 1u) {
+                                account(ci, lev, e);
+                                if (!((pf_skip >> ci) & 1u)) sample_taps(ci, lev, ld_meta(A.pt + e));
+                                continue;
+                            }
+                        } else {
+                            const int pv = ld_meta(A.pt + e);
+                            if (pv >= 0) {
+                                sample(ci, lev, pv, e);
+                                continue;
+                            }
                         }
                         {
                             const unsigned long long key = key_hi | ev++;
@@ -1006,9 +1122,16 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                             }
                         }
                         // nearest resident level in this node, coarser first
+                        int32_t e2 = -1;
+#if RO_LP2_LOCAL
+                        LevelPos lp2;  // (not cached across channels: fewer live registers)
+                        lp2.lev = -1;
+#else
+                        LevelPos &lp2 = sc.lp2;
+#endif
                         const int2 sub = substitute(A.pt, S, ci, lev, k, mask, px, py, pz,
-                                                    lbx, lby, lbz, sc.lp2);
-                        if (sub.x >= 0) sample2(ci, sub.x, sub.y);
+                                                    lbx, lby, lbz, lp2, e2);
+                        if (sub.x >= 0) sample2(ci, sub.x, sub.y, e2, lp2);
                     }
                 }
                 end_depth = d;
@@ -1107,6 +1230,12 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
             if (CHECK && F.max_samples > 0 && ++n_probe >= F.max_samples) alive = false;
         }
     }
+    // close every channel's last brick run
+    for (int ci = 0; ci < n_ch && RO_RUNLEN; ++ci) {
+        const unsigned long long rv = run[ci * kBlock + tid];
+        const uint32_t cnt = (uint32_t)(rv >> 36);
+        if (cnt) hist_t[(ci * k + (int)((rv >> 32) & 15)) * kBlock + tid] += cnt;
+    }
     if (active) {
         const float4 px4 = make_float4(__double2float_rn(accR), __double2float_rn(accG),
                                        __double2float_rn(accB), __double2float_rn(accA));
@@ -1144,7 +1273,7 @@ cudaError_t launch_b(const ro_frame &F, const RayArgs &A, cudaStream_t s) {
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev);
     }
-    size_t dyn = (size_t)F.n_ch * kBlock * 4 * 3 + (size_t)F.n_ch * A.L.k * kBlock * 4;
+    size_t dyn = (size_t)F.n_ch * kBlock * (8 + 4 * 2) + (size_t)F.n_ch * A.L.k * kBlock * 4;
 #ifdef RO_EXTRA_SMEM
     dyn += RO_EXTRA_SMEM;  // experiment knob: shared-memory / L1 split sensitivity
 #endif

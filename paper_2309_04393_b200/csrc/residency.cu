@@ -19,15 +19,16 @@
 // every leaf overlapped by a changed brick is recomputed for that brick's
 // (slot, level) from the final page table, then ancestors are re-ORed level
 // by level.  Metadata bits (16..31) are never touched here.
-#include <cub/cub.cuh>
-
 #include <cstring>
 #include <unordered_map>
 #include <vector>
 
 #include "internal.cuh"
+#include "topk.cuh"
 
 namespace ro {
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -47,93 +48,6 @@ __global__ void k_check_batch(const DevLayout L, const int64_t *__restrict__ ids
     entries[i] = e;
     if (pt[e] >= 0) atomicOr(flag, 1);
     if (atomicExch(claim + e, epoch) == epoch) atomicOr(flag, 1);
-}
-
-// phase (i): pop the free list top-first
-__global__ void k_assign_free(int32_t n1, const int32_t *__restrict__ free_stack,
-                              int32_t free_count, int32_t *__restrict__ slots,
-                              int64_t *__restrict__ evicted) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n1) return;
-    slots[i] = free_stack[free_count - 1 - i];
-    evicted[i] = -1;
-}
-
-// stale keys: (last_used << 32 | slot) for occupied slots with last_used < frame
-__global__ void k_stale_keys(const int64_t *__restrict__ slot_brick,
-                             const int64_t *__restrict__ last_used, int64_t S,
-                             int64_t frame, unsigned long long *__restrict__ keys,
-                             int32_t *__restrict__ count) {
-    int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < S; s += stride) {
-        if (slot_brick[s] >= 0 && last_used[s] < frame) {
-            int pos = atomicAdd(count, 1);
-            keys[pos] = ((unsigned long long)last_used[s] << 32) | (unsigned long long)s;
-        }
-    }
-}
-
-// phases (ii) and (iii)
-__global__ void k_assign_victims(int32_t n1, int32_t n, int32_t n2,
-                                 const unsigned long long *__restrict__ sorted,
-                                 const int64_t *__restrict__ slot_brick,
-                                 const int64_t *__restrict__ ids,
-                                 int32_t *__restrict__ slots,
-                                 int64_t *__restrict__ evicted) {
-    int i = n1 + blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    int j = i - n1;
-    if (j < n2) {
-        int32_t s = (int32_t)(sorted[j] & 0xFFFFFFFFull);
-        slots[i] = s;
-        evicted[i] = slot_brick[s];
-    } else {
-        slots[i] = 0;
-        // first phase-(iii) insert: fixed up by k_phase3_first
-        evicted[i] = (i == n1 + n2) ? -2 : ids[i - 1];
-    }
-}
-
-// occupant of slot 0 when phase (iii) starts
-__global__ void k_phase3_first(int32_t p3, const int32_t *__restrict__ slots,
-                               const int64_t *__restrict__ ids,
-                               const int64_t *__restrict__ slot_brick,
-                               int64_t *__restrict__ evicted) {
-    int64_t occ = slot_brick[0];
-    for (int i = p3 - 1; i >= 0; --i) {
-        if (slots[i] == 0) { occ = ids[i]; break; }
-    }
-    evicted[p3] = occ;
-}
-
-// map batch bricks; final occupants own their slot
-__global__ void k_map_batch(const DevLayout L, int32_t n, int32_t p3,
-                            const int64_t *__restrict__ ids,
-                            const int64_t *__restrict__ entries,
-                            const int32_t *__restrict__ slots,
-                            int32_t *__restrict__ pt,
-                            int64_t *__restrict__ slot_brick,
-                            int64_t *__restrict__ last_used, int64_t frame,
-                            uint8_t *__restrict__ final_flag) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    int32_t s = slots[i];
-    pt[entries[i]] = s;
-    bool final_occ = (p3 >= n) ? true : (s == 0 ? i == n - 1 : true);
-    final_flag[i] = final_occ ? 1 : 0;
-    if (final_occ) slot_brick[s] = ids[i];
-    last_used[s] = frame;
-}
-
-__global__ void k_unmap_evicted(const DevLayout L, int32_t n,
-                                const int64_t *__restrict__ evicted,
-                                int32_t *__restrict__ pt) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    int64_t v = evicted[i];
-    if (v < 0) return;
-    Decoded d = decode_id(L, v);
-    pt[entry_index(L, d.slot, d.lev, d.x, d.y, d.z)] = RO_PT_UNMAPPED;
 }
 
 // copy payloads of final occupants into their cache slots (16-byte lanes)
@@ -198,7 +112,7 @@ __global__ void k_copy_payloads_bytes(int32_t n, int64_t bvox,
 }
 
 // literal sequential insert_brick loop (one thread) for irregular batches
-__global__ void k_sequential_insert(const DevLayout L, int32_t n,
+__device__ void sequential_insert(const DevLayout L, int32_t n,
                                     const int64_t *__restrict__ ids,
                                     int32_t *__restrict__ pt,
                                     int64_t *__restrict__ slot_brick,
@@ -285,114 +199,6 @@ __global__ void k_release(const DevLayout L, int32_t n, const int64_t *__restric
     }
 }
 
-// ---- octree: per changed brick, node boxes at every depth ----
-struct BrickBoxes {
-    int slot, lev;
-    int lo[3], hi[3];  // leaf box at depth D
-    bool empty;
-};
-
-__global__ void k_brick_counts(const DevLayout L, int32_t n,
-                               const int64_t *__restrict__ ids,
-                               int64_t *__restrict__ counts /* [(D+1)*n] */) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    int64_t id = ids[i];
-    Box3 b;
-    b.empty = true;
-    if (id >= 0) {
-        Decoded d = decode_id(L, id);
-        if (d.ok) b = leaf_box(L, d.lev, d.x, d.y, d.z);
-    }
-    for (int dd = 0; dd <= L.depth; ++dd) {
-        int64_t c = 0;
-        if (!b.empty) {
-            int sh = L.depth - dd;
-            c = 1;
-            for (int a = 0; a < 3; ++a) c *= (int64_t)((b.hi[a] >> sh) - (b.lo[a] >> sh) + 1);
-        }
-        counts[(int64_t)dd * n + i] = c;
-    }
-}
-
-__device__ __forceinline__ int find_seg(const int64_t *__restrict__ off, int n, int64_t j) {
-    int lo = 0, hi = n - 1;
-    while (lo < hi) {
-        int mid = (lo + hi + 1) >> 1;
-        if (off[mid] <= j) lo = mid; else hi = mid - 1;
-    }
-    return lo;
-}
-
-// depth D: recompute the (slot, level) bit of each overlapped leaf
-__global__ void k_update_leaves(const DevLayout L, int32_t n,
-                                const int64_t *__restrict__ ids,
-                                const int64_t *__restrict__ off /* level D seg */,
-                                const int64_t *__restrict__ total_p,
-                                const int32_t *__restrict__ pt,
-                                uint32_t *__restrict__ words) {
-    const int64_t total = *total_p;
-    const int D = L.depth;
-    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < total;
-         j += (int64_t)gridDim.x * blockDim.x) {
-        int i = find_seg(off, n, j);
-        Decoded d = decode_id(L, ids[i]);
-        Box3 b = leaf_box(L, d.lev, d.x, d.y, d.z);
-        int64_t r = j - off[i];
-        int w = b.hi[0] - b.lo[0] + 1, h = b.hi[1] - b.lo[1] + 1;
-        int lx = b.lo[0] + (int)(r % w);
-        int lyy = b.lo[1] + (int)((r / w) % h);
-        int lz = b.lo[2] + (int)(r / ((int64_t)w * h));
-        Box3 bb = brick_box(L, D, lx, lyy, lz, d.lev);
-        bool backed = false;
-        if (!bb.empty) {
-            for (int z = bb.lo[2]; z <= bb.hi[2] && !backed; ++z)
-                for (int y = bb.lo[1]; y <= bb.hi[1] && !backed; ++y)
-                    for (int x = bb.lo[0]; x <= bb.hi[0]; ++x)
-                        if (pt[entry_index(L, d.slot, d.lev, x, y, z)] >= 0) { backed = true; break; }
-        }
-        int64_t side = int64_t(1) << D;
-        int64_t nidx = level_offset(D) + ((int64_t)lz * side + lyy) * side + lx;
-        uint32_t bit = 1u << d.lev;
-        if (backed) atomicOr(words + nidx * L.m + d.slot, bit);
-        else atomicAnd(words + nidx * L.m + d.slot, ~bit);
-    }
-}
-
-// depth dd < D: mask = OR of the 8 children's masks
-__global__ void k_update_parents(const DevLayout L, int32_t n, int dd,
-                                 const int64_t *__restrict__ ids,
-                                 const int64_t *__restrict__ off,
-                                 const int64_t *__restrict__ total_p,
-                                 uint32_t *__restrict__ words) {
-    const int64_t total = *total_p;
-    const int sh = L.depth - dd;
-    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < total;
-         j += (int64_t)gridDim.x * blockDim.x) {
-        int i = find_seg(off, n, j);
-        Decoded d = decode_id(L, ids[i]);
-        Box3 b = leaf_box(L, d.lev, d.x, d.y, d.z);
-        int lo0 = b.lo[0] >> sh, lo1 = b.lo[1] >> sh, lo2 = b.lo[2] >> sh;
-        int w = (b.hi[0] >> sh) - lo0 + 1, h = (b.hi[1] >> sh) - lo1 + 1;
-        int64_t r = j - off[i];
-        int nx = lo0 + (int)(r % w);
-        int ny = lo1 + (int)((r / w) % h);
-        int nz = lo2 + (int)(r / ((int64_t)w * h));
-        int64_t cside = int64_t(1) << (dd + 1);
-        int64_t cbase = level_offset(dd + 1);
-        uint32_t mask = 0;
-        for (int c = 0; c < 8; ++c) {
-            int64_t cx = 2 * nx + (c & 1), cy = 2 * ny + ((c >> 1) & 1), cz = 2 * nz + (c >> 2);
-            mask |= words[(cbase + (cz * cside + cy) * cside + cx) * L.m + d.slot] & 0xFFFFu;
-        }
-        int64_t side = int64_t(1) << dd;
-        uint32_t *wp = words + (level_offset(dd) + ((int64_t)nz * side + ny) * side + nx) * L.m + d.slot;
-        uint32_t old = *wp;
-        uint32_t nw = (old & 0xFFFF0000u) | mask;
-        if (nw != old) *wp = nw;
-    }
-}
-
 // ---- full rebuild (verification) ----
 __global__ void k_rebuild_leaves(const DevLayout L, const int32_t *__restrict__ pt,
                                  uint32_t *__restrict__ words) {
@@ -472,38 +278,69 @@ __global__ void k_reset_range(int32_t *__restrict__ pt, int64_t lo, int64_t hi) 
         pt[e] = RO_PT_UNMAPPED;
 }
 
-__global__ void k_swap_flags(const DevLayout L, const int64_t *__restrict__ slot_brick,
-                             int32_t cs, int32_t *__restrict__ flags) {
-    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < L.num_slots;
-         s += (int64_t)gridDim.x * blockDim.x) {
-        int64_t b = slot_brick[s];
-        flags[s] = (b >= 0 && (int)(((b >> 24) & 0xFF) / L.k) == cs) ? 1 : 0;
+// Engine.swap_channel's release (paging.py:280-283): every slot holding a
+// brick of channel slot cs is freed and pushed on the free list in
+// ascending slot order.  Cooperative: each CTA owns a contiguous slot range,
+// counts its slots, and after one grid sync appends them in order at its
+// offset (block-wide ballot scan).
+__global__ void __launch_bounds__(1024, 1) k_swap_release(const DevLayout L, int32_t cs,
+                                                          int64_t *__restrict__ slot_brick,
+                                                          int64_t *__restrict__ last_used,
+                                                          int32_t *__restrict__ free_stack,
+                                                          int32_t *__restrict__ free_count,
+                                                          uint32_t *__restrict__ cta_counts) {
+    __shared__ uint32_t s_warp[32];
+    __shared__ uint32_t s_total;
+    cg::grid_group grid = cg::this_grid();
+    const int64_t S = L.num_slots;
+    const int64_t per = (S + gridDim.x - 1) / gridDim.x;
+    const int64_t s0 = blockIdx.x * per, s1 = min(S, s0 + per);
+    auto mine = [&](int64_t sl) {
+        if (sl >= s1) return false;
+        const int64_t b = slot_brick[sl];
+        return b >= 0 && (int)(((b >> 24) & 0xFF) / L.k) == cs;
+    };
+    uint32_t cnt = 0;
+    for (int64_t sl = s0 + threadIdx.x; sl < s1; sl += blockDim.x) cnt += mine(sl) ? 1 : 0;
+    cnt = __reduce_add_sync(0xffffffffu, cnt);
+    if ((threadIdx.x & 31) == 0) s_warp[threadIdx.x >> 5] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t t = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_warp[w];
+        cta_counts[blockIdx.x] = t;
     }
-}
-
-// push released slots onto the free list in ascending slot order
-__global__ void k_swap_release(const DevLayout L, const int32_t *__restrict__ flags,
-                               const int32_t *__restrict__ pos,
-                               int64_t *__restrict__ slot_brick,
-                               int64_t *__restrict__ last_used,
-                               int32_t *__restrict__ free_stack,
-                               const int32_t *__restrict__ free_count) {
     const int32_t base = *free_count;
-    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < L.num_slots;
-         s += (int64_t)gridDim.x * blockDim.x) {
-        if (flags[s]) {
-            slot_brick[s] = -1;
-            last_used[s] = 0;
-            free_stack[base + pos[s]] = (int32_t)s;
+    grid.sync();
+    int64_t off = base;
+    for (unsigned c = 0; c < blockIdx.x; ++c) off += __ldcg(cta_counts + c);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int64_t t0 = s0; t0 < s1; t0 += blockDim.x) {
+        const int64_t sl = t0 + threadIdx.x;
+        const bool f = mine(sl);
+        const unsigned bal = __ballot_sync(0xffffffffu, f);
+        __syncthreads();
+        if (lane == 0) s_warp[warp] = __popc(bal);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t run = 0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+                const uint32_t c = s_warp[w];
+                s_warp[w] = run;
+                run += c;
+            }
+            s_total = run;
         }
+        __syncthreads();
+        if (f) {
+            free_stack[off + s_warp[warp] + __popc(bal & ((1u << lane) - 1u))] = (int32_t)sl;
+            slot_brick[sl] = -1;
+            last_used[sl] = 0;
+        }
+        off += s_total;
     }
-}
-
-__global__ void k_swap_count(const DevLayout L, const int32_t *__restrict__ flags,
-                             const int32_t *__restrict__ pos,
-                             int32_t *__restrict__ free_count) {
-    int64_t last = L.num_slots - 1;
-    *free_count += pos[last] + flags[last];
+    grid.sync();
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) *free_count = (int32_t)off;
 }
 
 __global__ void k_invalidate(const DevLayout L, int32_t slot, uint32_t *__restrict__ words) {
@@ -512,7 +349,279 @@ __global__ void k_invalidate(const DevLayout L, int32_t slot, uint32_t *__restri
         words[i * L.m + slot] = 0x00FF0000u;
 }
 
-__global__ void k_sub_free(int32_t *free_count, int32_t n1) { *free_count -= n1; }
+// ---- LRU batch: phases (i)-(iii), page-table map / unmap, one launch ----
+constexpr int kCoopThreads = 1024;
+constexpr int kLruMaxChunks = 1024;
+// ctl (u32, zeroed before the launch): [0] stale count, [1] max stale
+// last_used, [8, 8 + kLruMaxChunks) gather counters, then the select ring
+constexpr int kLruHist = 8 + kLruMaxChunks;
+constexpr int kLruCtlWords = kLruHist + topk::kHistWords;
+
+struct LruArgs {
+    DevLayout L;
+    int32_t n;
+    const int64_t *ids, *entries;
+    const int32_t *flag;  // k_check_batch: 0 = regular batch
+    int32_t *pt;
+    int64_t *slot_brick, *last_used;
+    int32_t *free_stack, *free_count;
+    int64_t S, frame;
+    int32_t *slots;
+    int64_t *evicted;
+    uint8_t *final_flag;
+    unsigned long long *gather;  // [n] victim keys
+    uint32_t *ctl;
+};
+
+// stale occupant of slot s: key (last_used << 32 | s), the argmin order of
+// paging.py:205-206 (min last_used, ties to the lower slot)
+__device__ __forceinline__ bool stale_key(const LruArgs &A, int64_t s, unsigned long long &q) {
+    const int64_t lu = __ldcg(A.last_used + s);
+    if (__ldcg(A.slot_brick + s) < 0 || lu >= A.frame) return false;
+    q = ((unsigned long long)lu << 32) | (unsigned long long)s;
+    return true;
+}
+
+__global__ void __launch_bounds__(kCoopThreads, 1) k_lru_batch(const __grid_constant__ LruArgs A) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ uint32_t s_hist[256];
+    cg::grid_group grid = cg::this_grid();
+    const int32_t n = A.n;
+    const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
+    if (__ldcg(A.flag) != 0) {  // duplicates / mapped ids: the literal loop
+        if (gtid == 0)
+            sequential_insert(A.L, n, A.ids, A.pt, A.slot_brick, A.last_used, A.free_stack,
+                              A.free_count, A.frame, A.slots, A.evicted, A.final_flag);
+        return;
+    }
+    const int32_t fc = __ldcg(A.free_count);
+    const int32_t n1 = n < fc ? n : fc;
+    // (i) pop the free list top-first
+    for (int64_t i = gtid; i < n1; i += gstride) {
+        A.slots[i] = __ldcg(A.free_stack + fc - 1 - i);
+        A.evicted[i] = -1;
+    }
+    const int32_t want = n - n1;
+    int32_t n2 = 0;
+    if (want > 0) {
+        // (ii) the `want` stalest occupants at batch start, in (last_used, slot) order
+        uint32_t cnt = 0, mx = 0;
+        for (int64_t s = gtid; s < A.S; s += gstride) {
+            unsigned long long q;
+            if (stale_key(A, s, q)) {
+                ++cnt;
+                mx = max(mx, (uint32_t)(q >> 32));
+            }
+        }
+        cnt = __reduce_add_sync(0xffffffffu, cnt);
+        mx = __reduce_max_sync(0xffffffffu, mx);
+        if ((threadIdx.x & 31) == 0 && cnt) {
+            atomicAdd(&A.ctl[0], cnt);
+            atomicMax(&A.ctl[1], mx);
+        }
+        grid.sync();
+        const int64_t n_stale = __ldcg(&A.ctl[0]);
+        n2 = (int32_t)(want < n_stale ? want : n_stale);
+        const int bits = 32 + topk::bit_len64(__ldcg(&A.ctl[1]));
+        const int top_shift = ((bits + 7) / 8 - 1) * 8;
+        auto key_of = [&](int64_t s, unsigned long long &q) { return stale_key(A, s, q); };
+        uint32_t g = 0;
+        bool has_lo = false;
+        unsigned long long lo = 0;
+        int chunk = 0;
+        for (int64_t done = 0; done < n2; done += topk::kChunk, ++chunk) {
+            const int64_t w = n2 - done < topk::kChunk ? n2 - done : topk::kChunk;
+            unsigned long long hi = ~0ull;
+            if (done + w < n_stale)
+                hi = topk::select_kth(grid, A.S, key_of, has_lo, lo, w, top_shift,
+                                      A.ctl + kLruHist, g, s_hist);
+            uint32_t *cntp = &A.ctl[8 + chunk % kLruMaxChunks];
+            for (int64_t s = gtid; s < A.S; s += gstride) {
+                unsigned long long q;
+                if (!stale_key(A, s, q) || (has_lo && q <= lo) || q > hi) continue;
+                A.gather[done + atomicAdd(cntp, 1u)] = q;
+            }
+            grid.sync();
+            if (blockIdx.x == (unsigned)(chunk % gridDim.x)) {
+                auto *sk = reinterpret_cast<unsigned long long *>(smem);
+                auto *sv = reinterpret_cast<int32_t *>(sk + topk::kChunk);
+                for (int j = threadIdx.x; j < w; j += blockDim.x) {
+                    sk[j] = __ldcg(A.gather + done + j);
+                    sv[j] = 0;
+                }
+                topk::sort_pairs(sk, sv, (int)w);
+                for (int j = threadIdx.x; j < w; j += blockDim.x) {
+                    const int32_t slot = (int32_t)(sk[j] & 0xFFFFFFFFull);
+                    A.slots[n1 + done + j] = slot;
+                    A.evicted[n1 + done + j] = __ldcg(A.slot_brick + slot);
+                }
+                __syncthreads();
+            }
+            has_lo = true;
+            lo = hi;
+        }
+    }
+    // (iii) cache full of this frame's bricks: every further insert takes slot 0
+    const int32_t p3 = n1 + n2;
+    for (int64_t i = p3 + gtid; i < n; i += gstride) {
+        A.slots[i] = 0;
+        A.evicted[i] = i == p3 ? -2 : A.ids[i - 1];
+    }
+    grid.sync();
+    if (p3 < n && gtid == 0) {  // slot 0's occupant when phase (iii) starts
+        int64_t occ = __ldcg(A.slot_brick);
+        for (int32_t i = p3 - 1; i >= 0; --i)
+            if (__ldcg(A.slots + i) == 0) { occ = A.ids[i]; break; }
+        A.evicted[p3] = occ;
+    }
+    grid.sync();
+    // map the batch; final occupants own their slot
+    for (int64_t i = gtid; i < n; i += gstride) {
+        const int32_t s = __ldcg(A.slots + i);
+        A.pt[A.entries[i]] = s;
+        const bool fin = p3 >= n || s != 0 || i == n - 1;
+        A.final_flag[i] = fin ? 1 : 0;
+        if (fin) A.slot_brick[s] = A.ids[i];
+        A.last_used[s] = A.frame;
+    }
+    grid.sync();
+    for (int64_t i = gtid; i < n; i += gstride) {
+        const int64_t v = __ldcg(A.evicted + i);
+        if (v < 0) continue;
+        const Decoded d = decode_id(A.L, v);
+        A.pt[entry_index(A.L, d.slot, d.lev, d.x, d.y, d.z)] = RO_PT_UNMAPPED;
+    }
+    if (gtid == 0) *A.free_count = fc - n1;
+}
+
+// ---- octree update: every level of the changed bricks, one launch ----
+struct OctArgs {
+    DevLayout L;
+    int32_t n;
+    const int64_t *ids;  // changed bricks (< 0: skip)
+    const int32_t *pt;
+    uint32_t *words;
+    int64_t *offs;  // [n + 1] per-level exclusive scan of node counts
+};
+
+// nodes of brick i's leaf box at depth dd (0 for skipped / empty)
+__device__ __forceinline__ int64_t level_count(const OctArgs &A, int32_t i, int dd, Box3 &b) {
+    b.empty = true;
+    const int64_t id = A.ids[i];
+    if (id < 0) return 0;
+    const Decoded d = decode_id(A.L, id);
+    if (!d.ok) return 0;
+    b = leaf_box(A.L, d.lev, d.x, d.y, d.z);
+    if (b.empty) return 0;
+    const int sh = A.L.depth - dd;
+    int64_t c = 1;
+    for (int a = 0; a < 3; ++a) c *= (int64_t)((b.hi[a] >> sh) - (b.lo[a] >> sh) + 1);
+    return c;
+}
+
+__global__ void __launch_bounds__(kCoopThreads, 1) k_octree_update(const __grid_constant__ OctArgs A) {
+    __shared__ int64_t s_part[kCoopThreads];
+    cg::grid_group grid = cg::this_grid();
+    const int D = A.L.depth;
+    const int32_t n = A.n;
+    const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
+    for (int dd = D; dd >= 0; --dd) {
+        // CTA 0: exclusive scan of the per-brick node counts at this depth
+        if (blockIdx.x == 0) {
+            const int32_t per = (n + kCoopThreads - 1) / kCoopThreads;
+            const int32_t b0 = threadIdx.x * per, b1 = min(n, b0 + per);
+            int64_t sum = 0;
+            Box3 b;
+            for (int32_t i = b0; i < b1; ++i) sum += level_count(A, i, dd, b);
+            s_part[threadIdx.x] = sum;
+            __syncthreads();
+            for (int o = 1; o < kCoopThreads; o <<= 1) {  // Hillis-Steele inclusive scan
+                const int64_t y = threadIdx.x >= o ? s_part[threadIdx.x - o] : 0;
+                __syncthreads();
+                s_part[threadIdx.x] += y;
+                __syncthreads();
+            }
+            int64_t run = s_part[threadIdx.x] - sum;
+            for (int32_t i = b0; i < b1; ++i) {
+                A.offs[i] = run;
+                run += level_count(A, i, dd, b);
+            }
+            if (threadIdx.x == kCoopThreads - 1) A.offs[n] = s_part[threadIdx.x];
+        }
+        grid.sync();
+        const int64_t total = __ldcg(A.offs + n);
+        const int sh = D - dd;
+        for (int64_t j = gtid; j < total; j += gstride) {
+            // brick owning work item j: last i with offs[i] <= j
+            int lo = 0, hi = n - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (__ldcg(A.offs + mid) <= j) lo = mid; else hi = mid - 1;
+            }
+            const int32_t i = lo;
+            const Decoded d = decode_id(A.L, A.ids[i]);
+            const Box3 b = leaf_box(A.L, d.lev, d.x, d.y, d.z);
+            const int lo0 = b.lo[0] >> sh, lo1 = b.lo[1] >> sh, lo2 = b.lo[2] >> sh;
+            const int w = (b.hi[0] >> sh) - lo0 + 1, h = (b.hi[1] >> sh) - lo1 + 1;
+            const int64_t r = j - __ldcg(A.offs + i);
+            const int nx = lo0 + (int)(r % w);
+            const int ny = lo1 + (int)((r / w) % h);
+            const int nz = lo2 + (int)(r / ((int64_t)w * h));
+            const int64_t side = int64_t(1) << dd;
+            uint32_t *wp = A.words +
+                           (level_offset(dd) + ((int64_t)nz * side + ny) * side + nx) * A.L.m + d.slot;
+            if (dd == D) {
+                // leaf: this (slot, level) bit = some MAPPED brick of that level
+                // overlaps the leaf (octree.py:221-226 _leaf_backed)
+                const Box3 bb = brick_box(A.L, D, nx, ny, nz, d.lev);
+                bool backed = false;
+                if (!bb.empty) {
+                    for (int z = bb.lo[2]; z <= bb.hi[2] && !backed; ++z)
+                        for (int y = bb.lo[1]; y <= bb.hi[1] && !backed; ++y)
+                            for (int x = bb.lo[0]; x <= bb.hi[0]; ++x)
+                                if (A.pt[entry_index(A.L, d.slot, d.lev, x, y, z)] >= 0) {
+                                    backed = true;
+                                    break;
+                                }
+                }
+                const uint32_t bit = 1u << d.lev;
+                if (backed) atomicOr(wp, bit);
+                else atomicAnd(wp, ~bit);
+            } else {
+                // inner node: OR of the 8 children's masks (octree.py:228-246)
+                const int64_t cside = side * 2, cbase = level_offset(dd + 1);
+                uint32_t mask = 0;
+                for (int c = 0; c < 8; ++c) {
+                    const int64_t cx = 2 * nx + (c & 1), cy = 2 * ny + ((c >> 1) & 1),
+                                  cz = 2 * nz + (c >> 2);
+                    mask |= __ldcg(A.words + (cbase + (cz * cside + cy) * cside + cx) * A.L.m +
+                                   d.slot) & 0xFFFFu;
+                }
+                const uint32_t old = __ldcg(wp);
+                const uint32_t nw = (old & 0xFFFF0000u) | mask;
+                if (nw != old) *wp = nw;
+            }
+        }
+        grid.sync();
+    }
+}
+
+// one CTA per SM (cooperative kernels above)
+int coop_grid(const void *kern, size_t smem, int *out) {
+    static int sms = 0;
+    if (sms == 0) {
+        int dev = 0;
+        RO_CUDA(cudaGetDevice(&dev));
+        RO_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    int per_sm = 0;
+    RO_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kCoopThreads, smem));
+    if (per_sm < 1) return fail(RO_ECUDA, "cooperative kernel cannot be resident");
+    *out = sms;
+    return RO_OK;
+}
 
 inline unsigned blocks_for(int64_t n, int threads = kThreads) {
     int64_t b = (n + threads - 1) / threads;
@@ -527,35 +636,21 @@ inline unsigned blocks_for(int64_t n, int threads = kThreads) {
 int octree_update(ro_ctx *c, const ro_state *st, const int64_t *ids, int32_t n,
                   cudaStream_t s) {
     if (st->words == nullptr || n <= 0) return RO_OK;
-    const int D = c->layout.depth;
-    const int64_t nseg = (int64_t)(D + 1) * n;
-    void *pc, *po, *tmp;
+    void *po;
     int rc;
-    if ((rc = scratch(c, 5, sizeof(int64_t) * (nseg + D + 1), &pc))) return rc;
-    if ((rc = scratch(c, 6, sizeof(int64_t) * (nseg + D + 1), &po))) return rc;
-    int64_t *counts = (int64_t *)pc, *offs = (int64_t *)po;
-    k_brick_counts<<<(n + 255) / 256, 256, 0, s>>>(c->dl, n, ids, counts);
-    RO_CUDA(cudaGetLastError());
-    // per-level exclusive scans; the level total is stored after the segments
-    size_t tb = 0, tb2 = 0;
-    RO_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, counts, offs, (int)n, s));
-    RO_CUDA(cub::DeviceReduce::Sum(nullptr, tb2, counts, offs, (int)n, s));
-    if (tb2 > tb) tb = tb2;
-    if ((rc = scratch(c, 7, tb, &tmp))) return rc;
-    int64_t *totals = offs + nseg;
-    for (int dd = D; dd >= 0; --dd) {
-        int64_t *cseg = counts + (int64_t)dd * n, *oseg = offs + (int64_t)dd * n;
-        RO_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, cseg, oseg, (int)n, s));
-        // total = off[n-1] + count[n-1]: folded into the kernels via a tiny add
-        RO_CUDA(cub::DeviceReduce::Sum(tmp, tb, cseg, totals + dd, (int)n, s));
-        if (dd == D)
-            k_update_leaves<<<kGridStride, kThreads, 0, s>>>(c->dl, n, ids, oseg,
-                                                             totals + dd, st->pt, st->words);
-        else
-            k_update_parents<<<kGridStride, kThreads, 0, s>>>(c->dl, n, dd, ids, oseg,
-                                                              totals + dd, st->words);
-        RO_CUDA(cudaGetLastError());
-    }
+    if ((rc = scratch(c, 6, sizeof(int64_t) * ((size_t)n + 1), &po))) return rc;
+    OctArgs A;
+    A.L = c->dl;
+    A.n = n;
+    A.ids = ids;
+    A.pt = st->pt;
+    A.words = st->words;
+    A.offs = (int64_t *)po;
+    int grid = 0;
+    if ((rc = coop_grid((const void *)k_octree_update, 0, &grid))) return rc;
+    void *args[] = {&A};
+    RO_CUDA(cudaLaunchCooperativeKernel((const void *)k_octree_update, dim3(grid),
+                                        dim3(kCoopThreads), args, 0, s));
     return RO_OK;
 }
 
@@ -568,39 +663,60 @@ int apply_bricks(ro_ctx *c, const ro_state *st, const int64_t *ids_h, int64_t n6
     if (frame < 0 || frame >= ((int64_t)1 << 31)) return fail(RO_EINVAL, "frame out of range");
     const int32_t n = (int32_t)n64;
     const int64_t bvox = c->bvox;
+    // ids are validated on the host: nothing is queued for a bad batch
+    for (int32_t i = 0; i < n; ++i) {
+        if (!decode_id(c->dl, ids_h[i]).ok) {
+            char msg[160];
+            snprintf(msg, sizeof msg, "brick id outside the layout (index %d of %d, id %lld)",
+                     i, n, (long long)ids_h[i]);
+            return fail(RO_EINVAL, msg);
+        }
+    }
     int rc;
-    void *p;
-    // device scratch layout (slot 0..4 are feedback's; use a dedicated pool)
-    // ids | evicted | entries | slots | final | flag   (ids+evicted contiguous:
-    // together they are the changed set of the octree pass)
-    size_t need = sizeof(int64_t) * 3 * n + sizeof(int32_t) * n + n + 64;
+    void *p, *pl;
+    // ids | evicted | entries | gather | slots | final | flag  (ids + evicted
+    // contiguous: together they are the changed set of the octree pass)
+    size_t need = sizeof(int64_t) * 4 * n + sizeof(int32_t) * n + n + 64;
     if ((rc = scratch(c, 1, need, &p))) return rc;
     int64_t *d_ids = (int64_t *)p;
     int64_t *d_evicted = d_ids + n;
     int64_t *d_entries = d_evicted + n;
-    int32_t *d_slots = (int32_t *)(d_entries + n);
+    auto *d_gather = (unsigned long long *)(d_entries + n);
+    int32_t *d_slots = (int32_t *)(d_gather + n);
     uint8_t *d_final = (uint8_t *)(d_slots + n);
     int32_t *d_flag = (int32_t *)(((uintptr_t)(d_final + n) + 15) & ~(uintptr_t)15);
+    if ((rc = scratch(c, 13, sizeof(uint32_t) * kLruCtlWords, &pl))) return rc;
+    auto *d_ctl = (uint32_t *)pl;
+    int grid = 0;
+    RO_CUDA(cudaFuncSetAttribute(k_lru_batch, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)topk::kSortSmem));
+    if ((rc = coop_grid((const void *)k_lru_batch, topk::kSortSmem, &grid))) return rc;
+    void *dp = nullptr;
+    const size_t bytes = (size_t)bvox * n;
+    if (payloads && !on_device) {
+        // the upload has a scratch slot of its own: nothing else on the
+        // stream can reuse it while the DMA may still run
+        if ((rc = scratch(c, 12, bytes, &dp))) return rc;
+    }
 
-    // payload upload on the side stream (overlaps the checks)
+    // payload upload on the side stream (overlaps the checks and the LRU)
     const uint8_t *d_payload = nullptr;
-    bool caller_pinned = false;
-    // a DMA from the caller's pinned buffer completes before any return
-    struct UploadWait {
+    bool queued = false, caller_pinned = false;
+    // once the DMA is queued, every return makes the stream wait for it, and
+    // a caller-pinned source buffer is released only when the DMA is done
+    struct UploadGuard {
         ro_ctx *c;
-        const bool *on;
-        ~UploadWait() { if (*on) cudaEventSynchronize(c->upload_done); }
-    } upload_wait{c, &caller_pinned};
+        cudaStream_t s;
+        const bool *queued, *pinned;
+        ~UploadGuard() {
+            if (*queued) cudaStreamWaitEvent(s, c->upload_done, 0);
+            if (*queued && *pinned) cudaEventSynchronize(c->upload_done);
+        }
+    } guard{c, s, &queued, &caller_pinned};
     if (payloads) {
         if (on_device) {
             d_payload = (const uint8_t *)payloads;
         } else {
-            void *dp;
-            if ((rc = scratch(c, 2, (size_t)bvox * n, &dp))) return rc;
-            size_t bytes = (size_t)bvox * n;
-            // payloads already in pinned memory are DMA'd straight from the
-            // caller's buffer (waited for before returning); pageable ones go
-            // through the handle's pinned staging buffer
             cudaPointerAttributes pa;
             if (cudaPointerGetAttributes(&pa, payloads) != cudaSuccess) {
                 cudaGetLastError();
@@ -609,7 +725,9 @@ int apply_bricks(ro_ctx *c, const ro_state *st, const int64_t *ids_h, int64_t n6
             caller_pinned = pa.type == cudaMemoryTypeHost;
             const void *src = payloads;
             if (!caller_pinned) {
+                // pageable payloads: one host copy into the handle's pinned staging
                 if (c->staging_bytes < bytes) {
+                    RO_CUDA(cudaEventSynchronize(c->upload_done));
                     if (c->staging) cudaFreeHost(c->staging);
                     c->staging = nullptr;
                     c->staging_bytes = 0;
@@ -625,11 +743,13 @@ int apply_bricks(ro_ctx *c, const ro_state *st, const int64_t *ids_h, int64_t n6
             RO_CUDA(cudaStreamWaitEvent(c->upload, c->host_done, 0));
             RO_CUDA(cudaMemcpyAsync(dp, src, bytes, cudaMemcpyHostToDevice, c->upload));
             RO_CUDA(cudaEventRecord(c->upload_done, c->upload));
+            queued = true;
             d_payload = (const uint8_t *)dp;
         }
     }
     RO_CUDA(cudaMemcpyAsync(d_ids, ids_h, sizeof(int64_t) * n, cudaMemcpyHostToDevice, s));
     RO_CUDA(cudaMemsetAsync(d_flag, 0, sizeof(int32_t), s));
+    RO_CUDA(cudaMemsetAsync(d_ctl, 0, sizeof(uint32_t) * kLruCtlWords, s));
     if (++c->epoch == 0) {  // stamp wrap: clear claims
         RO_CUDA(cudaMemsetAsync(c->claim, 0, sizeof(uint32_t) * c->E, s));
         c->epoch = 1;
@@ -637,77 +757,31 @@ int apply_bricks(ro_ctx *c, const ro_state *st, const int64_t *ids_h, int64_t n6
     k_check_batch<<<(n + 255) / 256, 256, 0, s>>>(c->dl, d_ids, n, st->pt, c->claim,
                                                   c->epoch, d_flag, d_entries);
     RO_CUDA(cudaGetLastError());
-    int32_t *h = reinterpret_cast<int32_t *>(c->pinned_small);
-    RO_CUDA(cudaMemcpyAsync(h, d_flag, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    RO_CUDA(cudaMemcpyAsync(h + 1, st->free_count, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    RO_CUDA(cudaStreamSynchronize(s));
-    const int32_t flag = h[0], free_count = h[1];
-    if (flag & 2) {
-        std::vector<int64_t> back(n), ent(n);
-        cudaMemcpy(back.data(), d_ids, sizeof(int64_t) * n, cudaMemcpyDeviceToHost);
-        cudaMemcpy(ent.data(), d_entries, sizeof(int64_t) * n, cudaMemcpyDeviceToHost);
-        int32_t bad = -1;
-        for (int32_t i = 0; i < n; ++i)
-            if (ent[i] < 0) { bad = i; break; }
-        char msg[256];
-        snprintf(msg, sizeof msg,
-                 "brick id outside the layout (flag %d, n %d, first bad index %d, "
-                 "device id %lld, host id %lld)", flag, n, bad,
-                 bad >= 0 ? (long long)back[bad] : -1LL,
-                 bad >= 0 ? (long long)ids_h[bad] : -1LL);
-        return fail(RO_EINVAL, msg);
-    }
-
-    int32_t p3 = n;  // first phase-(iii) index
-    if (flag == 0) {
-        const int32_t n1 = n < free_count ? n : free_count;
-        if (n1 > 0) {
-            k_assign_free<<<(n1 + 255) / 256, 256, 0, s>>>(n1, st->free_stack, free_count,
-                                                           d_slots, d_evicted);
-            k_sub_free<<<1, 1, 0, s>>>(st->free_count, n1);
-        }
-        if (n > n1) {
-            void *pk, *pk2, *ptmp;
-            const int64_t S = c->S;
-            if ((rc = scratch(c, 3, sizeof(unsigned long long) * S + 16, &pk))) return rc;
-            if ((rc = scratch(c, 0, sizeof(unsigned long long) * S, &pk2))) return rc;
-            auto *keys = (unsigned long long *)pk, *sorted = (unsigned long long *)pk2;
-            int32_t *d_cnt = (int32_t *)(keys + S);
-            RO_CUDA(cudaMemsetAsync(d_cnt, 0, sizeof(int32_t), s));
-            k_stale_keys<<<blocks_for(S), kThreads, 0, s>>>(st->slot_brick, st->slot_last_used,
-                                                             S, frame, keys, d_cnt);
-            RO_CUDA(cudaMemcpyAsync(h + 2, d_cnt, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-            RO_CUDA(cudaStreamSynchronize(s));
-            const int32_t n_stale = h[2];
-            const int32_t want = n - n1;
-            const int32_t n2 = want < n_stale ? want : n_stale;
-            if (n_stale > 0) {
-                size_t tb = 0;
-                RO_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, keys, sorted, n_stale, 0, 64, s));
-                if ((rc = scratch(c, 4, tb, &ptmp))) return rc;
-                RO_CUDA(cub::DeviceRadixSort::SortKeys(ptmp, tb, keys, sorted, n_stale, 0, 64, s));
-            }
-            k_assign_victims<<<(want + 255) / 256, 256, 0, s>>>(n1, n, n2, sorted, st->slot_brick,
-                                                                d_ids, d_slots, d_evicted);
-            RO_CUDA(cudaGetLastError());
-            if (n1 + n2 < n) {
-                p3 = n1 + n2;
-                k_phase3_first<<<1, 1, 0, s>>>(p3, d_slots, d_ids, st->slot_brick, d_evicted);
-            }
-        }
-        k_map_batch<<<(n + 255) / 256, 256, 0, s>>>(c->dl, n, p3, d_ids, d_entries, d_slots,
-                                                    st->pt, st->slot_brick, st->slot_last_used,
-                                                    frame, d_final);
-        k_unmap_evicted<<<(n + 255) / 256, 256, 0, s>>>(c->dl, n, d_evicted, st->pt);
-        RO_CUDA(cudaGetLastError());
-    } else {
-        k_sequential_insert<<<1, 1, 0, s>>>(c->dl, n, d_ids, st->pt, st->slot_brick,
-                                            st->slot_last_used, st->free_stack, st->free_count,
-                                            frame, d_slots, d_evicted, d_final);
-        RO_CUDA(cudaGetLastError());
-    }
+    // LRU assignment + page-table map / unmap: one cooperative launch, the
+    // regular / sequential choice made on the device (no host round trip)
+    LruArgs A;
+    A.L = c->dl;
+    A.n = n;
+    A.ids = d_ids;
+    A.entries = d_entries;
+    A.flag = d_flag;
+    A.pt = st->pt;
+    A.slot_brick = st->slot_brick;
+    A.last_used = st->slot_last_used;
+    A.free_stack = st->free_stack;
+    A.free_count = st->free_count;
+    A.S = c->S;
+    A.frame = frame;
+    A.slots = d_slots;
+    A.evicted = d_evicted;
+    A.final_flag = d_final;
+    A.gather = d_gather;
+    A.ctl = d_ctl;
+    void *args[] = {&A};
+    RO_CUDA(cudaLaunchCooperativeKernel((const void *)k_lru_batch, dim3(grid),
+                                        dim3(kCoopThreads), args, topk::kSortSmem, s));
     if (d_payload) {
-        if (!on_device) RO_CUDA(cudaStreamWaitEvent(s, c->upload_done, 0));
+        if (queued) RO_CUDA(cudaStreamWaitEvent(s, c->upload_done, 0));
         if (bvox % 16 == 0 && ((uintptr_t)d_payload & 15) == 0 &&
             ((uintptr_t)st->cache & 15) == 0)
             k_copy_payloads<<<blocks_for((bvox / 16) * n), kThreads, 0, s>>>(
@@ -828,21 +902,18 @@ int swap_channel(ro_ctx *c, const ro_state *st, int32_t cs, int32_t invalidate,
     const int k = c->layout.k;
     const int64_t lo = c->layout.pt_offsets[cs * k], hi = c->layout.pt_offsets[cs * k + k];
     if (hi > lo) k_reset_range<<<blocks_for(hi - lo), kThreads, 0, s>>>(st->pt, lo, hi);
-    const int64_t S = c->S;
-    void *pf, *pp, *tmp;
-    int rc;
-    if ((rc = scratch(c, 2, sizeof(int32_t) * S, &pf))) return rc;
-    if ((rc = scratch(c, 3, sizeof(int32_t) * S, &pp))) return rc;
-    int32_t *flags = (int32_t *)pf, *pos = (int32_t *)pp;
-    k_swap_flags<<<blocks_for(S), kThreads, 0, s>>>(c->dl, st->slot_brick, cs, flags);
-    size_t tb = 0;
-    RO_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, flags, pos, (int)S, s));
-    if ((rc = scratch(c, 4, tb, &tmp))) return rc;
-    RO_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, flags, pos, (int)S, s));
-    k_swap_release<<<blocks_for(S), kThreads, 0, s>>>(c->dl, flags, pos, st->slot_brick,
-                                                       st->slot_last_used, st->free_stack,
-                                                       st->free_count);
-    k_swap_count<<<1, 1, 0, s>>>(c->dl, flags, pos, st->free_count);
+    void *pc;
+    int rc, grid = 0;
+    if ((rc = coop_grid((const void *)k_swap_release, 0, &grid))) return rc;
+    if ((rc = scratch(c, 14, sizeof(uint32_t) * grid, &pc))) return rc;
+    DevLayout L = c->dl;
+    int32_t cs_ = cs;
+    int64_t *sb = st->slot_brick, *lu = st->slot_last_used;
+    int32_t *fs = st->free_stack, *fc = st->free_count;
+    uint32_t *cnt = (uint32_t *)pc;
+    void *args[] = {&L, &cs_, &sb, &lu, &fs, &fc, &cnt};
+    RO_CUDA(cudaLaunchCooperativeKernel((const void *)k_swap_release, dim3(grid),
+                                        dim3(kCoopThreads), args, 0, s));
     if (invalidate && st->words)
         k_invalidate<<<blocks_for(c->num_nodes), kThreads, 0, s>>>(c->dl, cs, st->words);
     RO_CUDA(cudaGetLastError());
