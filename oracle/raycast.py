@@ -52,7 +52,7 @@ class _Frame(C.Structure):
         ("meta_req", _P), ("meta_req_n", _P), ("req_cap", C.c_int64),
         ("seen_brick", _P), ("seen_meta", _P), ("required", _P),
         ("pix_required", _P), ("hist", _P), ("counters", _P),
-        ("pix_begin", C.c_int64), ("pix_end", C.c_int64),
+        ("pix_begin", C.c_int64), ("pix_end", C.c_int64), ("touched", C.c_void_p),
     ]
 
 
@@ -196,13 +196,15 @@ def _ptr(a):
 def render(state: OracleState, channels, camera, image_dims, base_step,
            t0=1.0, early_alpha=0.99, budget=256, start_level=2,
            mode=MODE_RESIDENCY, reference_state: OracleState | None = None,
-           rows=None, threads=1, rays=None, classic=None) -> OracleOutput:
+           rows=None, threads=1, rays=None, classic=None, touched=None) -> OracleOutput:
     """One oracle frame.
 
     camera: (position, target, up, fov_deg).  ``classic`` = (min u8[n, m],
     max u8[n, m], depth) for MODE_CLASSIC (render.py:271-315).  ``rows`` = (row_begin,
     row_end) renders only those scanlines (the other pixels stay zero);
     ``threads`` > 1 uses the band-parallel driver (identical results).
+    ``touched``: optional u8 array shaped like the cache; every voxel a
+    trilinear fetch reads is set to 1 (fixture generation only).
     """
     lib = _lib()
     k, m = state.k, state.m
@@ -296,7 +298,7 @@ def render(state: OracleState, channels, camera, image_dims, base_step,
         seen_brick=_ptr(seen_brick), seen_meta=_ptr(seen_meta),
         required=_ptr(required), pix_required=_ptr(pix_required),
         hist=_ptr(hist), counters=_ptr(counters),
-        pix_begin=r0 * w, pix_end=r1 * w)
+        pix_begin=r0 * w, pix_end=r1 * w, touched=_ptr(touched))
     if threads <= 1:
         rc = lib.oracle_raycast(C.byref(fr))
     else:

@@ -84,6 +84,9 @@ typedef struct oracle_frame {
     int64_t *hist;            /* [n_ch*k] */
     int64_t *counters;        /* [5]: steps, evaluated, skipped, violations, livelocks */
     int64_t pix_begin, pix_end;
+    /* optional [S*bvox]: every cache byte a trilinear fetch reads is set to
+       1 (fixture generation: which voxels a frame depends on) */
+    uint8_t *touched;
 } oracle_frame;
 
 static inline double lerp(double a, double b, double t) { return a + (b - a) * t; }
@@ -170,7 +173,7 @@ static void tf_eval(const oracle_frame *f, int64_t ci, double v, double *r,
 /* kernels.py:136-174 */
 static double trilinear_brick(const uint8_t *cache, int64_t slot_lin, double lx,
                               double ly, double lz, int64_t bx, int64_t by,
-                              int64_t bz) {
+                              int64_t bz, uint8_t *touched) {
     double fx = lx - 0.5, fy = ly - 0.5, fz = lz - 0.5;
     if (fx < 0.0) fx = 0.0;
     if (fy < 0.0) fy = 0.0;
@@ -184,6 +187,13 @@ static double trilinear_brick(const uint8_t *cache, int64_t slot_lin, double lx,
     int64_t z1 = z0 + 1 < bz ? z0 + 1 : bz - 1;
     double tx = fx - x0, ty = fy - y0, tz = fz - z0;
     const uint8_t *c = cache + slot_lin * bx * by * bz;
+    if (touched) {
+        uint8_t *tc = touched + slot_lin * bx * by * bz;
+        const int64_t zs[2] = {z0, z1}, ys[2] = {y0, y1}, xs[2] = {x0, x1};
+        for (int a = 0; a < 2; ++a)
+            for (int b2 = 0; b2 < 2; ++b2)
+                for (int c2 = 0; c2 < 2; ++c2) tc[(zs[a] * by + ys[b2]) * bx + xs[c2]] = 1;
+    }
 #define V(z, y, x) ((double)c[((z) * by + (y)) * bx + (x)])
     double c00 = lerp(V(z0, y0, x0), V(z0, y0, x1), tx);
     double c10 = lerp(V(z0, y1, x0), V(z0, y1, x1), tx);
@@ -226,7 +236,8 @@ static double ref_value(const oracle_frame *f, int64_t slot, int64_t lev,
     double lx = px * f->dims[lev * 3 + 0] - (double)(cbx * f->bx);
     double ly = py * f->dims[lev * 3 + 1] - (double)(cby * f->by);
     double lz = pz * f->dims[lev * 3 + 2] - (double)(cbz * f->bz);
-    return trilinear_brick(f->ref_cache, f->ref_slot[e], lx, ly, lz, f->bx, f->by, f->bz);
+    return trilinear_brick(f->ref_cache, f->ref_slot[e], lx, ly, lz, f->bx, f->by, f->bz,
+                           NULL);
 }
 
 static inline void push_req(int64_t *buf, int64_t *n, int64_t cap, int64_t v) {
@@ -599,7 +610,8 @@ int oracle_raycast(const oracle_frame *f) {
                     double lx = px * f->dims[lev * 3 + 0] - (double)(cbx * bx);
                     double ly = py * f->dims[lev * 3 + 1] - (double)(cby * by);
                     double lz = pz * f->dims[lev * 3 + 2] - (double)(cbz * bz);
-                    v = trilinear_brick(f->cache, out_slot[ci], lx, ly, lz, bx, by, bz);
+                    v = trilinear_brick(f->cache, out_slot[ci], lx, ly, lz, bx, by, bz,
+                                        f->touched);
                     int64_t gb = entry_index(f, f->ch_slot[ci], lev, cbx, cby, cbz);
                     f->required[gb] = 1;
                     f->hist[ci * k + lev] += 1;

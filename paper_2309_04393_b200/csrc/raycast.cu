@@ -169,6 +169,14 @@ __device__ __forceinline__ double i2d(int v) {
     return __hiloint2double(0x43300000, v) - kTwo52;
 }
 
+// (int)x for 0 <= x < 2^31 on the fp64 pipe: x + 2^52 rounded toward zero
+// is 2^52 + trunc(x) exactly (ulp 1 in [2^52, 2^53)); its low word is the
+// integer.  Same value as the F2I.F64.TRUNC conversion, without the
+// conversion unit's latency.
+__device__ __forceinline__ int d2i_nn(double x) {
+    return __double2loint(__dadd_rz(x, kTwo52));
+}
+
 // (1-alpha)^(2^j): the reference calls libm pow with ratio = step/base_step,
 // always an exact power of two.  Repeated squaring in double-double gives
 // the correctly rounded power (glibc pow is within 0.52 ulp, so the two
@@ -192,7 +200,8 @@ __device__ __forceinline__ int lod_raw(double t, double t0, double inv_t0, bool 
                                        const FrameSmem &S) {
     const double ratio = t0_pow2 ? t * inv_t0 : t / t0;  // exact when t0 = 2^k
     if (ratio < 1.0) return 0;
-    const int e = ilogb(ratio);
+    // ratio >= 1 (or +inf): the unbiased exponent field is ilogb(ratio)
+    const int e = ((__double2hiint(ratio) >> 20) & 0x7FF) - 1023;
     if (e >= RO_MAX_LEVELS - 1) return RO_MAX_LEVELS - 1;
     int lev = e;
     if (ratio >= S.lod_thr[lev + 1]) lev += 1;
@@ -213,7 +222,7 @@ __device__ __forceinline__ void tf_eval(const FrameSmem &S, int ci, double v,
     if (n < 2 || v < S.tf_x[ci][0] || v > S.tf_x[ci][n - 1]) return;
     // the reference takes the first segment with x0 <= v <= x1; with strictly
     // increasing knots that is the first i with x[i+1] >= v
-    int i = S.tf_seg[ci][(int)v];
+    int i = S.tf_seg[ci][d2i_nn(v)];
     while (i < n - 2 && S.tf_x[ci][i + 1] < v) ++i;
     const double dxs = S.tf_dx[ci][i];
     const double t = (dxs == 0.0) ? 0.0 : (v - S.tf_x[ci][i]) / dxs;
@@ -263,6 +272,12 @@ __device__ __forceinline__ void request(unsigned long long *keys, int32_t *, int
 
 // Brick coordinates of one level at the current sample position:
 // P = fl(p * dim) (kernels.py:179 numerator), c = int(P / b) = int(P) >> lb.
+#ifndef RO_STATS
+#define RO_STATS 0
+#endif
+#ifndef RO_LEAF_CACHE
+#define RO_LEAF_CACHE 0
+#endif
 #ifndef RO_LP2_LOCAL
 #define RO_LP2_LOCAL 0
 #endif
@@ -292,7 +307,7 @@ __device__ __forceinline__ void level_pos(LevelPos &lp, int lev, double px, doub
 #if !RO_LP_NOP
         lp.P[a] = P;
 #endif
-        const int ip = (int)P;
+        const int ip = d2i_nn(P);
         int c = ip >> lb3[a];
         const int g = S.grids[lev][a];
         lp.cb[a] = c > g - 1 ? g - 1 : c;
@@ -386,8 +401,9 @@ __device__ __forceinline__ void taps_of(Taps &tp, const LevelPos &lp, double px,
 #endif
         double f = (P - i2d(lp.cb[a] * B[a])) - 0.5;
         if (f < 0.0) f = 0.0;
-        if (f > S.bm1[a]) f = S.bm1[a];
-        const int c0 = (int)f;
+        const double bm1 = (double)(B[a] - 1);  // a constant for compile-time bricks
+        if (f > bm1) f = bm1;
+        const int c0 = d2i_nn(f);
         i0[a] = c0;
         tw[a] = f - i2d(c0);
     }
@@ -515,7 +531,11 @@ __global__ void __launch_bounds__(256) k_classify_nodes(const __grid_constant__ 
     }
 }
 
-template <int MODE, bool CHECK, int BX, int BY>
+__host__ __device__ constexpr int ilog2c(int v) { return v > 1 ? 1 + ilog2c(v >> 1) : 0; }
+
+// BX / BY / BZ: compile-time brick extent (0: runtime) -- tap offsets, brick
+// and sub-block coordinates then use constant shifts and masks
+template <int MODE, bool CHECK, int BX, int BY, int BZ>
 __global__ void __launch_bounds__(kBlock, RO_MINB * 4 / kWarps)
 k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A) {
     __shared__ FrameSmem S;
@@ -594,6 +614,14 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
     const int tiles_x = (F.width + kTileW - 1) / kTileW;
     // per-thread work counters (32-bit: a thread's share stays far below 2^32)
     uint32_t c_steps = 0, c_eval = 0, c_skip = 0, c_viol = 0, c_live = 0;
+#if RO_STATS
+    // instrumentation build only: counters[5..7] = probe misses, tap loads,
+    // full TF evaluations
+    uint32_t c_s5 = 0, c_s6 = 0, c_s7 = 0;
+#define RO_STAT(v) (v) += 1
+#else
+#define RO_STAT(v) do { } while (0)
+#endif
 
 #if RO_PERSISTENT
     // Persistent CTAs: tables are staged once per CTA, then 16x8 pixel tiles
@@ -631,8 +659,9 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
     const int gy = ((ly / tr) * F.n_parts + F.part) * tr + (ly % tr);
     const bool active = x < F.width && ly < A.local_rows && gy < F.height;
 
-    const int bx = A.L.bx, by = A.L.by, bz = A.L.bz;
-    const int lbx = __ffs(bx) - 1, lby = __ffs(by) - 1, lbz = __ffs(bz) - 1;
+    const int bx = BX ? BX : A.L.bx, by = BY ? BY : A.L.by, bz = BZ ? BZ : A.L.bz;
+    const int lbx = BX ? ilog2c(BX) : __ffs(bx) - 1, lby = BY ? ilog2c(BY) : __ffs(by) - 1,
+              lbz = BZ ? ilog2c(BZ) : __ffs(bz) - 1;
     const int bvox = bx * by * bz;
     const int D = A.L.depth;
     const bool vec4 = (m == 4);
@@ -669,6 +698,13 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
     int stall = 0;
     uint32_t ev = 0;  // request event index within this pixel
     int32_t pixreq = 0;
+#if RO_LEAF_CACHE
+    // the last node word vector / class read by this ray (frame-constant
+    // state: reusable by the next sample in the same node)
+    int cur_node = -1, cls_node = -1;
+    bool cls_fast = false;
+    uint4 wv = make_uint4(0, 0, 0, 0);
+#endif
     [[maybe_unused]] int n_probe = 0;  // CHECK: cursor-resolved samples (max_samples)
 
     // Warp-uniform sample loop: lanes whose ray ended idle until the whole
@@ -752,6 +788,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                 RO_ASSERT(slot_lin >= 0 && slot_lin < A.L.num_slots && tp.o >= 0 &&
                           tp.o + (int64_t)bx * by + bx + 1 < 2 * (int64_t)bvox);
                 load_taps<BX, BY>(tv, A.cache + (int64_t)slot_lin * bvox + tp.o, bx, bx * by);
+                RO_STAT(c_s6);
                 // The trilinear value never exceeds the largest tap (every lerp
                 // is a rounded convex combination).  If that tap lies in the
                 // TF's leading zero-opacity range, r*a, g*a, b*a are +0 and
@@ -759,6 +796,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                 const int mt = max(max(max(tv[0], tv[1]), max(tv[2], tv[3])),
                                    max(max(tv[4], tv[5]), max(tv[6], tv[7])));
                 if (mt <= S.zero_upto[ci]) return;
+                RO_STAT(c_s7);
                 const double val = trilerp(tv, tp);
                 double r, g, b, a;
                 tf_eval(S, ci, val, r, g, b, a);
@@ -838,7 +876,8 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                 // (node depth d <-> level cls_depth - d, one brick per node)
                 const int CD = F.cls_depth;
                 const double cside = (double)(1 << CD);
-                const int qx = (int)(px * cside), qy = (int)(py * cside), qz = (int)(pz * cside);
+                const int qx = d2i_nn(px * cside), qy = d2i_nn(py * cside),
+                          qz = d2i_nn(pz * cside);
                 bool all_empty = true;
                 int deep_d = -1, dix = 0, diy = 0, diz = 0;
 #pragma unroll 1
@@ -903,15 +942,18 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                 }
             } else {
                 // kernels.py:431-558 -- one cursor shared by all channels
-                const int qx = (int)(px * S.side_d), qy = (int)(py * S.side_d), qz = (int)(pz * S.side_d);
+                const int qx = d2i_nn(px * S.side_d), qy = d2i_nn(py * S.side_d),
+                          qz = d2i_nn(pz * S.side_d);
                 int d = prev_depth - 1;
                 if (d < 0) d = 0;
                 if (F.start_level < d) d = F.start_level;
                 if (d > dt_) d = dt_;
                 bool all_cz = true;
                 int ix = 0, iy = 0, iz = 0;
+#if !RO_LEAF_CACHE
                 int cur_node = -1;
                 uint4 wv = make_uint4(0, 0, 0, 0);
+#endif
                 const int d0 = d;
                 // pre-classified depth-dt node (k_classify_nodes): every
                 // channel reaches dt through plain nodes and probes there
@@ -921,19 +963,24 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                     const int lx = qx >> sh, lyy = qy >> sh, lz = qz >> sh;
                     const int leaf = S.lvl_off[dt_] + (((lz << dt_) + lyy) << dt_) + lx;
                     RO_ASSERT(leaf >= 0 && leaf < A.L.num_nodes);
+#if RO_LEAF_CACHE
+                    if (leaf != cls_node) {
+                        cls_node = leaf;
+                        cls_fast = __ldg(A.node_class + leaf) != 0;
+                    }
+                    fast = cls_fast;
+#else
                     fast = __ldg(A.node_class + leaf) != 0;
+#endif
                     if (fast) {
                         c_steps += dt_ - d0 + n_ch;
                         d = dt_;
                         ix = lx;
                         iy = lyy;
                         iz = lz;
-                        if (vec4) {
+                        if (vec4 && leaf != cur_node)
                             wv = ld_meta4(reinterpret_cast<const uint4 *>(A.words) + leaf);
-                            cur_node = leaf;
-                        } else {
-                            cur_node = leaf;
-                        }
+                        cur_node = leaf;
                     }
                 }
 #if RO_FAST_DESCENT
@@ -1114,6 +1161,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                             }
                         }
                         {
+                            RO_STAT(c_s5);
                             const unsigned long long key = key_hi | ev++;
                             int32_t &lb = last_breq[ci * kBlock + tid];
                             if (e != lb) {
@@ -1247,16 +1295,22 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
     }  // tile loop
 
     // ---- block reductions ----
+#if RO_STATS
+    unsigned long long vals[8] = {c_steps, c_eval, c_skip, c_viol, c_live, c_s5, c_s6, c_s7};
+    constexpr int kNV = 8;
+#else
     unsigned long long vals[5] = {c_steps, c_eval, c_skip, c_viol, c_live};
+    constexpr int kNV = 5;
+#endif
 #pragma unroll
-    for (int i = 0; i < 5; ++i) {
+    for (int i = 0; i < kNV; ++i) {
         unsigned long long vv = vals[i];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) vv += __shfl_down_sync(0xffffffffu, vv, o);
         if (lane == 0 && vv) atomicAdd(&S.red[i], vv);
     }
     __syncthreads();
-    if (tid < 5 && S.red[tid]) atomicAdd(A.counters + tid, S.red[tid]);
+    if (tid < kNV && S.red[tid]) atomicAdd(A.counters + tid, S.red[tid]);
     for (int i = tid; i < n_ch * k; i += kBlock) {
         unsigned long long s = 0;
         for (int j = 0; j < kBlock; ++j) s += hist_t[i * kBlock + j];
@@ -1264,7 +1318,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
     }
 }
 
-template <int MODE, bool CHECK, int BX, int BY>
+template <int MODE, bool CHECK, int BX, int BY, int BZ>
 cudaError_t launch_b(const ro_frame &F, const RayArgs &A, cudaStream_t s) {
     int n_tiles = ((F.width + kTileW - 1) / kTileW) * ((A.local_rows + kTileH - 1) / kTileH);
     static int sm_count = 0;
@@ -1277,7 +1331,7 @@ cudaError_t launch_b(const ro_frame &F, const RayArgs &A, cudaStream_t s) {
 #ifdef RO_EXTRA_SMEM
     dyn += RO_EXTRA_SMEM;  // experiment knob: shared-memory / L1 split sensitivity
 #endif
-    auto kern = k_raycast<MODE, CHECK, BX, BY>;
+    auto kern = k_raycast<MODE, CHECK, BX, BY, BZ>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)dyn);
     if (e != cudaSuccess) return e;
@@ -1298,9 +1352,11 @@ cudaError_t launch_b(const ro_frame &F, const RayArgs &A, cudaStream_t s) {
 // brick sizes with compile-time tap offsets; anything else uses runtime ones
 template <int MODE, bool CHECK>
 cudaError_t launch(const ro_frame &F, const RayArgs &A, cudaStream_t s) {
-    if (A.L.bx == 32 && A.L.by == 32) return launch_b<MODE, CHECK, 32, 32>(F, A, s);
-    if (A.L.bx == 16 && A.L.by == 16) return launch_b<MODE, CHECK, 16, 16>(F, A, s);
-    return launch_b<MODE, CHECK, 0, 0>(F, A, s);
+    if (A.L.bx == 32 && A.L.by == 32 && A.L.bz == 32)
+        return launch_b<MODE, CHECK, 32, 32, 32>(F, A, s);
+    if (A.L.bx == 16 && A.L.by == 16 && A.L.bz == 16)
+        return launch_b<MODE, CHECK, 16, 16, 16>(F, A, s);
+    return launch_b<MODE, CHECK, 0, 0, 0>(F, A, s);
 }
 
 }  // namespace

@@ -521,6 +521,125 @@ def tf_queries():
     return {"tfs": items}, rec
 
 
+def config2_bands():
+    """BASELINE config 2 at its benchmarked scale -- k = 7 levels, octree
+    D = 6, 4 of 16 CyCIF-like 2048x2048x128 channels, partial residency
+    (levels >= 2 + half of levels 0/1, so rays substitute coarser levels),
+    exact dilated metadata, 1920x1080 -- built on the CPU with the package's
+    own scenario recipe (scenarios.cycif), then rendered by the REFERENCE's
+    numba kernel (kernels.raycast_frame, kernels.py:209-234) on row bands of
+    the frame, driven exactly as render._run drives it (render.py:125-233).
+
+    Stored: the reference-layout page table and octree words, and only the
+    bricks those bands sample (every other resident brick points at one
+    all-zero slot -- a ray reads voxels of sampled bricks only, so the
+    compacted state renders identically; re-checked here by rendering the
+    bands again from it), plus each band's image, complete first-seen
+    brick / metadata request lists, usage mask, level histogram, per-pixel
+    brick switches and counters."""
+    import torch
+    torch.set_num_threads(os.cpu_count() or 1)
+    sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+    from paper_2309_04393_b200 import scenarios
+    from resoctree import kernels
+    from resoctree import render as rrender
+    from resoctree.camera import Camera as RCamera, generate_rays
+    scn = scenarios.cycif(device="cpu")
+    st = scenarios.reference_state(scn)
+    cfg = scn.render
+    w, hgt = cfg.image_dims
+    k, m, D = st["k"], st["m"], st["depth"]
+    rchans = [ChannelSettings(slot=c.slot, tf=TransferFunction(points=c.tf.points),
+                              level_range=tuple(c.level_range)) for c in scn.channels]
+    packed = rrender._pack_channels(rchans, k)
+    cam = scn.camera
+    origins, dirs = generate_rays(RCamera(position=cam.position, target=cam.target,
+                                          up=cam.up, fov_deg=cam.fov_deg), w, hgt)
+    lvl_off = np.array([((1 << (3 * d)) - 1) // 7 for d in range(D + 1)], dtype=np.int64)
+    dims = np.ascontiguousarray(st["level_dims"], dtype=np.int32)
+    grids = np.ascontiguousarray(st["level_grids"], dtype=np.int32)
+    bsz = np.array(st["brick_size"], dtype=np.int32)
+    E = int(st["pt_offsets"][-1])
+    words = np.ascontiguousarray(st["words"], dtype=np.uint32)
+    cap = 1 << 18
+
+    def band(a, b, pt_status, pt_slot, cache):
+        sl = slice(a * w, b * w)
+        o, d = np.ascontiguousarray(origins[sl]), np.ascontiguousarray(dirs[sl])
+        npix = (b - a) * w
+        image = np.zeros((npix, 4), dtype=np.float32)
+        breq, bn = np.zeros(cap, dtype=np.int64), np.zeros(1, dtype=np.int64)
+        mreq, mn = np.zeros(cap, dtype=np.int64), np.zeros(1, dtype=np.int64)
+        required = np.zeros(E, dtype=np.uint8)
+        pixr = np.zeros(npix, dtype=np.int32)
+        hist = np.zeros((len(rchans), k), dtype=np.int64)
+        counters = np.zeros(4, dtype=np.int64)
+        kernels.raycast_frame(
+            kernels.MODE_RESIDENCY, o, d, *packed,
+            cfg.base_step, cfg.lod_reference_distance, cfg.early_term_alpha, st["eps_h"],
+            cfg.traversal_start_level, D, k, m, lvl_off, words, dims, grids, bsz,
+            st["pt_offsets"], pt_status, pt_slot, cache, st["pt_offsets"],
+            rrender._DUMMY_U8_2D, rrender._DUMMY_U8_2D, 0, rrender._DUMMY_I64,
+            0, rrender._DUMMY_I8, rrender._DUMMY_I32, rrender._DUMMY_CACHE,
+            image, breq, bn, mreq, mn,
+            np.zeros(E, dtype=np.uint8), np.zeros(words.shape[0] * m, dtype=np.uint8),
+            required, pixr, hist, counters)
+        assert bn[0] < cap and mn[0] < cap
+        return {"image": image.reshape(b - a, w, 4), "bricks": breq[:bn[0]].copy(),
+                "metas": mreq[:mn[0]].copy(), "required": required, "pix_required": pixr,
+                "hist": hist, "counters": counters}
+
+    bands = [(300, 302), (536, 538), (760, 762)]
+    full = [band(a, b, st["pt_status"], st["pt_slot"], st["cache"]) for a, b in bands]
+    # compact cache: sampled bricks get slots 1.., every other resident one
+    # slot 0; voxels no trilinear fetch of the bands reads are zeroed (found
+    # with the C oracle's read tracking, then the REFERENCE re-renders the
+    # bands from the compacted state below: identical outputs prove the
+    # dropped bytes never mattered)
+    sampled = np.flatnonzero(np.bitwise_or.reduce([r["required"] for r in full]))
+    assert (st["pt_status"][sampled] == 1).all()
+    old = st["pt_slot"][sampled]
+    import oracle
+    from oracle import raycast as orc
+    oracle.build()
+    ost = orc.OracleState(**st)
+    och = [orc.OracleChannel(slot=c.slot, points=c.tf.points, level_range=c.level_range)
+           for c in scn.channels]
+    touched = np.zeros(st["cache"].shape, dtype=np.uint8)
+    for a, b in bands:
+        orc.render(ost, och, (cam.position, cam.target, cam.up, cam.fov_deg), (w, hgt),
+                   cfg.base_step, t0=cfg.lod_reference_distance,
+                   early_alpha=cfg.early_term_alpha, budget=1 << 16,
+                   start_level=cfg.traversal_start_level, rows=(a, b), touched=touched)
+    cache = np.zeros((len(sampled) + 1,) + st["cache"].shape[1:], dtype=np.uint8)
+    cache[1:] = st["cache"][old] * touched[old]
+    pt_slot = np.where(st["pt_status"] == 1, 0, -1).astype(np.int32)
+    pt_slot[sampled] = np.arange(1, len(sampled) + 1, dtype=np.int32)
+    rec = {"pt_status": st["pt_status"], "pt_slot": pt_slot, "cache": cache, "words": words,
+           "level_dims": dims, "level_grids": grids, "pt_offsets": st["pt_offsets"]}
+    for i, ((a, b), r) in enumerate(zip(bands, full)):
+        again = band(a, b, st["pt_status"], pt_slot, cache)
+        for key in r:
+            assert np.array_equal(again[key], r[key]), (key, a)
+        for key in ("image", "bricks", "metas", "pix_required", "hist", "counters"):
+            rec[f"b{i}_{key}"] = r[key]
+        rec[f"b{i}_required"] = np.flatnonzero(r["required"]).astype(np.int32)
+    meta = {"scene": "scenarios.cycif(device='cpu'): config 2 recipe, torch CPU generator",
+            "bands": bands, "image": [w, hgt], "depth": D, "k": k, "m": m, "eps_h": st["eps_h"],
+            "brick_size": list(st["brick_size"]),
+            "camera": {"position": list(cam.position), "target": list(cam.target),
+                       "up": list(cam.up), "fov_deg": cam.fov_deg},
+            "render": {"base_step": cfg.base_step, "t0": cfg.lod_reference_distance,
+                       "early_alpha": cfg.early_term_alpha,
+                       "start_level": cfg.traversal_start_level},
+            "channels": [{"slot": c.slot, "tf": tf_points(c.tf),
+                          "level_range": list(c.level_range)} for c in scn.channels],
+            "resident_bricks": int(len(scn.brick_ids)), "sampled_bricks": int(len(sampled)),
+            "state_sha": {"words": h(words), "pt_status": h(st["pt_status"]),
+                          "cache_full": h(st["cache"])}}
+    return meta, rec
+
+
 def main():
     tmp = tempfile.mkdtemp()
     only = set(sys.argv[1:])
@@ -531,7 +650,8 @@ def main():
                      ("baselines_sparse256x4", lambda: baselines_sparse256x4(tmp)),
                      ("baselines_vessel256", baselines_vessel256),
                      ("lz4_frames", lz4_frames),
-                     ("tf_queries", tf_queries)):
+                     ("tf_queries", tf_queries),
+                     ("config2_bands", config2_bands)):
         if only and name not in only:
             continue
         print("generating", name, flush=True)

@@ -615,6 +615,41 @@ def test_gpu_config2_full_size_properties():
         out.stats.samples_evaluated + out.stats.samples_skipped
 
 
+@pytest.mark.parametrize("budget", [256, 65536])
+def test_gpu_config2_full_frame_matches_oracle(budget):
+    """BASELINE config 2 at full size, the WHOLE 1920x1080 frame against the
+    C oracle (the reference's algorithm, pinned to reference-generated
+    fixtures at this k = 7 / D = 6 scale by tests/test_oracle_golden.py):
+    image, ordered brick and metadata request lists, usage mask, level
+    histogram, per-pixel brick switches and work counters bit-exact.  With
+    budget 65536 every touched entry is emitted, so the complete first-seen
+    order is compared (and the feedback kernel sorts in several chunks)."""
+    import dataclasses
+    import os
+    from oracle import raycast as orc
+    from paper_2309_04393_b200 import render_frame, scenarios
+    scn = scenarios.cycif(device="cuda")
+    eng = scenarios.build_engine(scn)
+    cfg = dataclasses.replace(scn.render, max_requests_per_frame=budget)
+    out = render_frame(eng.paging, eng.octree, scn.channels, scn.camera, cfg)
+    ref = orc.OracleState(**scenarios.reference_state(scn))
+    och = [orc.OracleChannel(slot=c.slot, points=c.tf.points, level_range=c.level_range)
+           for c in scn.channels]
+    o = orc.render(ref, och, cam_tuple(scn.camera), cfg.image_dims, cfg.base_step,
+                   budget=budget, threads=os.cpu_count() or 1)
+    assert np.array_equal(out.image, o.image)
+    assert out.brick_requests == o.brick_requests
+    assert out.metadata_requests == o.metadata_requests
+    assert np.array_equal(out.required_mask, o.required_mask)
+    assert np.array_equal(out.level_histogram, o.level_histogram)
+    assert np.array_equal(out.pixel_required.reshape(-1), o.pixel_required.reshape(-1))
+    assert [out.stats.traversal_steps, out.stats.samples_evaluated,
+            out.stats.samples_skipped, out.stats.livelocked_rays] == \
+        [int(o.counters[0]), int(o.counters[1]), int(o.counters[2]), int(o.counters[4])]
+    if budget > 256:
+        assert len(out.brick_requests) > 256  # the complete order, not just a prefix
+
+
 def test_gpu_capacity_mode_parts_converge_to_single_gpu_image():
     """Sort-first capacity mode: two part sessions, each
     with its own cache / LRU / octree fed only by its own rows' requests,

@@ -277,3 +277,42 @@ def test_oracle_baselines_vessel256_match_reference(oracle_lib):
             if mode == orc.MODE_PAGETABLE:
                 skipped += int(out.counters[2])
     assert skipped > 0  # the EMPTY brick-exit skip was exercised
+
+
+def test_oracle_config2_bands_match_reference(oracle_lib):
+    """BASELINE config 2 at its benchmarked scale (k = 7, D = 6, 4 of 16
+    CyCIF-like 2048x2048x128 channels, partial residency with coarser-LOD
+    substitution, 1080p): row bands rendered by the reference's own kernel
+    (tests/golden/make_golden.py config2_bands) -- image rows, complete
+    ordered brick / metadata request lists, usage mask, histogram, per-pixel
+    brick switches and counters -- equal the C oracle's, which the GPU test
+    test_gpu_config2_full_frame_matches_oracle holds the CUDA kernel to over
+    the whole frame."""
+    import os
+    from oracle import raycast as orc
+    meta, rec = load_golden("config2_bands")
+    st = orc.OracleState(m=meta["m"], k=meta["k"], brick_size=tuple(meta["brick_size"]),
+                         level_dims=rec["level_dims"], level_grids=rec["level_grids"],
+                         pt_offsets=rec["pt_offsets"], pt_status=rec["pt_status"],
+                         pt_slot=rec["pt_slot"], cache=rec["cache"], words=rec["words"],
+                         depth=meta["depth"], eps_h=meta["eps_h"])
+    chans = [orc.OracleChannel(slot=c["slot"],
+                               points=tuple((x, tuple(v)) for x, v in c["tf"]),
+                               level_range=tuple(c["level_range"])) for c in meta["channels"]]
+    cam = meta["camera"]
+    r = meta["render"]
+    w, hh = meta["image"]
+    m = meta["m"]
+    for i, (a, b) in enumerate(meta["bands"]):
+        o = orc.render(st, chans, (tuple(cam["position"]), tuple(cam["target"]),
+                                   tuple(cam["up"]), cam["fov_deg"]), (w, hh), r["base_step"],
+                       t0=r["t0"], early_alpha=r["early_alpha"], budget=1 << 16,
+                       start_level=r["start_level"], rows=(a, b), threads=os.cpu_count() or 1)
+        assert np.array_equal(o.image[a:b], rec[f"b{i}_image"]), a
+        assert o.brick_requests == rec[f"b{i}_bricks"].tolist(), a
+        assert o.metadata_requests == [divmod(int(v), m) for v in rec[f"b{i}_metas"]], a
+        assert np.array_equal(np.flatnonzero(o.required_mask), rec[f"b{i}_required"]), a
+        assert np.array_equal(o.level_histogram, rec[f"b{i}_hist"]), a
+        assert np.array_equal(o.pixel_required.reshape(-1)[a * w:b * w], rec[f"b{i}_pix_required"])
+        assert np.array_equal(o.counters[:4], rec[f"b{i}_counters"]), a
+        assert len(rec[f"b{i}_bricks"]) > 0 or len(rec[f"b{i}_metas"]) > 0

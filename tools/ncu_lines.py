@@ -70,3 +70,15 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+def dump_sass(rep, path):
+    """Every SASS instruction of the report with its CUDA line, stall samples
+    and executed count, in address order."""
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source",
+                          "sass"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    with open(path, "w") as f:
+        for r in rows:
+            if len(r) > 8 and r[0].startswith("0x"):
+                f.write(f"{r[0][-5:]} {int(r[2]):7d} {int(r[5]):11d}  {r[1]}\n")
