@@ -536,7 +536,14 @@ __host__ __device__ constexpr int ilog2c(int v) { return v > 1 ? 1 + ilog2c(v >>
 // BX / BY / BZ: compile-time brick extent (0: runtime) -- tap offsets, brick
 // and sub-block coordinates then use constant shifts and masks
 template <int MODE, bool CHECK, int BX, int BY, int BZ>
-__global__ void __launch_bounds__(kBlock, RO_MINB * 4 / kWarps)
+#ifndef RO_CTAS_PER_SM
+#define RO_CTAS_PER_SM (RO_MINB * 4 / kWarps)
+#endif
+#ifdef RO_MAXNREG  // experiment knob: an explicit register cap instead of a CTA count
+__global__ void __maxnreg__(RO_MAXNREG)
+#else
+__global__ void __launch_bounds__(kBlock, RO_CTAS_PER_SM)
+#endif
 k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A) {
     __shared__ FrameSmem S;
     extern __shared__ int32_t dyn[];  // per-thread channel state
