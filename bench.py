@@ -362,14 +362,15 @@ def run_ours(args):
         fp.render()
         if events:
             events[1].record(stream)
-        fp.collect()
+        fp.collect(asynchronous=world > 1)
         if world > 1:
             from paper_2309_04393_b200.distributed import exchange
             b = fp.buf
             return exchange(dict(image=b.image, required=b.required,
                                  pix_required=b.pix_required, hist=b.hist,
-                                 counters=b.counters, fb=b.fb, counts=b.counts),
-                            cfg.image_dims, 8, cfg.max_requests_per_frame, m)
+                                 counters=b.counters, fb=b.fb, counts_dev=b.counts_dev),
+                            cfg.image_dims, 8, cfg.max_requests_per_frame, m,
+                            paging=eng.paging)
         return None
 
     for i in range(args.warmup):
@@ -453,12 +454,13 @@ def run_ours(args):
             else:
                 fp = passes[i % len(passes)]
                 fp.render()
-                fp.collect()
+                fp.collect(asynchronous=True)
                 b = fp.buf
                 res = _exchange(dict(image=b.image, required=b.required,
                                      pix_required=b.pix_required, hist=b.hist,
-                                     counters=b.counters, fb=b.fb, counts=b.counts),
-                                cfg.image_dims, 8, cfg.max_requests_per_frame, m)
+                                     counters=b.counters, fb=b.fb, counts_dev=b.counts_dev),
+                                cfg.image_dims, 8, cfg.max_requests_per_frame, m,
+                                paging=eng.paging)
                 if rank == 0:
                     pin_img.copy_(res["image"], non_blocking=True)
             torch.cuda.synchronize()

@@ -273,6 +273,23 @@ int ro_feedback_collect(ro_ctx *ctx, int64_t budget, int32_t bricks_first,
 int ro_note_sampled(ro_ctx *ctx, const ro_state *state,
                     const uint8_t *required, int64_t frame, void *stream);
 
+/* Sort-first request merge: n_parts parts' ordered
+   request blocks -- blocks[p] = the 4 x budget ro_feedback arrays
+   (brick keys, brick ids, meta keys, meta ids) of part p, counts[p] its
+   ro_feedback counts ([2] bricks, [3] metas emitted), all DEVICE -- are
+   folded into this context's first-seen key arrays (smallest key per
+   entry wins); a following ro_feedback_collect(bricks_first = 1) returns
+   exactly the lists of one full-frame pass.  Asynchronous. */
+int ro_feedback_merge(ro_ctx *ctx, const int64_t *blocks, const int64_t *counts,
+                      int32_t n_parts, int64_t budget, void *stream);
+
+/* Sort-first image assembly: parts [n_parts][part_stride floats] (part p's
+   local RGBA rows, ro_frame partition layout) -> full [height][width][4],
+   DEVICE buffers, 16-byte aligned.  Asynchronous. */
+int ro_gather_rows(const float *parts, int32_t n_parts, int64_t part_stride,
+                   int32_t height, int32_t width, int32_t tile_rows, float *full,
+                   void *stream);
+
 /* Insert n bricks in order.  ids: HOST array.  payloads: n*brick bytes on the
    host (payload_on_device=0) or device (=1).  Host payloads in page-locked
    memory (cudaHostAlloc / torch pin_memory) are DMA'd straight from the

@@ -121,6 +121,8 @@ _SIGS = {
     "ro_render": ([_p, C.POINTER(Frame), C.POINTER(State), C.POINTER(Outputs), _p], _i32),
     "ro_feedback_collect": ([_p, _i64, _i32, C.POINTER(Feedback), _p], _i32),
     "ro_note_sampled": ([_p, C.POINTER(State), _p, _i64, _p], _i32),
+    "ro_feedback_merge": ([_p, _p, _p, _i32, _i64, _p], _i32),
+    "ro_gather_rows": ([_p, _i32, _i64, _i32, _i32, _i32, _p, _p], _i32),
     "ro_apply_bricks": ([_p, C.POINTER(State), _p, _i64, _p, _i32, _i64, _i32, _p, _p, _p], _i32),
     "ro_evict_bricks": ([_p, C.POINTER(State), _p, _i64, _i32, _p], _i32),
     "ro_mark_empty": ([_p, C.POINTER(State), _p, _i64, _p], _i32),

@@ -51,6 +51,10 @@ int feedback_collect(ro_ctx *c, int64_t budget, int32_t bricks_first,
                      const ro_feedback *fb, cudaStream_t s);
 int note_sampled(ro_ctx *c, const ro_state *st, const uint8_t *required,
                  int64_t frame, cudaStream_t s);
+int feedback_merge(ro_ctx *c, const int64_t *blocks, const int64_t *counts, int32_t n_parts,
+                   int64_t budget, cudaStream_t s);
+int gather_rows(const float *parts, int32_t n_parts, int64_t part_stride, int32_t height,
+                int32_t width, int32_t tile_rows, float *full, cudaStream_t s);
 int apply_bricks(ro_ctx *c, const ro_state *st, const int64_t *ids_h, int64_t n,
                  const void *payloads, int32_t on_device, int64_t frame,
                  int32_t update_octree, int32_t *slots_out, int64_t *evicted_out,
@@ -228,6 +232,22 @@ int ro_feedback_collect(ro_ctx *c, int64_t budget, int32_t bricks_first,
     if (budget > 0 && (!fb->brick_keys || !fb->brick_ids || !fb->meta_keys || !fb->meta_ids))
         return fail(RO_EINVAL, "null feedback buffer");
     return feedback_collect(c, budget, bricks_first, fb, (cudaStream_t)stream);
+}
+
+int ro_feedback_merge(ro_ctx *c, const int64_t *blocks, const int64_t *counts,
+                      int32_t n_parts, int64_t budget, void *stream) {
+    if (!c) return fail(RO_EINVAL, "null context");
+    if (budget > 0 && (!blocks || !counts)) return fail(RO_EINVAL, "null request blocks");
+    return feedback_merge(c, blocks, counts, n_parts, budget, (cudaStream_t)stream);
+}
+
+int ro_gather_rows(const float *parts, int32_t n_parts, int64_t part_stride, int32_t height,
+                   int32_t width, int32_t tile_rows, float *full, void *stream) {
+    if (!parts || !full) return fail(RO_EINVAL, "null image");
+    if (n_parts < 1 || tile_rows < 1 || height < 1 || width < 1)
+        return fail(RO_EINVAL, "bad partition");
+    return gather_rows(parts, n_parts, part_stride, height, width, tile_rows, full,
+                       (cudaStream_t)stream);
 }
 
 int ro_note_sampled(ro_ctx *c, const ro_state *st, const uint8_t *required, int64_t frame,

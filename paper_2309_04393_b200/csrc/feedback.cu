@@ -206,6 +206,36 @@ __global__ void __launch_bounds__(kFbThreads, 1) k_feedback(const __grid_constan
     }
 }
 
+// Sort-first merge: every part's ordered (key, id) lists
+// -- each already cut to the budget, which keeps every entry of the global
+// first `budget` -- are scattered back into the first-seen key arrays with
+// the ray caster's own RED.MIN rule (the smallest key of an entry wins);
+// ro_feedback_collect then orders them exactly like one full-frame pass.
+__global__ void k_merge_requests(const DevLayout L, int32_t n_parts, int64_t budget,
+                                 const int64_t *__restrict__ blocks,  // [n_parts][4][budget]
+                                 const int64_t *__restrict__ counts,  // [n_parts][4]
+                                 unsigned long long *__restrict__ bkeys,
+                                 unsigned long long *__restrict__ mkeys) {
+    const int64_t per = 2 * budget;  // brick slots then meta slots of one part
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n_parts * per;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t p = (int32_t)(j / per);
+        const int64_t r = j - p * per;
+        const bool meta = r >= budget;
+        const int64_t i = meta ? r - budget : r;
+        if (i >= counts[p * 4 + (meta ? 3 : 2)]) continue;
+        const int64_t *blk = blocks + (int64_t)p * 4 * budget;
+        const unsigned long long key = (unsigned long long)blk[(meta ? 2 : 0) * budget + i];
+        const int64_t id = blk[(meta ? 3 : 1) * budget + i];
+        if (meta) {
+            atomicMin(mkeys + id, key);
+        } else {
+            const Decoded d = decode_id(L, id);
+            if (d.ok) atomicMin(bkeys + entry_index(L, d.slot, d.lev, d.x, d.y, d.z), key);
+        }
+    }
+}
+
 // engine.py:72-81: every sampled entry that is MAPPED stamps its slot
 __global__ void k_note_sampled(const uint8_t *__restrict__ required,
                                const int32_t *__restrict__ pt, int64_t E,
@@ -276,6 +306,23 @@ int feedback_collect(ro_ctx *c, int64_t budget, int32_t bricks_first,
         RO_CUDA(cudaStreamSynchronize(s));
         for (int i = 0; i < 4; ++i) fb->counts[i] = h[i];
     }
+    return RO_OK;
+}
+
+int feedback_merge(ro_ctx *c, const int64_t *blocks, const int64_t *counts, int32_t n_parts,
+                   int64_t budget, cudaStream_t s) {
+    if (n_parts < 1 || budget < 0) return fail(RO_EINVAL, "bad part count / budget");
+    if (budget == 0) return RO_OK;
+    if (!meta_keys(c)) {
+        int rc = ensure_meta_keys(c);
+        if (rc) return rc;
+    }
+    const int64_t total = 2 * budget * n_parts;
+    int64_t blocks_n = (total + 255) / 256;
+    if (blocks_n > 148 * 8) blocks_n = 148 * 8;
+    k_merge_requests<<<(unsigned)blocks_n, 256, 0, s>>>(c->dl, n_parts, budget, blocks, counts,
+                                                        brick_keys(c), meta_keys(c));
+    RO_CUDA(cudaGetLastError());
     return RO_OK;
 }
 

@@ -278,6 +278,9 @@ __device__ __forceinline__ void request(unsigned long long *keys, int32_t *, int
 #ifndef RO_LEAF_CACHE
 #define RO_LEAF_CACHE 0
 #endif
+#ifndef RO_LOD_INC
+#define RO_LOD_INC 1
+#endif
 #ifndef RO_LP2_LOCAL
 #define RO_LP2_LOCAL 0
 #endif
@@ -341,6 +344,14 @@ __device__ __forceinline__ uint4 ld_meta4(const uint4 *p) {
 #else
     return __ldg(p);
 #endif
+}
+
+// word of channel slot s (0..3) from a node's four-slot vector: two
+// predicated selects, no branch chain
+__device__ __forceinline__ uint32_t word_of_slot(const uint4 &wv, int s) {
+    const uint32_t lo = (s & 1) ? wv.y : wv.x;
+    const uint32_t hi = (s & 1) ? wv.w : wv.z;
+    return (s & 2) ? hi : lo;
 }
 
 // kernels.py:518-549: nearest resident level in the node's mask, coarser
@@ -705,6 +716,12 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
     int stall = 0;
     uint32_t ev = 0;  // request event index within this pixel
     int32_t pixreq = 0;
+#if RO_LOD_INC
+    // t only grows along the ray, so the raw LOD level only grows: it is
+    // recomputed when t / t0 reaches the next level's threshold
+    int raw_c = 0;
+    double next_thr = -1.0;
+#endif
 #if RO_LEAF_CACHE
     // the last node word vector / class read by this ray (frame-constant
     // state: reusable by the next sample in the same node)
@@ -727,7 +744,18 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
             if (py > kClampHi) py = kClampHi;
             if (pz > kClampHi) pz = kClampHi;
 
+#if RO_LOD_INC
+            {
+                const double ratio = S.t0_pow2 ? t * S.inv_t0 : t / t0;
+                if (ratio >= next_thr) {
+                    raw_c = lod_raw(t, t0, S.inv_t0, S.t0_pow2, S);
+                    next_thr = S.lod_thr[raw_c + 1];
+                }
+            }
+            const int raw = raw_c;
+#else
             const int raw = lod_raw(t, t0, S.inv_t0, S.t0_pow2, S);
+#endif
             double step = S.step_tab[raw];
             int jexp = S.maxlev[raw];
             const int dt_ = S.dt_tab[raw];
@@ -1076,7 +1104,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                     const int slot = chc.x;
                     uint32_t mask;
                     if (fast) {
-                        mask = (vec4 ? (slot == 0 ? wv.x : slot == 1 ? wv.y : slot == 2 ? wv.z : wv.w)
+                        mask = (vec4 ? word_of_slot(wv, slot)
                                      : __ldg(A.words + cur_node * m + slot)) & 0xFFFFu;
                     } else {
                     bool probe = false;
@@ -1094,7 +1122,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                                 wv = ld_meta4(reinterpret_cast<const uint4 *>(A.words) + nidx);
                                 cur_node = nidx;
                             }
-                            w = slot == 0 ? wv.x : slot == 1 ? wv.y : slot == 2 ? wv.z : wv.w;
+                            w = word_of_slot(wv, slot);
                         } else {
                             RO_ASSERT(nidx >= 0 && nidx < A.L.num_nodes);
                             w = __ldg(A.words + nidx * m + slot);
@@ -1301,6 +1329,11 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
     }  // packets of the tile
     }  // tile loop
 
+    // parts writing another GPU's buffers (sort-first over peer memory):
+    // their stores / atomics are flushed to the owner before the kernel's
+    // completion is signalled to any other rank
+    if (F.shared_outputs) __threadfence_system();
+
     // ---- block reductions ----
 #if RO_STATS
     unsigned long long vals[8] = {c_steps, c_eval, c_skip, c_viol, c_live, c_s5, c_s6, c_s7};
@@ -1367,6 +1400,37 @@ cudaError_t launch(const ro_frame &F, const RayArgs &A, cudaStream_t s) {
 }
 
 }  // namespace
+
+// Sort-first image assembly: part p's local rows are the row blocks
+// b = p, p + n, p + 2n, ... of tile_rows rows (ro_frame.n_parts/part/tile_rows);
+// parts [n_parts][part_stride floats] -> full [height][width][4].
+__global__ void k_gather_rows(const float4 *__restrict__ parts, int32_t n_parts,
+                              int64_t part_stride4, int32_t height, int32_t width,
+                              int32_t tile_rows, float4 *__restrict__ full) {
+    const int64_t total = (int64_t)height * width;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t y = (int32_t)(i / width), x = (int32_t)(i - (int64_t)y * width);
+        const int32_t b = y / tile_rows, p = b % n_parts;
+        const int64_t ly = (int64_t)(b / n_parts) * tile_rows + (y - b * tile_rows);
+        full[i] = parts[p * part_stride4 + ly * width + x];
+    }
+}
+
+int gather_rows(const float *parts, int32_t n_parts, int64_t part_stride, int32_t height,
+                int32_t width, int32_t tile_rows, float *full, cudaStream_t s) {
+    if (part_stride % 4 || (reinterpret_cast<uintptr_t>(parts) & 15) ||
+        (reinterpret_cast<uintptr_t>(full) & 15))
+        return fail(RO_EINVAL, "image buffers must be 16-byte aligned RGBA");
+    const int64_t total = (int64_t)height * width;
+    int64_t blocks = (total + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    k_gather_rows<<<(unsigned)blocks, 256, 0, s>>>(reinterpret_cast<const float4 *>(parts),
+                                                    n_parts, part_stride / 4, height, width,
+                                                    tile_rows, reinterpret_cast<float4 *>(full));
+    RO_CUDA(cudaGetLastError());
+    return RO_OK;
+}
 
 int render(ro_ctx *c, const ro_frame *F, const ro_state *st,
            const ro_outputs *out, cudaStream_t s) {

@@ -45,6 +45,18 @@ def _np(x):
     return np.asarray(x)
 
 
+def _gather_stacked(x: torch.Tensor) -> torch.Tensor:
+    """All-gather into one (world, *x.shape) tensor (a single NCCL
+    all-gather; per-rank views for other backends)."""
+    world = dist.get_world_size()
+    out = torch.empty((world,) + tuple(x.shape), dtype=x.dtype, device=x.device)
+    if dist.get_backend() == "nccl":
+        dist.all_gather_into_tensor(out, x.contiguous())
+    else:
+        dist.all_gather(list(out.unbind(0)), x.contiguous())
+    return out
+
+
 def merge_feedback(key_id_lists, budget: int, m: int):
     """key_id_lists: [(bkeys, bids, mkeys, mids)] per part (numpy).
 
@@ -100,13 +112,20 @@ def merge_parts(parts, image_dims, n_parts, tile_rows, budget, m) -> dict:
 
 
 def exchange(local: dict, image_dims, tile_rows: int, budget: int, m: int,
-             gather_image: bool = True) -> dict:
+             gather_image: bool = True, paging=None) -> dict:
     """One frame's collective step; every rank returns the merged feedback,
     rank 0 also the assembled image.
 
     local: image (local_rows*w, 4), required (E,) u8, pix_required, hist,
     counters (tensors on this rank's device), fb (4, budget) i64 tensor,
-    counts (4,) host array."""
+    counts (4,) host array (or counts_dev, a (4,) device tensor).
+
+    With ``paging`` (a GPU replica) the whole step stays on the device:
+    the gathered request blocks are folded into the replica's first-seen
+    key arrays (ro_feedback_merge) and ordered by ro_feedback_collect, and
+    the image is assembled by ro_gather_rows -- no host round trip until
+    the caller reads the lists.  Without it (CPU / gloo checks) the same
+    merge runs on the host (merge_feedback)."""
     world = dist.get_world_size()
     rank = dist.get_rank()
     w, h = image_dims
@@ -120,18 +139,36 @@ def exchange(local: dict, image_dims, tile_rows: int, budget: int, m: int,
     dist.all_reduce(counters)
     # request lists: fixed-size (4, budget) blocks + counts
     fb = local["fb"].contiguous()
-    counts = torch.as_tensor(np.asarray(local["counts"], dtype=np.int64), device=dev)
-    fbs = [torch.empty_like(fb) for _ in range(world)]
-    cts = [torch.empty_like(counts) for _ in range(world)]
-    dist.all_gather(fbs, fb)
-    dist.all_gather(cts, counts)
-    lists = []
-    for f, c in zip(fbs, cts):
-        f = f.cpu().numpy()
-        c = c.cpu().numpy()
-        nb, nm = int(c[2]), int(c[3])
-        lists.append((f[0][:nb], f[1][:nb], f[2][:nm], f[3][:nm]))
-    bricks, metas = merge_feedback(lists, budget, m)
+    if local.get("counts_dev") is not None:
+        counts = local["counts_dev"].contiguous()
+    else:
+        counts = torch.as_tensor(np.asarray(local["counts"], dtype=np.int64), device=dev)
+    fbs = _gather_stacked(fb)
+    cts = _gather_stacked(counts)
+    if paging is not None:
+        from . import _native as N
+        import ctypes as C
+        merged = torch.zeros((4, max(budget, 1)), dtype=torch.int64, device=dev)
+        mcounts = torch.zeros(4, dtype=torch.int64, device=dev)
+        N.check(N.lib().ro_feedback_merge(paging.ctx, fbs.data_ptr(), cts.data_ptr(), world,
+                                          budget, N.stream_ptr()))
+        fbd = N.Feedback(merged[0].data_ptr(), merged[1].data_ptr(), merged[2].data_ptr(),
+                         merged[3].data_ptr(), None, mcounts.data_ptr())
+        N.check(N.lib().ro_feedback_collect(paging.ctx, budget, 1, C.byref(fbd),
+                                            N.stream_ptr()))
+        host = torch.cat([mcounts, merged.reshape(-1)]).cpu().numpy()  # one read-back
+        nb, nm = int(host[2]), int(host[3])
+        blk = host[4:].reshape(4, -1)
+        bricks = [int(v) for v in blk[1][:nb]]
+        metas = [(int(v) // m, int(v) % m) for v in blk[3][:nm]]
+    else:
+        lists = []
+        for f, c in zip(fbs, cts):
+            f = f.cpu().numpy()
+            c = c.cpu().numpy()
+            nb, nm = int(c[2]), int(c[3])
+            lists.append((f[0][:nb], f[1][:nb], f[2][:nm], f[3][:nm]))
+        bricks, metas = merge_feedback(lists, budget, m)
     out = dict(bricks=bricks, metas=metas, required=required, hist=hist,
                counters=counters)
     if gather_image:
@@ -149,10 +186,16 @@ def exchange(local: dict, image_dims, tile_rows: int, budget: int, m: int,
             dist.all_gather(parts, img)
         if rank == 0:
             full = torch.empty((h, w, 4), dtype=torch.float32, device=dev)
-            for p in range(world):
-                rows = part_rows(h, world, p, tile_rows)
-                idx = torch.as_tensor(rows, device=dev, dtype=torch.long)
-                full.index_copy_(0, idx, parts[p][:len(rows) * w].reshape(len(rows), w, 4))
+            if paging is not None:
+                from . import _native as N
+                stacked = torch.stack(parts)
+                N.check(N.lib().ro_gather_rows(stacked.data_ptr(), world, max_rows * w * 4, h, w,
+                                               tile_rows, full.data_ptr(), N.stream_ptr()))
+            else:
+                for p in range(world):
+                    rows = part_rows(h, world, p, tile_rows)
+                    idx = torch.as_tensor(rows, device=dev, dtype=torch.long)
+                    full.index_copy_(0, idx, parts[p][:len(rows) * w].reshape(len(rows), w, 4))
             out["image"] = full
     return out
 
@@ -241,6 +284,8 @@ class PeerFrame:
             with torch.cuda.device(dev):   # this rank's kernels reach the owner's GPU
                 N.check(N.lib().ro_enable_peer_access(owner_dev))
         self.bufs = bufs
+        self.nccl = dist.get_backend() == "nccl"
+        self._tok = torch.zeros(1, dtype=torch.int32, device=dev if self.nccl else "cpu")
         N.check(N.lib().ro_set_feedback_buffers(paging.ctx, bufs["bkeys"].data_ptr(),
                                                 bufs["mkeys"].data_ptr()))
         self.outputs = N.Outputs(bufs["image"].data_ptr(), bufs["required"].data_ptr(),
@@ -250,38 +295,59 @@ class PeerFrame:
         # meet the others at the caller's next collective (bench.py agrees on
         # peer vs NCCL exchange with one all-reduce)
 
+    def _token(self):
+        """A rank-wide rendezvous.  NCCL: a one-element all-reduce on the
+        current stream -- every later launch on this stream is ordered after
+        every rank reached it, without blocking the host.  Other backends
+        (the one-GPU gloo check): the host waits for the stream, then meets
+        the other ranks."""
+        if self.nccl:
+            dist.all_reduce(self._tok)
+        else:
+            torch.cuda.current_stream().synchronize()
+            dist.all_reduce(self._tok)
+
     def frame(self, fp, budget: int, m: int, events=None):
         """One sort-first frame: ``fp`` is this rank's FramePass (its
         partition set, bricks_first=True).  Returns (bricks, metas) on every
         rank; the full-frame image / usage / histogram / counters are
         ``self.bufs`` (complete on every rank after the call, valid until the
-        next ``frame`` call, which first waits for every rank)."""
+        next ``frame`` call).
+
+        Stream-ordered (NCCL): owner clears the accumulators -> token ->
+        every part ray-casts into the owner's buffers -> token -> owner
+        orders the requests on the device -> the ordered block (<= budget
+        entries + counts) is broadcast -> one host read.  The host waits
+        once per frame, for the lists it must return."""
         N = self.N
         stream = torch.cuda.current_stream()
-        dist.barrier()                     # every rank is done with the previous frame's buffers
         if self.rank == 0:
             for n in ("required", "hist", "counters"):
                 self.bufs[n].zero_()
-            stream.synchronize()
-        dist.barrier()                     # accumulators clear before any part writes
+        # (the previous frame's broadcast already ordered every rank's
+        # previous render before this clear)
+        self._token()                      # accumulators clear before any part writes
         fp.frame.shared_outputs = 1
         if events:
             events[0].record(stream)
         fp.render(self.outputs)
         if events:
             events[1].record(stream)
-        stream.synchronize()
-        dist.barrier()                     # every part's writes / atomics landed
-        lists = [None]
+        self._token()                      # every part's writes / atomics landed
+        b = fp.buf
         if self.rank == 0:
-            fp.collect()                   # owner's keys hold every part's requests
-            b = fp.buf
-            nb, nm = b.n_bricks, b.n_metas
-            fb = b.fb.cpu().numpy()
-            lists = [([int(v) for v in fb[1][:nb]],
-                      [(int(v) // m, int(v) % m) for v in fb[3][:nm]])]
-        dist.broadcast_object_list(lists, src=0)
-        return lists[0]
+            fp.collect(asynchronous=True)  # owner's keys hold every part's requests
+        block = b.small[b.hist.numel() + b.counters.numel():]   # lists + counts
+        if self.nccl:
+            dist.broadcast(block, src=0)
+            host = block.cpu().numpy()
+        else:
+            host_t = block.cpu()
+            dist.broadcast(host_t, src=0)
+            host = host_t.numpy()
+        nb, nm = int(host[-2]), int(host[-1])
+        fbh = host[:-4].reshape(4, -1)
+        return ([int(v) for v in fbh[1][:nb]], [(int(v) // m, int(v) % m) for v in fbh[3][:nm]])
 
     def close(self):
         self.N.check(self.N.lib().ro_set_feedback_buffers(self.paging.ctx, None, None))

@@ -324,6 +324,34 @@ def test_gpu_sort_first_parts_merge_to_full_frame(n_parts):
     assert merged["counters"][0] == full.stats.traversal_steps
     rows = sum(len(part_rows(cfg.image_dims[1], n_parts, p, 8)) for p in range(n_parts))
     assert rows == cfg.image_dims[1]
+    # the device form of the same merge (distributed.exchange with a GPU
+    # replica): ro_feedback_merge + ro_feedback_collect, ro_gather_rows
+    import ctypes as C
+    from paper_2309_04393_b200 import _native as N
+    budget = cfg.max_requests_per_frame
+    blocks = torch.stack([p["fb"] for p in parts]).contiguous()
+    counts = torch.as_tensor(np.stack([p["counts"] for p in parts]), device=blocks.device)
+    out = torch.zeros((4, budget), dtype=torch.int64, device=blocks.device)
+    cdev = torch.zeros(4, dtype=torch.int64, device=blocks.device)
+    N.check(N.lib().ro_feedback_merge(eng.paging.ctx, blocks.data_ptr(), counts.data_ptr(),
+                                      n_parts, budget, N.stream_ptr()))
+    fb = N.Feedback(out[0].data_ptr(), out[1].data_ptr(), out[2].data_ptr(), out[3].data_ptr(),
+                    None, cdev.data_ptr())
+    N.check(N.lib().ro_feedback_collect(eng.paging.ctx, budget, 1, C.byref(fb), N.stream_ptr()))
+    c = cdev.cpu().numpy()
+    o = out.cpu().numpy()
+    m = eng.paging.config.m
+    assert o[1][:c[2]].tolist() == full.brick_requests
+    assert [divmod(int(v), m) for v in o[3][:c[3]]] == full.metadata_requests
+    w, h = cfg.image_dims
+    max_rows = max(len(part_rows(h, n_parts, p, 8)) for p in range(n_parts))
+    stacked = torch.zeros((n_parts, max_rows * w, 4), dtype=torch.float32, device=blocks.device)
+    for i, p in enumerate(parts):
+        stacked[i, :p["image"].shape[0]] = p["image"]
+    img = torch.empty((h, w, 4), dtype=torch.float32, device=blocks.device)
+    N.check(N.lib().ro_gather_rows(stacked.data_ptr(), n_parts, max_rows * w * 4, h, w, 8,
+                                   img.data_ptr(), N.stream_ptr()))
+    assert np.array_equal(img.cpu().numpy(), full.image)
 
 
 def test_gpu_edge_cases():
