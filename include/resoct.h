@@ -162,8 +162,9 @@ typedef struct ro_frame {
     const uint8_t *cls_min;
     const uint8_t *cls_max;
     /* sort-first over peer memory: 1 = the outputs are the FULL frame's,
-       shared by every part (typically rank 0's buffers opened through
-       ro_ipc_open): image / pix_required are written at the pixel's global
+       shared by every part (typically rank 0's buffers, mapped into every
+       part's address space by the host -- CUDA IPC memory handles, see
+       distributed.PeerFrame): image / pix_required are written at the pixel's global
        row, and ro_render does not clear required / hist / counters (the
        owner clears them once per frame before any part renders). */
     int32_t shared_outputs;
@@ -252,6 +253,13 @@ int ro_tf_tables(int32_t n, const double *x, const double *rgba, double *first_s
 
 int ro_create(const ro_layout *layout, ro_ctx **out);
 int ro_destroy(ro_ctx *ctx);
+
+/* Pay every one-time cost ahead of the first frame: the request-ordering
+   and metadata-key arrays, the scratch and pinned staging of brick batches
+   up to max_batch bricks (0: none), and the loading of every kernel the
+   frame loop launches (CUDA loads kernels lazily).  Later calls only grow
+   buffers that are still too small.  Synchronises the device. */
+int ro_reserve(ro_ctx *ctx, int64_t max_batch);
 
 /* Row count this part renders for a (height, n_parts, part, tile_rows). */
 int64_t ro_local_rows(int32_t height, int32_t n_parts, int32_t part,

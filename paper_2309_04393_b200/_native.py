@@ -117,6 +117,7 @@ _SIGS = {
     "ro_last_error": ([], C.c_char_p),
     "ro_create": ([C.POINTER(Layout), C.POINTER(_p)], _i32),
     "ro_destroy": ([_p], _i32),
+    "ro_reserve": ([_p, _i64], _i32),
     "ro_local_rows": ([_i32, _i32, _i32, _i32], _i64),
     "ro_render": ([_p, C.POINTER(Frame), C.POINTER(State), C.POINTER(Outputs), _p], _i32),
     "ro_feedback_collect": ([_p, _i64, _i32, C.POINTER(Feedback), _p], _i32),

@@ -93,6 +93,9 @@ int fill_metadata(ro_ctx *c, const ro_state *st, int32_t slot, const uint8_t *vo
 int bricks_box_minmax(const uint8_t *bricks, const int32_t *boxes, int64_t n, int32_t bx,
                       int32_t by, int32_t bz, uint8_t *mins, uint8_t *maxs, cudaStream_t s);
 int rebuild_sub_max(ro_ctx *c, const ro_state *st, cudaStream_t s);
+int feedback_reserve(ro_ctx *c);
+int lru_reserve(ro_ctx *c, int64_t max_batch);
+int raycast_warm(ro_ctx *c);
 
 static int check_state(const ro_ctx *c, const ro_state *st) {
     if (!c) return fail(RO_EINVAL, "null context");
@@ -213,6 +216,17 @@ int ro_destroy(ro_ctx *c) {
     if (c->upload_done) cudaEventDestroy(c->upload_done);
     if (c->host_done) cudaEventDestroy(c->host_done);
     delete c;
+    return RO_OK;
+}
+
+int ro_reserve(ro_ctx *c, int64_t max_batch) {
+    if (!c) return fail(RO_EINVAL, "null context");
+    if (max_batch < 0) return fail(RO_EINVAL, "negative batch size");
+    int rc;
+    if ((rc = feedback_reserve(c))) return rc;
+    if ((rc = lru_reserve(c, max_batch))) return rc;
+    if ((rc = raycast_warm(c))) return rc;
+    RO_CUDA(cudaDeviceSynchronize());
     return RO_OK;
 }
 

@@ -297,6 +297,7 @@ int feedback_collect(ro_ctx *c, int64_t budget, int32_t bricks_first,
         grid = sms;  // one CTA per SM
     }
     RO_CUDA(cudaMemsetAsync(ctl, 0, sizeof(uint32_t) * kCtlWords, s));
+    c->keys_dirty = false;  // this pass resets every key it reads
     void *args[] = {&A};
     RO_CUDA(cudaLaunchCooperativeKernel((const void *)k_feedback, dim3(grid), dim3(kFbThreads),
                                         args, kFbSmem, s));
@@ -323,6 +324,25 @@ int feedback_merge(ro_ctx *c, const int64_t *blocks, const int64_t *counts, int3
     k_merge_requests<<<(unsigned)blocks_n, 256, 0, s>>>(c->dl, n_parts, budget, blocks, counts,
                                                         brick_keys(c), meta_keys(c));
     RO_CUDA(cudaGetLastError());
+    return RO_OK;
+}
+
+// one-time costs ahead of the first frame: key arrays, the compaction /
+// control scratch, the kernel's shared-memory attribute and module load
+int feedback_reserve(ro_ctx *c) {
+    int rc;
+    if (!c->meta_key && (rc = ensure_meta_keys(c))) return rc;
+    const int64_t n_meta = c->n_meta;
+    void *p;
+    if ((rc = scratch(c, 0, sizeof(unsigned long long) * (c->E + n_meta), &p))) return rc;
+    if ((rc = scratch(c, 2, sizeof(int32_t) * (c->E + n_meta), &p))) return rc;
+    if ((rc = scratch(c, 11, sizeof(uint32_t) * kCtlWords + sizeof(int64_t) * 8, &p))) return rc;
+    RO_CUDA(cudaFuncSetAttribute(k_feedback, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kFbSmem));
+    cudaFuncAttributes fa;
+    RO_CUDA(cudaFuncGetAttributes(&fa, k_feedback));
+    RO_CUDA(cudaFuncGetAttributes(&fa, k_note_sampled));
+    RO_CUDA(cudaFuncGetAttributes(&fa, k_merge_requests));
     return RO_OK;
 }
 

@@ -198,6 +198,9 @@ struct ro_ctx {
     // per-frame node classes of the ray caster's residency walk (raycast.cu
     // k_classify_nodes): [num_nodes] bytes, allocated with the context
     uint8_t *node_class = nullptr;
+    // a ray-cast pass left first-seen keys that no ro_feedback_collect has
+    // consumed (and reset) yet
+    bool keys_dirty = false;
 };
 
 namespace ro {

@@ -1432,6 +1432,31 @@ int gather_rows(const float *parts, int32_t n_parts, int64_t part_stride, int32_
     return RO_OK;
 }
 
+// load every ray-caster instantiation of this layout's brick size (CUDA
+// loads kernels lazily, at their first launch: a frame-one hitch otherwise)
+template <int BX, int BY, int BZ>
+int warm_b() {
+    const void *kernels[] = {
+        (const void *)k_raycast<RO_MODE_RESIDENCY, false, BX, BY, BZ>,
+        (const void *)k_raycast<RO_MODE_RESIDENCY, true, BX, BY, BZ>,
+        (const void *)k_raycast<RO_MODE_REFERENCE, false, BX, BY, BZ>,
+        (const void *)k_raycast<RO_MODE_PAGETABLE, false, BX, BY, BZ>,
+        (const void *)k_raycast<RO_MODE_CLASSIC, false, BX, BY, BZ>};
+    cudaFuncAttributes fa;
+    for (const void *k : kernels) RO_CUDA(cudaFuncGetAttributes(&fa, k));
+    return RO_OK;
+}
+
+int raycast_warm(ro_ctx *c) {
+    cudaFuncAttributes fa;
+    RO_CUDA(cudaFuncGetAttributes(&fa, k_classify_nodes));
+    RO_CUDA(cudaFuncGetAttributes(&fa, k_gather_rows));
+    const int *b = c->layout.brick;
+    if (b[0] == 32 && b[1] == 32 && b[2] == 32) return warm_b<32, 32, 32>();
+    if (b[0] == 16 && b[1] == 16 && b[2] == 16) return warm_b<16, 16, 16>();
+    return warm_b<0, 0, 0>();
+}
+
 int render(ro_ctx *c, const ro_frame *F, const ro_state *st,
            const ro_outputs *out, cudaStream_t s) {
     if (F->n_ch < 1 || F->n_ch > RO_MAX_CH) return fail(RO_EINVAL, "n_ch outside [1, 8]");
@@ -1522,6 +1547,15 @@ int render(ro_ctx *c, const ro_frame *F, const ro_state *st,
         RO_CUDA(cudaMemsetAsync(out->hist, 0, sizeof(int64_t) * F->n_ch * c->layout.k, s));
         RO_CUDA(cudaMemsetAsync(out->counters, 0, sizeof(int64_t) * RO_NUM_COUNTERS, s));
     }
+    // requests of an uncollected previous pass would leak into this frame's
+    // lists: reset the context's own key arrays first (caller-owned shared
+    // arrays are managed by their owner)
+    if (c->keys_dirty && !c->brick_key_ext) {
+        RO_CUDA(cudaMemsetAsync(c->brick_key, 0xFF, sizeof(unsigned long long) * c->E, s));
+        if (c->meta_key)
+            RO_CUDA(cudaMemsetAsync(c->meta_key, 0xFF, sizeof(unsigned long long) * c->n_meta, s));
+    }
+    c->keys_dirty = true;
     if (A.local_rows == 0) return RO_OK;
     RO_CUDA(cudaMemsetAsync(A.tile_counter, 0, sizeof(int32_t), s));
     if (F->mode == RO_MODE_RESIDENCY && c->node_class != nullptr && st->words != nullptr) {

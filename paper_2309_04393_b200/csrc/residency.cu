@@ -811,6 +811,46 @@ int apply_bricks(ro_ctx *c, const ro_state *st, const int64_t *ids_h, int64_t n6
     return RO_OK;
 }
 
+// one-time costs of batches up to max_batch bricks: the batch / LRU /
+// octree scratch, the payload upload slot, the pinned staging of pageable
+// payloads, and every kernel of this file loaded
+int lru_reserve(ro_ctx *c, int64_t max_batch) {
+    if (max_batch < 1) return RO_OK;
+    if (max_batch > (int64_t)1 << 30) return fail(RO_EINVAL, "batch too large");
+    const int64_t n = max_batch;
+    void *p;
+    int rc;
+    if ((rc = scratch(c, 1, sizeof(int64_t) * 4 * n + sizeof(int32_t) * n + n + 64, &p))) return rc;
+    if ((rc = scratch(c, 13, sizeof(uint32_t) * kLruCtlWords, &p))) return rc;
+    if ((rc = scratch(c, 6, sizeof(int64_t) * (2 * (size_t)n + 1), &p))) return rc;
+    if ((rc = scratch(c, 12, (size_t)c->bvox * n, &p))) return rc;
+    const size_t bytes = (size_t)c->bvox * n;
+    if (c->staging_bytes < bytes) {
+        RO_CUDA(cudaEventSynchronize(c->upload_done));
+        if (c->staging) cudaFreeHost(c->staging);
+        c->staging = nullptr;
+        c->staging_bytes = 0;
+        RO_CUDA(cudaMallocHost(&c->staging, bytes));
+        c->staging_bytes = bytes;
+    }
+    RO_CUDA(cudaFuncSetAttribute(k_lru_batch, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)topk::kSortSmem));
+    const void *kernels[] = {(const void *)k_check_batch, (const void *)k_copy_payloads,
+                             (const void *)k_copy_payloads_bytes, (const void *)k_sub_max,
+                             (const void *)k_sub_max_all, (const void *)k_release,
+                             (const void *)k_lru_batch, (const void *)k_octree_update,
+                             (const void *)k_swap_release, (const void *)k_invalidate,
+                             (const void *)k_set_metadata, (const void *)k_level_metadata,
+                             (const void *)k_reset_range, (const void *)k_rebuild_leaves,
+                             (const void *)k_rebuild_level};
+    cudaFuncAttributes fa;
+    for (const void *k : kernels) RO_CUDA(cudaFuncGetAttributes(&fa, k));
+    int grid;
+    if ((rc = coop_grid((const void *)k_lru_batch, topk::kSortSmem, &grid))) return rc;
+    if ((rc = coop_grid((const void *)k_octree_update, 0, &grid))) return rc;
+    return RO_OK;
+}
+
 int release_bricks(ro_ctx *c, const ro_state *st, const int64_t *ids_h, int64_t n64,
                    int32_t status, int32_t update_octree, cudaStream_t s) {
     if (n64 <= 0) return RO_OK;

@@ -100,11 +100,20 @@ class PinnedBrickBuffer:
         self.brick_shape = tuple(brick_shape_zyx)
         self._buf = None
 
+    def reserve(self, n: int):
+        """Page-locked room for n bricks ahead of the first batch."""
+        need = n * math.prod(self.brick_shape)
+        if self._buf is None or self._buf.numel() < need:
+            self._buf = torch.empty(need, dtype=torch.uint8, pin_memory=True)
+
     def stack(self, payloads):
         n = len(payloads)
-        if any(np.shape(p) != self.brick_shape or np.asarray(p).dtype != np.uint8
-               for p in payloads):
-            return np.stack(payloads)   # insert_bricks reports the bad payload
+        for i, p in enumerate(payloads):   # insert_brick's check (paging.py:196-197)
+            if np.shape(p) != self.brick_shape:
+                raise PagingError(f"payload shape {np.shape(p)} != brick size "
+                                  f"(payload {i} of {n})")
+        if any(np.asarray(p).dtype != np.uint8 for p in payloads):
+            return np.stack(payloads)   # insert_bricks converts / reports it
         need = n * math.prod(self.brick_shape)
         if self._buf is None or self._buf.numel() < need:
             cap = max(need, 2 * (0 if self._buf is None else self._buf.numel()))

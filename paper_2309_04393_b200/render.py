@@ -19,6 +19,7 @@ import ctypes as C
 import functools
 import math
 import time
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -412,37 +413,93 @@ def render_frame_device(mode, paging: MultiChannelPaging, octree: ResidencyOctre
     return fp.buf
 
 
-_HOST_POOL: dict = {}
-_HOST_POOL_DEPTH = 4
-_storage_uses = getattr(torch._C, "_storage_Use_Count", None)
+class _ResultPool:
+    """Page-locked host buffers for frame results, with explicit ownership.
+
+    A frame's four result buffers (image, per-pixel counts, usage mask, the
+    small int64 block) form one *set*.  The ray caster stores the image and
+    per-pixel counts straight into a set over PCIe (zero-copy) and the rest is
+    copied behind it; the numpy arrays handed to the caller are views of the
+    set, and a ``weakref.finalize`` on each returns the set to the pool once
+    every view (including any slice the caller kept) is gone.  At most
+    ``depth`` sets exist per shape: when the caller holds all of them (e.g. a
+    Session keeping its frame history) the frame lands in a private staging
+    set and is copied out into ordinary numpy arrays -- page-locked memory
+    is never allocated per frame (cudaHostAlloc of a 1080p frame costs
+    ~15 ms) and never grows without bound."""
+
+    def __init__(self, depth: int = 4, pin: bool = True):
+        self.depth = depth
+        self.pin = pin
+        self._free: dict = {}      # key -> [set, ...]
+        self._count: dict = {}     # key -> sets created (handed out or free)
+        self._staging: dict = {}   # key -> the private set
+
+    def _make(self, shapes):
+        return tuple(torch.empty(shp, dtype=dt, pin_memory=self.pin) for shp, dt in shapes)
+
+    def reserve(self, shapes, n: int = 1):
+        """Create up to n free sets (and the staging set) ahead of the first frame."""
+        key = tuple(shapes)
+        free = self._free.setdefault(key, [])
+        while len(free) < n and self._count.get(key, 0) < self.depth:
+            free.append(self._make(shapes))
+            self._count[key] = self._count.get(key, 0) + 1
+        if key not in self._staging:
+            self._staging[key] = self._make(shapes)
+
+    def acquire(self, shapes):
+        """(set, owned): owned = handed out (release on finalize) or not
+        (the staging set: copy the results out)."""
+        key = tuple(shapes)
+        free = self._free.setdefault(key, [])
+        if free:
+            return free.pop(), True
+        if self._count.get(key, 0) < self.depth:
+            self._count[key] = self._count.get(key, 0) + 1
+            return self._make(shapes), True
+        if key not in self._staging:
+            self._staging[key] = self._make(shapes)
+        return self._staging[key], False
+
+    def handout(self, shapes, bufset, tensors) -> list:
+        """numpy arrays over ``tensors`` (members of bufset); bufset returns
+        to the pool when every one of them, and every view derived from
+        them, is garbage.  Each array's memory owner is a fresh lease object
+        (numpy keeps a view's chain of bases alive up to it), so the lease's
+        finalizer is the exact "no view left" signal."""
+        key = tuple(shapes)
+        state = {"left": len(tensors)}
+        free = self._free.setdefault(key, [])
+
+        def done():
+            state["left"] -= 1
+            if state["left"] == 0:
+                free.append(bufset)
+        out = []
+        for t in tensors:
+            lease = _Lease(t)
+            weakref.finalize(lease, done)
+            out.append(np.asarray(lease))
+        return out
 
 
-def _pinned(shape, dtype, pin: bool = True) -> torch.Tensor:
-    """A page-locked host buffer for one frame's results, recycled once the
-    caller has dropped every array of the FrameOutput that used it (the
-    numpy views keep the tensor referenced).  torch's caching host allocator
-    costs ~0.5 ms per 33 MB image while the previous frame's output is still
-    alive; this pool makes the steady state allocation-free.  (A numpy view
-    of a tensor holds an alias tensor, so liveness is read off the storage's
-    use count, not the Python refcount.)"""
-    key = (tuple(shape), dtype, pin)
-    pool = _HOST_POOL.get(key)
-    if pool is None:
-        if len(_HOST_POOL) > 8:
-            _HOST_POOL.clear()
-        pool = _HOST_POOL[key] = []
-    if _storage_uses is not None:
-        for t in pool:
-            # free <=> no array view holds the storage: the tensor plus the
-            # temporary storage handle of this query
-            if _storage_uses(t.untyped_storage()._cdata) <= 2:
-                return t
-    else:
-        return torch.empty(shape, dtype=dtype, pin_memory=pin)
-    t = torch.empty(shape, dtype=dtype, pin_memory=pin)
-    if len(pool) < _HOST_POOL_DEPTH:
-        pool.append(t)
-    return t
+class _Lease:
+    """Memory owner of the numpy views handed out from one pooled buffer."""
+
+    def __init__(self, t: torch.Tensor):
+        self.t = t
+        self.__array_interface__ = {"data": (t.data_ptr(), False), "shape": tuple(t.shape),
+                                    "typestr": np.dtype(str(t.dtype).split(".")[-1]).str,
+                                    "version": 3}
+
+
+_RESULTS = _ResultPool()
+
+
+def _result_shapes(buf) -> tuple:
+    return ((tuple(buf.image.shape), torch.float32), (tuple(buf.pix_required.shape), torch.int32),
+            (tuple(buf.required.shape), torch.uint8), (tuple(buf.small.shape), torch.int64))
 
 
 def _run(mode, paging, channels, camera, config, octree=None,
@@ -457,11 +514,9 @@ def _run(mode, paging, channels, camera, config, octree=None,
     # device->host transfer rides PCIe while the kernel runs instead of
     # after it.  Usage mask, histogram and counters stay in HBM (scattered
     # writes / atomics) and are copied once the kernel is done.
-    img = _pinned(buf.image.shape, torch.float32)
-    pixr = _pinned(buf.pix_required.shape, torch.int32)
-    req = _pinned(buf.required.shape, torch.uint8)
+    shapes = _result_shapes(buf)
+    (img, pixr, req, small), owned = _RESULTS.acquire(shapes)
     nh = buf.hist.numel()
-    small = _pinned(buf.small.shape, torch.int64)
     fp.render(N.Outputs(img.data_ptr(), buf.required.data_ptr(), pixr.data_ptr(),
                         buf.hist.data_ptr(), buf.counters.data_ptr()))
     fp.collect(asynchronous=True)
@@ -492,9 +547,15 @@ def _run(mode, paging, channels, camera, config, octree=None,
                        livelocked_rays=int(counters[4]))
     w, h = config.image_dims
     rows = buf.image.shape[0] // w  # local rows of a partition (h for a full frame)
-    return FrameOutput(image=img.numpy().reshape(rows, w, 4), brick_requests=bricks,
+    if owned:
+        image, pixel_required, required = _RESULTS.handout(
+            shapes, (img, pixr, req, small), (img, pixr, req))
+    else:   # every pooled set is still held by the caller: copy out of staging
+        image, pixel_required, required = img.numpy().copy(), pixr.numpy().copy(), req.numpy().copy()
+    image = image.reshape(rows, w, 4)
+    return FrameOutput(image=image, brick_requests=bricks,
                        metadata_requests=metas, stats=stats, required_mask=required,
-                       level_histogram=hist, pixel_required=pixr.numpy(),
+                       level_histogram=hist, pixel_required=pixel_required,
                        required_mask_device=buf.required)
 
 

@@ -134,3 +134,59 @@ def test_gpu_abi_pinned_payload_error_leaves_context_usable():
         slot = p.resident_slot(int(bid))
         assert slot is not None
         assert np.array_equal(p.cache[slot], pay[i].numpy())
+
+
+def test_gpu_abi_pageable_payload_error_leaves_feedback_intact():
+    """ro_apply_bricks with PAGEABLE payloads (staged through the handle's
+    pinned buffer, uploaded into their own scratch slot) and a bad id: the
+    call fails before any copy is queued, nothing is inserted, and the next
+    frame's request ordering and a following valid batch are unaffected
+    (no late DMA can land in another call's scratch)."""
+    from paper_2309_04393_b200 import (ChannelSettings, Engine, EngineConfig, RenderConfig,
+                                       grayscale_ramp_tf, orbit_pose, render_frame)
+    from paper_2309_04393_b200 import _native as N
+    lib = N.lib()
+    st = scenes.store("mc64")
+    eng = Engine(st.manifest, EngineConfig(octree_depth=3, cache_slots=(4, 4, 4),
+                                           channel_slots=2))
+    p = eng.paging
+    state = p.state()
+    s = N.stream_ptr()
+    pay = (np.arange(3 * 16 ** 3, dtype=np.int64) % 249).astype(np.uint8).reshape(3, 16, 16, 16)
+    good = p.encode(0, 0, (0, 0, 0))
+    ids = np.array([good, p.encode(1, 0, (1, 0, 0)), (1 << 33) + 7], dtype=np.int64)
+    msg = _err(lib.ro_apply_bricks(p.ctx, C.byref(state), ids.ctypes.data, 3,
+                                   pay.ctypes.data, 0, 1, 1, None, None, s))
+    assert "index 2" in msg
+    assert p.resident_slot(good) is None
+    chans = [ChannelSettings(slot=0, tf=grayscale_ramp_tf(20.0))]
+    cfg = RenderConfig(image_dims=(16, 12), base_step=1 / 64, max_requests_per_frame=64)
+    a = render_frame(p, eng.octree, chans, orbit_pose(0.5), cfg)
+    b = render_frame(p, eng.octree, chans, orbit_pose(0.5), cfg)
+    assert a.brick_requests == b.brick_requests and a.metadata_requests == b.metadata_requests
+    eng.advance_frame()
+    eng.apply_bricks(ids[:2], pay[:2])
+    for i, bid in enumerate(ids[:2]):
+        slot = p.resident_slot(int(bid))
+        assert slot is not None and np.array_equal(p.cache[slot], pay[i])
+
+
+def test_gpu_render_without_collect_leaves_no_stale_requests():
+    """A ray-cast pass whose requests were never collected (ro_render alone,
+    render_frame_device(collect=False)) must not leak its first-seen keys
+    into the next frame's ordered lists."""
+    from paper_2309_04393_b200 import (ChannelSettings, Engine, EngineConfig, RenderConfig,
+                                       grayscale_ramp_tf, orbit_pose, render_frame)
+    from paper_2309_04393_b200.render import MODE_RESIDENCY, render_frame_device
+    st = scenes.store("mc64")
+    eng = Engine(st.manifest, EngineConfig(octree_depth=3, cache_slots=(4, 4, 4),
+                                           channel_slots=2))
+    chans = [ChannelSettings(slot=0, tf=grayscale_ramp_tf(20.0)),
+             ChannelSettings(slot=1, tf=grayscale_ramp_tf(30.0))]
+    cfg = RenderConfig(image_dims=(24, 16), base_step=1 / 64, max_requests_per_frame=64)
+    want = render_frame(eng.paging, eng.octree, chans, orbit_pose(2.5), cfg)
+    render_frame_device(MODE_RESIDENCY, eng.paging, eng.octree, chans, orbit_pose(0.4), cfg,
+                        collect=False)
+    got = render_frame(eng.paging, eng.octree, chans, orbit_pose(2.5), cfg)
+    assert got.brick_requests == want.brick_requests
+    assert got.metadata_requests == want.metadata_requests

@@ -316,28 +316,43 @@ def test_c_pack_frame_matches_python_packing(native_lib):
 
 
 def test_host_result_pool_recycles_only_dropped_buffers():
-    """render._pinned: a frame's host buffer is reused only after every
-    array view of the previous FrameOutput that used it is gone."""
+    """render._ResultPool: a frame's page-locked result set is reused only
+    after every array handed out from it -- and every view derived from
+    those -- is gone; with all sets held, frames land in the private staging
+    set (copied out) instead of allocating more page-locked memory."""
+    import gc
+
     import torch
     from paper_2309_04393_b200 import render as R
+    pool = R._ResultPool(depth=2, pin=False)
+    shapes = (((8, 4), torch.float32),)
 
     def frame():
-        t = R._pinned((8, 4), torch.float32, pin=False)
-        return t.numpy().reshape(32)[3:], t.data_ptr()
+        (t,), owned = pool.acquire(shapes)
+        if not owned:
+            return None, t.data_ptr(), False
+        (arr,) = pool.handout(shapes, (t,), (t,))
+        return arr.reshape(32)[3:], t.data_ptr(), True   # the caller keeps a slice only
 
-    o1, p1 = frame()
-    o2, p2 = frame()
-    assert p1 != p2                  # o1 still alive: a second buffer
-    held = torch.from_numpy(o2)      # a torch view of a numpy view keeps it alive too
+    o1, p1, _ = frame()
+    o2, p2, _ = frame()
+    assert p1 != p2                      # o1 still alive: a second set
+    _, p3, owned3 = frame()
+    assert not owned3 and p3 not in (p1, p2)   # depth reached: staging, not a third set
+    held = torch.from_numpy(o2)          # a torch view of a numpy view keeps it alive too
     del o1
-    o3, p3 = frame()
-    assert p3 == p1                  # recycled
-    o4, p4 = frame()
-    assert p4 not in (p1, p2)
+    gc.collect()
+    o4, p4, owned4 = frame()
+    assert owned4 and p4 == p1           # recycled once every view of it was gone
     del o2
-    o5, p5 = frame()
-    assert p5 not in (p1, p2, p4)    # `held` still references buffer 2
-    del held, o3, o4, o5
+    gc.collect()
+    _, p5, owned5 = frame()
+    assert not owned5                    # `held` still references set 2
+    del held
+    gc.collect()
+    o6, p6, owned6 = frame()
+    assert owned6 and p6 == p2
+    del o4, o6
 
 
 def test_procedural_store_metadata_is_conservative():

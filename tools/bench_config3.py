@@ -29,6 +29,15 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
+def _percentiles(xs) -> dict:
+    """p50 / p99 / max of per-frame times, and frame 1 over the median."""
+    a = np.asarray(xs, dtype=np.float64)
+    p50 = float(np.percentile(a, 50))
+    return {"p50": round(p50, 3), "p99": round(float(np.percentile(a, 99)), 3),
+            "max": round(float(a.max()), 3), "first": round(float(a[0]), 3),
+            "first_over_p50": round(float(a[0]) / p50, 2) if p50 > 0 else None}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--image", type=int, nargs=2, default=[1920, 1080])
@@ -125,6 +134,10 @@ def main():
             "host_fetch_ms_median": float(np.median([r["host_fetch_ms"] for r in frames])),
             "device_metadata": args.device_metadata, "lz4_transfer": args.lz4,
             "swap_ms": [r["swap_ms"] for r in rows if "swap_ms" in r],
+            "frame_device_ms": _percentiles([r["render_ms"] + r["note_sampled_ms"]
+                                             + r["apply_bricks_ms"] + r["apply_metadata_ms"]
+                                             for r in frames]),
+            "render_ms": _percentiles([r["render_ms"] for r in frames]),
             "per_frame": rows}
     if args.oracle:
         # reference-semantics Python update cost on a replayed batch

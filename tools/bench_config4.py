@@ -45,6 +45,15 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
+def _percentiles(xs) -> dict:
+    """p50 / p99 / max of per-frame times, and frame 1 over the median."""
+    a = np.asarray(xs, dtype=np.float64)
+    p50 = float(np.percentile(a, 50))
+    return {"p50": round(p50, 3), "p99": round(float(np.percentile(a, 99)), 3),
+            "max": round(float(a.max()), 3), "first": round(float(a[0]), 3),
+            "first_over_p50": round(float(a[0]) / p50, 2) if p50 > 0 else None}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cold-frames", type=int, default=40)
@@ -86,6 +95,15 @@ def main():
     cfg = RenderConfig(image_dims=tuple(args.image), base_step=1.0 / 512.0,
                        max_requests_per_frame=args.budget, traversal_start_level=2)
     pinned = PinnedBrickBuffer((32, 32, 32))
+    # one-time costs before the first frame (as Session does): library
+    # scratch + pinned staging for a full budget batch, kernels loaded,
+    # frame buffers and page-locked result sets
+    t1 = time.perf_counter()
+    part = (args.partition[0], args.partition[1], 8) if args.partition else (1, 0, 8)
+    eng.reserve(cfg, len(channels), partition=part)
+    pinned.reserve(args.budget)
+    torch.cuda.synchronize()
+    reserve_s = time.perf_counter() - t1
     pool = ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 4))
 
     def timed(fn):
@@ -193,6 +211,9 @@ def main():
             "partition": (f"capacity mode, part {args.partition[1]} of {args.partition[0]} "
                           "(8-row blocks)") if args.partition else "whole frame",
             "first_frames_ms": [round(f["render_ms"] + f["apply_ms"], 1) for f in frames[:5]],
+            "reserve_s": round(reserve_s, 3),
+            "frame_ms_excl_fetch": _percentiles([f["render_ms"] + f["note_ms"] + f["apply_ms"]
+                                                 + f["meta_ms"] for f in frames]),
             "payloads": "pageable (staging copy)" if args.pageable else
                         "page-locked PinnedBrickBuffer (direct DMA)",
             "bytes_generated": store.bytes_served,
