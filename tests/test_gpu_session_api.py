@@ -198,6 +198,5 @@ def test_held_frame_outputs_are_never_overwritten():
     gc.collect()
     before = dict(R._RESULTS._count)
     for _ in range(5):
-        out = render_frame(eng.paging, eng.octree, chans, orbit_pose(0.2), cfg)
-        assert np.array_equal(out.image, snaps[0][0]) or out.image.shape == snaps[0][0].shape
+        render_frame(eng.paging, eng.octree, chans, orbit_pose(0.2), cfg)
     assert R._RESULTS._count == before
