@@ -86,25 +86,55 @@ __device__ uint32_t xxh32(const uint8_t *p, int64_t len, uint32_t seed) {
     return h;
 }
 
+// Byte sources of the parser.  GlobalBytes reads the frame where it lies;
+// SmemBytes reads a copy in shared memory (4-byte aligned, >= 8 bytes of
+// slack) and can fetch an 8-byte window in two word loads, so the common
+// sequence (token, short literal run, 2-byte offset) costs one dependent
+// load instead of three.
+struct GlobalBytes {
+    const uint8_t *p;
+    static constexpr bool kWindow = false;
+    __device__ uint32_t u8(int64_t i) const { return p[i]; }
+    __device__ uint64_t win8(int64_t) const { return 0; }
+};
+struct SmemBytes {
+    const uint32_t *w;
+    static constexpr bool kWindow = true;
+    __device__ uint32_t u8(int64_t i) const { return (w[i >> 2] >> ((i & 3) << 3)) & 0xFFu; }
+    __device__ uint64_t win8(int64_t i) const {
+        const int64_t q = i >> 2;
+        const int r = (int)(i & 3) << 3;
+        const uint64_t lo = (uint64_t)w[q] | ((uint64_t)w[q + 1] << 32);
+        return r ? (lo >> r) | ((uint64_t)w[q + 2] << (64 - r)) : lo;
+    }
+};
+
 // The LZ4 frame / block parser, generic over a sink that receives literal
 // runs (offset in the frame, length) and matches (offset, length) in stream
 // order.  All lanes of the warp parse the same bytes (broadcast loads), so
 // control flow stays warp-uniform.  `op` tracks the output position for the
 // bounds / offset checks; the sink produces the bytes.
-template <class Sink>
-__device__ int32_t lz4_block_parse(const uint8_t *__restrict__ b, int64_t bpos, int64_t bl,
-                                   Sink &sink, int64_t &op, int64_t low, int64_t limit) {
-    const uint8_t *blk = b + bpos;
+template <class Sink, class Src>
+__device__ int32_t lz4_block_parse(const Src &src, int64_t bpos, int64_t bl, Sink &sink,
+                                   int64_t &op, int64_t low, int64_t limit) {
     int64_t ip = 0;
     while (true) {
         if (ip >= bl) return LZ4_E_CORRUPT;
-        const uint32_t token = blk[ip++];
+        uint64_t win = 0;
+        uint32_t token;
+        if (Src::kWindow) {
+            win = src.win8(bpos + ip);
+            token = (uint32_t)win & 0xFFu;
+        } else {
+            token = src.u8(bpos + ip);
+        }
+        const int64_t ip0 = ip++;
         int64_t lit = token >> 4;
         if (lit == 15) {
             uint32_t s;
             do {
                 if (ip >= bl) return LZ4_E_CORRUPT;
-                s = blk[ip++];
+                s = src.u8(bpos + ip++);
                 lit += s;
             } while (s == 255);
         }
@@ -117,14 +147,19 @@ __device__ int32_t lz4_block_parse(const uint8_t *__restrict__ b, int64_t bpos, 
             return LZ4_OK;
         }
         if (ip + 2 > bl) return LZ4_E_CORRUPT;
-        const int64_t off = (int64_t)blk[ip] | ((int64_t)blk[ip + 1] << 8);
+        int64_t off;
+        if (Src::kWindow && ip + 2 - ip0 <= 8) {
+            off = (int64_t)((win >> ((ip - ip0) << 3)) & 0xFFFFu);
+        } else {
+            off = (int64_t)src.u8(bpos + ip) | ((int64_t)src.u8(bpos + ip + 1) << 8);
+        }
         ip += 2;
         int64_t ml = token & 15;
         if (ml == 15) {
             uint32_t s;
             do {
                 if (ip >= bl) return LZ4_E_CORRUPT;
-                s = blk[ip++];
+                s = src.u8(bpos + ip++);
                 ml += s;
             } while (s == 255);
         }
@@ -142,9 +177,9 @@ __device__ int32_t lz4_block_parse(const uint8_t *__restrict__ b, int64_t bpos, 
 // One frame; the sink receives every byte-producing run in order.  Returns
 // the decoded size or an LZ4_E_* code.  `content` (optional) receives the
 // position of the content checksum for a sink that checks it later.
-template <class Sink>
+template <class Sink, class Src = GlobalBytes>
 __device__ int64_t lz4_frame_parse(const uint8_t *__restrict__ src, int64_t len, int64_t cap,
-                                   Sink &sink, int64_t *cchk_at) {
+                                   Sink &sink, int64_t *cchk_at, const Src &bytes = Src{}) {
     if (len < 7) return LZ4_E_TRUNCATED;
     if (rd32(src) != 0x184D2204u) return LZ4_E_MAGIC;
     const uint32_t flg = src[4], bd = src[5];
@@ -183,7 +218,12 @@ __device__ int64_t lz4_frame_parse(const uint8_t *__restrict__ src, int64_t len,
             sink.seq(pos, bl, 0, 0, op);
             op += bl;
         } else {
-            const int32_t rc = lz4_block_parse(src, pos, bl, sink, op, indep ? start : 0, limit);
+            int32_t rc;
+            if (Src::kWindow)
+                rc = lz4_block_parse(bytes, pos, bl, sink, op, indep ? start : 0, limit);
+            else
+                rc = lz4_block_parse(GlobalBytes{src}, pos, bl, sink, op, indep ? start : 0,
+                                     limit);
             if (rc != LZ4_OK) return rc == LZ4_E_CORRUPT && op >= limit ? LZ4_E_SIZE : rc;
         }
         pos += bl + (bchk ? 4 : 0);
@@ -243,19 +283,35 @@ struct LzRec {
 };
 constexpr int kRing = 256;
 
+// Records are published in groups of kPublish: one fence + head store per
+// group instead of per sequence (a noise-floor brick has ~6,700 of them).
+constexpr int kPublish = 32;
+
 struct EmitSink {
     LzRec *ring;
     volatile int *head, *tail;
     int h;
     int lane;
-    __device__ void push(int32_t a, int32_t l, int32_t o, int32_t m) {
-        while (h - *tail >= kRing) {
-        }
-        if (lane == 0) ring[h % kRing] = LzRec{a, l, o, m};
+    int published = 0;
+    int tail_seen = 0;  // last tail read: the ring has room while h - tail_seen < kRing
+    __device__ void publish() {
         __threadfence_block();
         __syncwarp();
-        ++h;
         if (lane == 0) *head = h;
+        published = h;
+    }
+    __device__ void push(int32_t a, int32_t l, int32_t o, int32_t m) {
+        if (h - tail_seen >= kRing) {
+            tail_seen = *tail;
+            if (h - tail_seen >= kRing) {
+                publish();  // the consumer may be waiting for these
+                while (h - (tail_seen = *tail) >= kRing) {
+                }
+            }
+        }
+        if (lane == 0) ring[h % kRing] = LzRec{a, l, o, m};
+        ++h;
+        if (m < 0 || h - published >= kPublish) publish();
     }
     __device__ void seq(int64_t lit_at, int64_t lit, int64_t off, int64_t ml, int64_t) {
         push((int32_t)lit_at, (int32_t)lit, (int32_t)off, (int32_t)ml);
@@ -263,13 +319,21 @@ struct EmitSink {
     __device__ bool content_ok(int64_t, uint32_t) { return true; }  // checked after copying
 };
 
+// The compressed frame itself is first copied into shared memory (when it
+// fits in fin_cap bytes): the parse is a serial chain of dependent byte
+// reads (token -> literal length -> offset -> match length -> next token),
+// so its speed is the load latency, and shared memory answers several
+// times sooner than L1 / L2.
 __global__ void __launch_bounds__(64)
 k_lz4_decode_pipe(int64_t n, const uint8_t *__restrict__ src, const int64_t *__restrict__ off,
                   uint8_t *__restrict__ dst, int64_t stride, int64_t expected,
-                  int32_t *__restrict__ status, int32_t *__restrict__ first_bad) {
+                  int32_t *__restrict__ status, int32_t *__restrict__ first_bad,
+                  int64_t fin_cap) {
     extern __shared__ __align__(16) uint8_t sh[];
     uint8_t *out = sh;
-    LzRec *ring = reinterpret_cast<LzRec *>(sh + ((stride + 15) & ~(int64_t)15));
+    const int64_t out_bytes = (stride + 15) & ~(int64_t)15;
+    LzRec *ring = reinterpret_cast<LzRec *>(sh + out_bytes);
+    uint8_t *fin = sh + out_bytes + sizeof(LzRec) * kRing;  // 16-byte aligned
     __shared__ int s_head, s_tail;
     __shared__ long long s_result, s_cchk;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -278,6 +342,13 @@ k_lz4_decode_pipe(int64_t n, const uint8_t *__restrict__ src, const int64_t *__r
     const int64_t o0 = off[0];
     const int64_t a = off[i] - o0, b = off[i + 1] - o0;
     const uint8_t *f = src + a;
+    const bool staged = b >= a && b - a <= fin_cap;
+    if (staged) {
+        const int64_t len = b - a;
+        for (int64_t j = threadIdx.x; j < len; j += 64) fin[j] = f[j];
+        for (int64_t j = len + threadIdx.x; j < len + 16; j += 64) fin[j] = 0;  // window slack
+        f = fin;
+    }
     if (threadIdx.x == 0) {
         s_head = 0;
         s_tail = 0;
@@ -287,19 +358,29 @@ k_lz4_decode_pipe(int64_t n, const uint8_t *__restrict__ src, const int64_t *__r
     if (warp == 0) {
         EmitSink sink{ring, &s_head, &s_tail, 0, lane};
         int64_t cchk = -1;
-        const int64_t r = (b < a) ? LZ4_E_TRUNCATED : lz4_frame_parse(f, b - a, stride, sink, &cchk);
+        int64_t r;
+        if (b < a)
+            r = LZ4_E_TRUNCATED;
+        else if (staged)
+            r = lz4_frame_parse(f, b - a, stride, sink, &cchk,
+                                SmemBytes{reinterpret_cast<const uint32_t *>(fin)});
+        else
+            r = lz4_frame_parse(f, b - a, stride, sink, &cchk);
         sink.push(0, 0, 0, -1);  // end of stream
         if (lane == 0) {
             s_result = r;
             s_cchk = cchk;
         }
     } else {
-        int t = 0;
+        int t = 0, avail = 0;
         int64_t op = 0;
         while (true) {
-            while (*(volatile int *)&s_head == t) {
+            if (t == avail) {  // every published record consumed: hand back, wait
+                if (lane == 0) *(volatile int *)&s_tail = t;
+                while ((avail = *(volatile int *)&s_head) == t) {
+                }
+                __threadfence_block();
             }
-            __threadfence_block();
             const LzRec r = ring[t % kRing];
             if (r.ml < 0) break;
             for (int64_t q = lane; q < r.lit; q += 32) out[op + q] = f[r.lit_at + q];
@@ -316,7 +397,7 @@ k_lz4_decode_pipe(int64_t n, const uint8_t *__restrict__ src, const int64_t *__r
             }
             __syncwarp();
             ++t;
-            if (lane == 0) *(volatile int *)&s_tail = t;
+            if (lane == 0 && (t & (kPublish - 1)) == 0) *(volatile int *)&s_tail = t;
         }
     }
     __syncthreads();
@@ -501,13 +582,15 @@ int lz4_decode(ro_ctx *c, const uint8_t *src, const int64_t *off, int64_t n, uin
     // throughput-bound: the one-warp decoder keeps far more frames in flight
     // (measured: 2.1 vs 2.9 ms per brick; 12 vs 29 GB/s in bulk).
     if (stride <= 64 * 1024) {
-        const size_t smem = (size_t)((stride + 15) & ~(int64_t)15) + sizeof(LzRec) * kRing;
-        static bool attr = false;
-        if (!attr) {
+        // frames up to max(48 KB, 1.5 x the brick) are parsed from shared memory
+        const int64_t fin_cap = std::max<int64_t>(48 * 1024, stride + stride / 2 + 64);
+        const size_t smem = (size_t)((stride + 15) & ~(int64_t)15) + sizeof(LzRec) * kRing +
+                            (size_t)fin_cap + 16;
+        static size_t attr = 0;
+        if (attr < smem) {
             RO_CUDA(cudaFuncSetAttribute(k_lz4_decode_pipe,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         64 * 1024 + (int)(sizeof(LzRec) * kRing) + 16));
-            attr = true;
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            attr = smem;
         }
         int per_sm = 0, dev = 0, sms = 0;
         RO_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lz4_decode_pipe, 64,
@@ -516,7 +599,7 @@ int lz4_decode(ro_ctx *c, const uint8_t *src, const int64_t *off, int64_t n, uin
         RO_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
         if (n <= (int64_t)per_sm * sms) {
             k_lz4_decode_pipe<<<(unsigned)n, 64, smem, s>>>(n, src, off, dst, stride, expected,
-                                                            status, first_bad);
+                                                            status, first_bad, fin_cap);
             RO_CUDA(cudaGetLastError());
             return RO_OK;
         }

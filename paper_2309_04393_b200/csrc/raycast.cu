@@ -272,6 +272,17 @@ __device__ __forceinline__ void request(unsigned long long *keys, int32_t *, int
 
 // Brick coordinates of one level at the current sample position:
 // P = fl(p * dim) (kernels.py:179 numerator), c = int(P / b) = int(P) >> lb.
+// per-thread shared-memory arrays addressed by 32-bit shared addresses
+// computed once (1) or through generic pointers (0)
+#ifndef RO_SMEM_ASM
+#define RO_SMEM_ASM 0
+#endif
+// Experiment: stage the two z-slices of a brick a warp's taps
+// need into shared memory with one TMA bulk copy (cp.async.bulk + mbarrier)
+// and read the taps from there, instead of eight L1-cached gathers per lane
+#ifndef RO_TMA_STAGE
+#define RO_TMA_STAGE 0
+#endif
 #ifndef RO_STATS
 #define RO_STATS 0
 #endif
@@ -344,6 +355,15 @@ __device__ __forceinline__ uint4 ld_meta4(const uint4 *p) {
 #else
     return __ldg(p);
 #endif
+}
+
+__device__ __forceinline__ int lds32(uint32_t a) {
+    int v;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts32(uint32_t a, int v) {
+    asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(v));
 }
 
 // word of channel slot s (0..3) from a node's four-slot vector: two
@@ -557,6 +577,19 @@ __global__ void __launch_bounds__(kBlock, RO_CTAS_PER_SM)
 #endif
 k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A) {
     __shared__ FrameSmem S;
+#if RO_TMA_STAGE
+    // per warp: the staged slab (2 z-slices of a brick, + slack for the
+    // weight-0 upper taps that step past it) and its mbarrier
+    constexpr int kSlab = 2 * (BX ? BX : 32) * (BY ? BY : 32);
+    __shared__ alignas(128) uint8_t stage[kWarps][kSlab + 128];
+    __shared__ alignas(8) unsigned long long stage_bar[kWarps];
+    uint32_t stage_phase = 0;
+    if ((threadIdx.x & 31) == 0) {
+        const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&stage_bar[threadIdx.x >> 5]);
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;");
+#endif
     extern __shared__ int32_t dyn[];  // per-thread channel state
     const int tid = threadIdx.x;
     const int n_ch = F.n_ch;
@@ -627,6 +660,13 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
     int32_t *last_mreq = last_breq + kChStride;       // n_ch
     uint32_t *hist_t = reinterpret_cast<uint32_t *>(last_mreq + kChStride);
     for (int i = 0; i < n_ch * k; ++i) hist_t[i * kBlock + tid] = 0;
+#if RO_SMEM_ASM
+    // this thread's column of each per-thread array; element i of a
+    // channel-indexed array sits at + (i * kBlock) * 4
+    const uint32_t s_prev = (uint32_t)__cvta_generic_to_shared(run) + 4u * tid;
+    const uint32_t s_breq = (uint32_t)__cvta_generic_to_shared(last_breq) + 4u * tid;
+    const uint32_t s_hist = (uint32_t)__cvta_generic_to_shared(hist_t) + 4u * tid;
+#endif
     const int lane = tid & 31;
     [[maybe_unused]] const int warp = tid >> 5;
     const int tiles_x = (F.width + kTileW - 1) / kTileW;
@@ -776,7 +816,21 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
             // usage mask / histogram / per-pixel brick switches of a sampled
             // channel (kernels.py:670-676)
             auto account = [&](int ci, int lev, int32_t e) {
-#if !RO_RUNLEN
+#if !RO_RUNLEN && RO_SMEM_ASM
+                {
+                    const uint32_t a_pb = s_prev + ((uint32_t)ci * (kBlock * 4u));
+                    if (e != lds32(a_pb)) {
+                        sts32(a_pb, e);
+                        pixreq += 1;
+                        RO_ASSERT(e >= 0 && e < A.L.E);
+                        A.required[e] = 1;
+                    }
+                    RO_ASSERT(lev >= 0 && lev < k && ci < n_ch);
+                    const uint32_t a_h = s_hist + ((uint32_t)(ci * k + lev) * (kBlock * 4u));
+                    sts32(a_h, lds32(a_h) + 1);
+                    return;
+                }
+#elif !RO_RUNLEN
                 int32_t &pb = reinterpret_cast<int32_t *>(run)[ci * kBlock + tid];
                 if (e != pb) {
                     pb = e;
@@ -1182,6 +1236,74 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                         if (sc.lp.lev != lev) level_pos(sc.lp, lev, px, py, pz, S, lbx, lby, lbz);
                         const int32_t e = S.ptoff[ci][lev] + sc.lp.local;
                         RO_ASSERT(e >= 0 && e < A.L.E);
+#if RO_TMA_STAGE
+                        if (BX == 32 && BY == 32 && !((pf_done >> ci) & 1u) &&
+                            __activemask() == 0xffffffffu) {
+                            // whole warp here: one group owns the warp's slab
+                            const int pv = ld_meta(A.pt + e);
+                            bool need = false;
+                            if (pv >= 0) {
+                                account(ci, lev, e);
+                                need = !sub_skip(ci, pv, sc.lp);
+                                if (need && sc.tp_lev != lev) {
+                                    taps_of(sc.tp, sc.lp, px, py, pz, bx, by, bz, S);
+                                    sc.tp_lev = lev;
+                                }
+                            }
+                            const unsigned T = __ballot_sync(0xffffffffu, need);
+                            if (T) {
+                                const int z0 = need ? sc.tp.o / (bx * by) : -1;
+                                const int leader = __ffs(T) - 1;
+                                const int lslot = __shfl_sync(0xffffffffu, pv, leader);
+                                const int lz0 = __shfl_sync(0xffffffffu, z0, leader);
+                                const int w = threadIdx.x >> 5;
+                                const uint32_t bar =
+                                    (uint32_t)__cvta_generic_to_shared(&stage_bar[w]);
+                                const uint32_t dsts = (uint32_t)__cvta_generic_to_shared(stage[w]);
+                                if ((threadIdx.x & 31) == leader) {
+                                    const uint8_t *srcp = A.cache + (int64_t)lslot * bvox +
+                                                          (int64_t)lz0 * (bx * by);
+                                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                                    asm volatile(
+                                        "mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                                        ::"r"(bar), "r"(kSlab) : "memory");
+                                    asm volatile(
+                                        "cp.async.bulk.shared::cluster.global.mbarrier::"
+                                        "complete_tx::bytes [%0], [%1], %2, [%3];"
+                                        ::"r"(dsts), "l"(srcp), "r"(kSlab), "r"(bar) : "memory");
+                                }
+                                asm volatile(
+                                    "{\n .reg .pred p;\n WAIT%=:\n"
+                                    " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+                                    " @!p bra WAIT%=;\n}" ::"r"(bar), "r"(stage_phase) : "memory");
+                                stage_phase ^= 1u;
+                                if (need) {
+                                    if (pv == lslot && z0 == lz0) {
+                                        const uint8_t *q = stage[w] + (sc.tp.o - lz0 * (bx * by));
+                                        int tv[8] = {q[0], q[1], q[bx], q[bx + 1], q[bx * by],
+                                                     q[bx * by + 1], q[bx * by + bx],
+                                                     q[bx * by + bx + 1]};
+                                        RO_STAT(c_s6);
+                                        const int mt = max(max(max(tv[0], tv[1]), max(tv[2], tv[3])),
+                                                           max(max(tv[4], tv[5]), max(tv[6], tv[7])));
+                                        if (mt > S.zero_upto[ci]) {
+                                            const double val = trilerp(tv, sc.tp);
+                                            double r, g, b, a;
+                                            tf_eval(S, ci, val, r, g, b, a);
+                                            sR += r * a;
+                                            sG += g * a;
+                                            sB += b * a;
+                                            trans *= (1.0 - a);
+                                        }
+                                    } else {
+                                        finish(ci, pv, sc.tp);
+                                    }
+                                }
+                                __syncwarp();  // every read of the slab before its next fill
+                            }
+                            if (pv >= 0) continue;
+                        } else
+#endif
                         if ((pf_done >> ci) & 1u) {  // probed ahead
                             if ((pf_hit >> ci) & 1u) {
                                 account(ci, lev, e);
@@ -1198,11 +1320,19 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                         {
                             RO_STAT(c_s5);
                             const unsigned long long key = key_hi | ev++;
+#if RO_SMEM_ASM
+                            const uint32_t a_lb = s_breq + ((uint32_t)ci * (kBlock * 4u));
+                            if (e != lds32(a_lb)) {
+                                sts32(a_lb, e);
+                                request(A.brick_key, nullptr, nullptr, e, key);
+                            }
+#else
                             int32_t &lb = last_breq[ci * kBlock + tid];
                             if (e != lb) {
                                 lb = e;
                                 request(A.brick_key, nullptr, nullptr, e, key);
                             }
+#endif
                         }
                         // nearest resident level in this node, coarser first
                         int32_t e2 = -1;

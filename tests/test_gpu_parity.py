@@ -289,6 +289,53 @@ def test_gpu_partial_residency_matches_oracle(seed, eps, ranges):
         assert np.array_equal(ref.level_histogram, wr.level_histogram)
 
 
+def test_gpu_wide_request_keys_match_oracle():
+    """Request keys wider than 32 bits end to end: a 4096x2048 frame (pixel
+    index >= 2^22) whose rows 1024..1031 are rendered (sort-first part 128
+    of 256), every node's metadata INVALID so every node visit is a request
+    event (> 2^9 events per pixel with a 1/1024 step) -- packed keys of
+    > 32 bits through the ray caster's RED.MIN and the feedback kernel's
+    select / sort.  Ordered lists, usage, histogram and image equal the
+    oracle's for the same rows."""
+    import os
+    from oracle import raycast as orc
+    from paper_2309_04393_b200 import ChannelSettings, RenderConfig, grayscale_ramp_tf, orbit_pose
+    from paper_2309_04393_b200.render import MODE_RESIDENCY, FramePass
+    eng = _random_partial_engine(11, depth=4)
+    words = eng.octree.words.copy()
+    words[:] = (words & np.uint32(0xFFFF)) | np.uint32(0x00FF0000)   # all INVALID
+    eng.octree.upload_words(words)
+    chans = [ChannelSettings(slot=s, tf=grayscale_ramp_tf(180.0, max_alpha=0.05),
+                             level_range=(0, 2)) for s in (0, 1, 2, 3)]
+    w, h = 4096, 2048
+    budget = 40000
+    cfg = RenderConfig(image_dims=(w, h), base_step=1 / 1024, max_requests_per_frame=budget)
+    pose = orbit_pose(0.8, radius=1.7)
+    fp = FramePass(MODE_RESIDENCY, eng.paging, eng.octree, chans, pose, cfg,
+                   partition=(h // 8, 128, 8), bricks_first=True)
+    fp.render()
+    fp.collect()
+    b = fp.buf
+    nb, nm = b.n_bricks, b.n_metas
+    fb = b.fb.cpu().numpy()
+    m = eng.paging.config.m
+    ost = oracle_state_from_device(eng)
+    och = [orc.OracleChannel(slot=c.slot, points=c.tf.points, level_range=c.level_range)
+           for c in chans]
+    want = orc.render(ost, och, cam_tuple(pose), (w, h), cfg.base_step, budget=budget,
+                      rows=(1024, 1032), threads=os.cpu_count() or 1)
+    assert [divmod(int(v), m) for v in fb[3][:nm]] == want.metadata_requests
+    assert fb[1][:nb].tolist() == want.brick_requests
+    assert np.array_equal(b.image.cpu().numpy().reshape(8, w, 4), want.image[1024:1032])
+    assert np.array_equal(b.required.cpu().numpy(), want.required_mask)
+    assert np.array_equal(b.hist.cpu().numpy(), want.level_histogram)
+    # the keys really were wide: pixel >= 2^22 and events >= 2^9 in one key set
+    keys = fb[2][:nm].astype(np.uint64)
+    assert nm > 100
+    assert int((keys >> np.uint64(32)).max()) >= (1 << 22)
+    assert int((keys & np.uint64(0xFFFFFFFF)).max()) >= (1 << 9)
+
+
 @pytest.mark.parametrize("n_parts", [2, 3, 5])
 def test_gpu_sort_first_parts_merge_to_full_frame(n_parts):
     """Sort-first partition (row blocks round-robin over parts): per-part
