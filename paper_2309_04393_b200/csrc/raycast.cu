@@ -129,6 +129,7 @@ struct FrameSmem {
     // largest integer value v with opacity(u) == 0 for every u <= v
     int32_t zero_upto[RO_MAX_CH];
     int4 chi[RO_MAX_CH];  // (slot, lo, hi, zero_upto): one LDS.128 per channel visit
+    uint32_t nest;        // bit l: dims[l] == 2 dims[l + 1] on every axis
     unsigned long long red[RO_NUM_COUNTERS];
     // frame constants kept out of registers
     double bm1[3];      // brick extent - 1, as fp64 (the reference's B - 1.0)
@@ -295,6 +296,9 @@ __device__ __forceinline__ void request(unsigned long long *keys, int32_t *, int
 #ifndef RO_LP2_LOCAL
 #define RO_LP2_LOCAL 0
 #endif
+#ifndef RO_NEST_DERIVE
+#define RO_NEST_DERIVE 0
+#endif
 #ifndef RO_LP_NOP
 #define RO_LP_NOP 0  // 1: taps recompute P = p * dim (3 DMUL, rare) instead of keeping it live
 #endif
@@ -302,6 +306,9 @@ struct LevelPos {
     int lev;
 #if !RO_LP_NOP
     double P[3];
+#endif
+#if RO_NEST_DERIVE
+    int ip[3];  // int(P): coarser exactly-halving levels derive from it by shifts
 #endif
     int cb[3];
     int local;  // (cz*gy + cy)*gx + cx
@@ -322,6 +329,9 @@ __device__ __forceinline__ void level_pos(LevelPos &lp, int lev, double px, doub
         lp.P[a] = P;
 #endif
         const int ip = d2i_nn(P);
+#if RO_NEST_DERIVE
+        lp.ip[a] = ip;
+#endif
         int c = ip >> lb3[a];
         const int g = S.grids[lev][a];
         lp.cb[a] = c > g - 1 ? g - 1 : c;
@@ -332,6 +342,31 @@ __device__ __forceinline__ void level_pos(LevelPos &lp, int lev, double px, doub
     // (bricks smaller than a sub-block have no sub_max table: lp.sub unused)
     lp.sub = (((sb[2] << max(lby - RO_SUB_LOG, 0)) + sb[1]) << max(lbx - RO_SUB_LOG, 0)) + sb[0];
 }
+
+#if RO_NEST_DERIVE
+// Position at a coarser level `lev` from a finer one when every level in
+// between halves the dims exactly (dims[l] == 2 dims[l+1] on every axis):
+// fl(p * dims[l]) = 2^j fl(p * dims[l + j]) exactly (power-of-two scaling
+// commutes with rounding), so int(P) at lev is int(P) at src.lev >> j.
+__device__ __forceinline__ void level_pos_from(LevelPos &lp, int lev, const LevelPos &src,
+                                               const FrameSmem &S, int lbx, int lby, int lbz) {
+    const int j = lev - src.lev;
+    lp.lev = lev;
+    const int lb3[3] = {lbx, lby, lbz};
+    int sb[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const int ip = src.ip[a] >> j;
+        lp.ip[a] = ip;
+        const int c = ip >> lb3[a];
+        const int g = S.grids[lev][a];
+        lp.cb[a] = c > g - 1 ? g - 1 : c;
+        sb[a] = min(ip - (lp.cb[a] << lb3[a]), (1 << lb3[a]) - 1) >> RO_SUB_LOG;
+    }
+    lp.local = (lp.cb[2] * S.grids[lev][1] + lp.cb[1]) * S.grids[lev][0] + lp.cb[0];
+    lp.sub = (((sb[2] << max(lby - RO_SUB_LOG, 0)) + sb[1]) << max(lbx - RO_SUB_LOG, 0)) + sb[0];
+}
+#endif
 
 #ifndef RO_META_HINT
 #define RO_META_HINT 0
@@ -357,6 +392,7 @@ __device__ __forceinline__ uint4 ld_meta4(const uint4 *p) {
 #endif
 }
 
+#if RO_SMEM_ASM
 __device__ __forceinline__ int lds32(uint32_t a) {
     int v;
     asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
@@ -365,6 +401,7 @@ __device__ __forceinline__ int lds32(uint32_t a) {
 __device__ __forceinline__ void sts32(uint32_t a, int v) {
     asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(v));
 }
+#endif
 
 // word of channel slot s (0..3) from a node's four-slot vector: two
 // predicated selects, no branch chain
@@ -380,7 +417,7 @@ __device__ __forceinline__ uint32_t word_of_slot(const uint4 &wv, int s) {
 __device__ __forceinline__ int2 substitute(const int32_t *__restrict__ pt, const FrameSmem &S, int ci,
                                 int lev, int k, uint32_t mask, double px, double py,
                                 double pz, int lbx, int lby, int lbz, LevelPos &lp2,
-                                int32_t &e_out) {
+                                int32_t &e_out, const LevelPos &lp) {
     // Visit the levels present in the mask in the reference's order
     // (distance 1, 2, ...; the coarser one first on a tie) by taking the
     // nearest remaining set bit on either side, instead of scanning every
@@ -392,7 +429,15 @@ __device__ __forceinline__ int2 substitute(const int32_t *__restrict__ pt, const
         const int da = above ? __ffs(above) : 64;
         const int db = below ? lev - (31 - __clz(below)) : 64;
         const int cand = da <= db ? lev + da : lev - db;
-        if (lp2.lev != cand) level_pos(lp2, cand, px, py, pz, S, lbx, lby, lbz);
+        if (lp2.lev != cand) {
+#if RO_NEST_DERIVE
+            const uint32_t span = ((1u << cand) - 1u) & ~((1u << lev) - 1u);  // levels lev..cand-1
+            if (cand > lev && lp.lev == lev && (S.nest & span) == span)
+                level_pos_from(lp2, cand, lp, S, lbx, lby, lbz);
+            else
+#endif
+                level_pos(lp2, cand, px, py, pz, S, lbx, lby, lbz);
+        }
         RO_ASSERT(cand >= 0 && cand < RO_MAX_LEVELS && lp2.local >= 0);
         const int32_t e2 = S.ptoff[ci][cand] + lp2.local;
         const int pv2 = ld_meta(pt + e2);
@@ -419,7 +464,11 @@ struct Taps {
 __device__ __forceinline__ void taps_of(Taps &tp, const LevelPos &lp, double px, double py,
                                         double pz, int bx, int by, int bz, const FrameSmem &S) {
     const int B[3] = {bx, by, bz};
+#if RO_LP_NOP
     const double p3[3] = {px, py, pz};
+#else
+    (void)px, (void)py, (void)pz;
+#endif
     int i0[3];
     double tw[3];
 #pragma unroll
@@ -646,6 +695,13 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
         S.bm1[1] = A.L.by - 1.0;
         S.bm1[2] = A.L.bz - 1.0;
         S.side_d = (double)(1 << A.L.depth);
+        uint32_t nest = 0;
+        for (int l = 0; l + 1 < k; ++l)
+            if (A.L.dims[l][0] == 2 * A.L.dims[l + 1][0] &&
+                A.L.dims[l][1] == 2 * A.L.dims[l + 1][1] &&
+                A.L.dims[l][2] == 2 * A.L.dims[l + 1][2])
+                nest |= 1u << l;
+        S.nest = nest;
         S.inv_t0 = 1.0 / F.t0;
         S.t0_pow2 = (__double_as_longlong(F.t0) & 0x000FFFFFFFFFFFFFll) == 0;
         S.eps_i = F.eps_h >= 255.0 ? 255 : (F.eps_h < 0.0 ? -1 : (int)F.eps_h);
@@ -1343,7 +1399,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                         LevelPos &lp2 = sc.lp2;
 #endif
                         const int2 sub = substitute(A.pt, S, ci, lev, k, mask, px, py, pz,
-                                                    lbx, lby, lbz, lp2, e2);
+                                                    lbx, lby, lbz, lp2, e2, sc.lp);
                         if (sub.x >= 0) sample2(ci, sub.x, sub.y, e2, lp2);
                     }
                 }
