@@ -296,6 +296,9 @@ __device__ __forceinline__ void request(unsigned long long *keys, int32_t *, int
 #ifndef RO_LP2_LOCAL
 #define RO_LP2_LOCAL 0
 #endif
+#ifndef RO_UNROLL4
+#define RO_UNROLL4 0
+#endif
 #ifndef RO_NEST_DERIVE
 #define RO_NEST_DERIVE 0
 #endif
@@ -1204,8 +1207,8 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                     }
                 }
 #endif
-#pragma unroll 1
-                for (int ci = 0; ci < n_ch; ++ci) {
+                // one channel of the sample, in the reference's channel order
+                auto channel = [&](const int ci) {
 #if RO_CHI
                     const int4 chc = S.chi[ci];
 #else
@@ -1283,7 +1286,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                         probe = true;
                         break;
                     }
-                    if (!probe) continue;
+                    if (!probe) return;
                     }
                     // at traversal depth: probe the desired brick
                     {
@@ -1357,20 +1360,20 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                                 }
                                 __syncwarp();  // every read of the slab before its next fill
                             }
-                            if (pv >= 0) continue;
+                            if (pv >= 0) return;
                         } else
 #endif
                         if ((pf_done >> ci) & 1u) {  // probed ahead
                             if ((pf_hit >> ci) & 1u) {
                                 account(ci, lev, e);
                                 if (!((pf_skip >> ci) & 1u)) sample_taps(ci, lev, ld_meta(A.pt + e));
-                                continue;
+                                return;
                             }
                         } else {
                             const int pv = ld_meta(A.pt + e);
                             if (pv >= 0) {
                                 sample(ci, lev, pv, e);
-                                continue;
+                                return;
                             }
                         }
                         {
@@ -1402,6 +1405,18 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                                                     lbx, lby, lbz, lp2, e2, sc.lp);
                         if (sub.x >= 0) sample2(ci, sub.x, sub.y, e2, lp2);
                     }
+                };
+#if RO_UNROLL4
+                if (fast && n_ch == 4) {
+                    // the common case unrolled: every channel-indexed constant,
+                    // table and per-thread array offset becomes a constant
+#pragma unroll
+                    for (int ci = 0; ci < 4; ++ci) channel(ci);
+                } else
+#endif
+                {
+#pragma unroll 1
+                    for (int ci = 0; ci < n_ch; ++ci) channel(ci);
                 }
                 end_depth = d;
                 if (all_cz) {

@@ -19,6 +19,7 @@
 // every leaf overlapped by a changed brick is recomputed for that brick's
 // (slot, level) from the final page table, then ancestors are re-ORed level
 // by level.  Metadata bits (16..31) are never touched here.
+#include <algorithm>
 #include <cstring>
 #include <unordered_map>
 #include <vector>
@@ -95,6 +96,62 @@ __global__ void k_sub_max(int32_t n, int bx, int by, int bz, const uint8_t *__re
                 }
         }
         sub_max[(int64_t)slots[i] * nsb + q] = (uint8_t)mx;
+    }
+}
+
+// The same maxima for bricks up to 32 KiB: the brick is staged in shared
+// memory and the dilated box max is separable -- x windows, then y, then z
+// (each sub-block's window is [4s - 1, 4s + 4] clipped to the brick).
+constexpr int kSubMaxThreads = 256;
+__global__ void __launch_bounds__(kSubMaxThreads)
+k_sub_max_smem(int32_t n, int bx, int by, int bz, const uint8_t *__restrict__ src,
+               const int32_t *__restrict__ slots, const uint8_t *__restrict__ final_flag,
+               uint8_t *__restrict__ sub_max) {
+    extern __shared__ __align__(16) uint8_t sm[];
+    const int i = blockIdx.x;
+    if (i >= n || !final_flag[i]) return;
+    constexpr int E = RO_SUB_E;
+    const int nx = bx >> RO_SUB_LOG, ny = by >> RO_SUB_LOG, nz = bz >> RO_SUB_LOG,
+              nsb = nx * ny * nz;
+    const int bvox = bx * by * bz;
+    uint8_t *v = sm;                      // [bz][by][bx]
+    uint8_t *tx = v + bvox;               // [bz][by][nx]
+    uint8_t *ty = tx + bz * by * nx;      // [bz][ny][nx]
+    uint8_t *out = sub_max + (int64_t)slots[i] * nsb;
+    if (!src) {  // payload unknown: "may be anything"
+        for (int q = threadIdx.x; q < nsb; q += blockDim.x) out[q] = 255;
+        return;
+    }
+    const uint8_t *b = src + (int64_t)i * bvox;
+    if ((((uintptr_t)b) & 15) == 0 && (bvox & 15) == 0) {
+        for (int j = threadIdx.x; j < bvox / 16; j += blockDim.x)
+            reinterpret_cast<uint4 *>(v)[j] = reinterpret_cast<const uint4 *>(b)[j];
+    } else {
+        for (int j = threadIdx.x; j < bvox; j += blockDim.x) v[j] = b[j];
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < bz * by * nx; j += blockDim.x) {
+        const int sx = j % nx, row = j / nx;
+        const uint8_t *r = v + row * bx;
+        unsigned m = 0;
+        for (int x = max(E * sx - 1, 0); x < min(E * sx + E + 1, bx); ++x) m = max(m, (unsigned)r[x]);
+        tx[j] = (uint8_t)m;
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < bz * ny * nx; j += blockDim.x) {
+        const int sx = j % nx, sy = (j / nx) % ny, z = j / (nx * ny);
+        unsigned m = 0;
+        for (int y = max(E * sy - 1, 0); y < min(E * sy + E + 1, by); ++y)
+            m = max(m, (unsigned)tx[(z * by + y) * nx + sx]);
+        ty[j] = (uint8_t)m;
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < nsb; q += blockDim.x) {
+        const int sx = q % nx, sy = (q / nx) % ny, sz = q / (nx * ny);
+        unsigned m = 0;
+        for (int z = max(E * sz - 1, 0); z < min(E * sz + E + 1, bz); ++z)
+            m = max(m, (unsigned)ty[(z * ny + sy) * nx + sx]);
+        out[q] = (uint8_t)m;
     }
 }
 
@@ -648,6 +705,9 @@ int octree_update(ro_ctx *c, const ro_state *st, const int64_t *ids, int32_t n,
     A.offs = (int64_t *)po;
     int grid = 0;
     if ((rc = coop_grid((const void *)k_octree_update, 0, &grid))) return rc;
+    // a grid sync costs microseconds per level: batches of a few hundred
+    // bricks (a few thousand node updates per level) run on fewer CTAs
+    grid = (int)std::min<int64_t>(grid, std::max<int64_t>(1, n / 8));
     void *args[] = {&A};
     RO_CUDA(cudaLaunchCooperativeKernel((const void *)k_octree_update, dim3(grid),
                                         dim3(kCoopThreads), args, 0, s));
@@ -793,9 +853,15 @@ int apply_bricks(ro_ctx *c, const ro_state *st, const int64_t *ids_h, int64_t n6
     }
     if (st->sub_max && c->layout.brick[0] >= RO_SUB_E && c->layout.brick[1] >= RO_SUB_E &&
         c->layout.brick[2] >= RO_SUB_E) {
-        k_sub_max<<<n, 128, 0, s>>>(n, c->layout.brick[0], c->layout.brick[1],
-                                    c->layout.brick[2], d_payload, d_slots, d_final,
-                                    st->sub_max);
+        const int bx = c->layout.brick[0], by = c->layout.brick[1], bz = c->layout.brick[2];
+        const size_t smem = (size_t)bx * by * bz + (size_t)bz * by * (bx >> RO_SUB_LOG) +
+                            (size_t)bz * (by >> RO_SUB_LOG) * (bx >> RO_SUB_LOG);
+        if (smem <= 48 * 1024)
+            k_sub_max_smem<<<n, kSubMaxThreads, smem, s>>>(n, bx, by, bz, d_payload, d_slots,
+                                                           d_final, st->sub_max);
+        else
+            k_sub_max<<<n, 128, 0, s>>>(n, bx, by, bz, d_payload, d_slots, d_final,
+                                        st->sub_max);
         RO_CUDA(cudaGetLastError());
     }
     if (update_octree && st->words) {
@@ -837,6 +903,7 @@ int lru_reserve(ro_ctx *c, int64_t max_batch) {
                                  (int)topk::kSortSmem));
     const void *kernels[] = {(const void *)k_check_batch, (const void *)k_copy_payloads,
                              (const void *)k_copy_payloads_bytes, (const void *)k_sub_max,
+                             (const void *)k_sub_max_smem,
                              (const void *)k_sub_max_all, (const void *)k_release,
                              (const void *)k_lru_batch, (const void *)k_octree_update,
                              (const void *)k_swap_release, (const void *)k_invalidate,

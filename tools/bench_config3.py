@@ -105,8 +105,8 @@ def main():
         if ids:
             if args.lz4:
                 eng.apply_bricks_lz4(ids, pays)
-            else:
-                eng.apply_bricks(ids, np.stack(pays))
+            else:   # page-locked payloads, as Session.step_frame stacks them
+                eng.apply_bricks(ids, sess._pinned.stack(pays))
         e[4].record()
         if metas:
             eng.apply_metadata_batch([m[0] for m in metas], [m[1] for m in metas],
