@@ -553,28 +553,51 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_lru_batch(const __grid_cons
 }
 
 // ---- octree update: every level of the changed bricks, one launch ----
+// a changed brick, decoded once: its (slot, level) and its leaf box at
+// depth D (lev < 0: skipped / empty)
+struct BrickInfo {
+    int lo[3], hi[3];
+    int slot, lev;
+};
+
 struct OctArgs {
     DevLayout L;
     int32_t n;
     const int64_t *ids;  // changed bricks (< 0: skip)
     const int32_t *pt;
     uint32_t *words;
-    int64_t *offs;  // [n + 1] per-level exclusive scan of node counts
+    int64_t *offs;     // [n + 1] per-level exclusive scan of node counts
+    BrickInfo *info;   // [n]
 };
 
 // nodes of brick i's leaf box at depth dd (0 for skipped / empty)
-__device__ __forceinline__ int64_t level_count(const OctArgs &A, int32_t i, int dd, Box3 &b) {
-    b.empty = true;
-    const int64_t id = A.ids[i];
-    if (id < 0) return 0;
-    const Decoded d = decode_id(A.L, id);
-    if (!d.ok) return 0;
-    b = leaf_box(A.L, d.lev, d.x, d.y, d.z);
-    if (b.empty) return 0;
-    const int sh = A.L.depth - dd;
+__device__ __forceinline__ int64_t level_count(const BrickInfo &b, int D, int dd) {
+    if (b.lev < 0) return 0;
+    const int sh = D - dd;
     int64_t c = 1;
     for (int a = 0; a < 3; ++a) c *= (int64_t)((b.hi[a] >> sh) - (b.lo[a] >> sh) + 1);
     return c;
+}
+
+// bricks of `lev` overlapping leaf (x, y, z) -- octree.py:161-189 at depth
+// D: the divisor 2^D * B is a power of two, so the exact floor / ceil
+// divisions of brick_box are shifts
+__device__ __forceinline__ Box3 leaf_bricks(const DevLayout &L, int lx, int ly, int lz, int lev) {
+    Box3 b;
+    b.empty = false;
+    const int n[3] = {lx, ly, lz};
+    const int B[3] = {L.bx, L.by, L.bz};
+    for (int a = 0; a < 3; ++a) {
+        const int shift = L.depth + (__ffs(B[a]) - 1);
+        const int64_t dim = L.dims[lev][a];
+        const int64_t lo = ((int64_t)n[a] * dim) >> shift;
+        int64_t hi = ((((int64_t)n[a] + 1) * dim + (int64_t(1) << shift) - 1) >> shift) - 1;
+        if (hi > L.grids[lev][a] - 1) hi = L.grids[lev][a] - 1;
+        if (lo > hi) b.empty = true;
+        b.lo[a] = (int)lo;
+        b.hi[a] = (int)hi;
+    }
+    return b;
 }
 
 __global__ void __launch_bounds__(kCoopThreads, 1) k_octree_update(const __grid_constant__ OctArgs A) {
@@ -584,14 +607,36 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_octree_update(const __grid_
     const int32_t n = A.n;
     const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
+    // decode every changed brick once (its leaf box costs six 64-bit divisions)
+    for (int64_t i = gtid; i < n; i += gstride) {
+        BrickInfo bi;
+        bi.lev = -1;
+        bi.slot = 0;
+        const int64_t id = A.ids[i];
+        if (id >= 0) {
+            const Decoded d = decode_id(A.L, id);
+            if (d.ok) {
+                const Box3 b = leaf_box(A.L, d.lev, d.x, d.y, d.z);
+                if (!b.empty) {
+                    for (int a = 0; a < 3; ++a) {
+                        bi.lo[a] = b.lo[a];
+                        bi.hi[a] = b.hi[a];
+                    }
+                    bi.slot = d.slot;
+                    bi.lev = d.lev;
+                }
+            }
+        }
+        A.info[i] = bi;
+    }
+    grid.sync();
     for (int dd = D; dd >= 0; --dd) {
         // CTA 0: exclusive scan of the per-brick node counts at this depth
         if (blockIdx.x == 0) {
             const int32_t per = (n + kCoopThreads - 1) / kCoopThreads;
             const int32_t b0 = threadIdx.x * per, b1 = min(n, b0 + per);
             int64_t sum = 0;
-            Box3 b;
-            for (int32_t i = b0; i < b1; ++i) sum += level_count(A, i, dd, b);
+            for (int32_t i = b0; i < b1; ++i) sum += level_count(A.info[i], D, dd);
             s_part[threadIdx.x] = sum;
             __syncthreads();
             for (int o = 1; o < kCoopThreads; o <<= 1) {  // Hillis-Steele inclusive scan
@@ -603,7 +648,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_octree_update(const __grid_
             int64_t run = s_part[threadIdx.x] - sum;
             for (int32_t i = b0; i < b1; ++i) {
                 A.offs[i] = run;
-                run += level_count(A, i, dd, b);
+                run += level_count(A.info[i], D, dd);
             }
             if (threadIdx.x == kCoopThreads - 1) A.offs[n] = s_part[threadIdx.x];
         }
@@ -618,8 +663,8 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_octree_update(const __grid_
                 if (__ldcg(A.offs + mid) <= j) lo = mid; else hi = mid - 1;
             }
             const int32_t i = lo;
-            const Decoded d = decode_id(A.L, A.ids[i]);
-            const Box3 b = leaf_box(A.L, d.lev, d.x, d.y, d.z);
+            const BrickInfo b = A.info[i];
+            struct { int slot, lev; } d = {b.slot, b.lev};
             const int lo0 = b.lo[0] >> sh, lo1 = b.lo[1] >> sh, lo2 = b.lo[2] >> sh;
             const int w = (b.hi[0] >> sh) - lo0 + 1, h = (b.hi[1] >> sh) - lo1 + 1;
             const int64_t r = j - __ldcg(A.offs + i);
@@ -632,7 +677,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_octree_update(const __grid_
             if (dd == D) {
                 // leaf: this (slot, level) bit = some MAPPED brick of that level
                 // overlaps the leaf (octree.py:221-226 _leaf_backed)
-                const Box3 bb = brick_box(A.L, D, nx, ny, nz, d.lev);
+                const Box3 bb = leaf_bricks(A.L, nx, ny, nz, d.lev);
                 bool backed = false;
                 if (!bb.empty) {
                     for (int z = bb.lo[2]; z <= bb.hi[2] && !backed; ++z)
@@ -695,7 +740,8 @@ int octree_update(ro_ctx *c, const ro_state *st, const int64_t *ids, int32_t n,
     if (st->words == nullptr || n <= 0) return RO_OK;
     void *po;
     int rc;
-    if ((rc = scratch(c, 6, sizeof(int64_t) * ((size_t)n + 1), &po))) return rc;
+    if ((rc = scratch(c, 6, sizeof(int64_t) * ((size_t)n + 2) + sizeof(BrickInfo) * (size_t)n, &po)))
+        return rc;
     OctArgs A;
     A.L = c->dl;
     A.n = n;
@@ -703,6 +749,7 @@ int octree_update(ro_ctx *c, const ro_state *st, const int64_t *ids, int32_t n,
     A.pt = st->pt;
     A.words = st->words;
     A.offs = (int64_t *)po;
+    A.info = reinterpret_cast<BrickInfo *>(A.offs + n + 2);
     int grid = 0;
     if ((rc = coop_grid((const void *)k_octree_update, 0, &grid))) return rc;
     // a grid sync costs microseconds per level: batches of a few hundred
@@ -888,7 +935,9 @@ int lru_reserve(ro_ctx *c, int64_t max_batch) {
     int rc;
     if ((rc = scratch(c, 1, sizeof(int64_t) * 4 * n + sizeof(int32_t) * n + n + 64, &p))) return rc;
     if ((rc = scratch(c, 13, sizeof(uint32_t) * kLruCtlWords, &p))) return rc;
-    if ((rc = scratch(c, 6, sizeof(int64_t) * (2 * (size_t)n + 1), &p))) return rc;
+    if ((rc = scratch(c, 6, sizeof(int64_t) * (2 * (size_t)n + 2) + sizeof(BrickInfo) * 2 * (size_t)n,
+                      &p)))
+        return rc;
     if ((rc = scratch(c, 12, (size_t)c->bvox * n, &p))) return rc;
     const size_t bytes = (size_t)c->bvox * n;
     if (c->staging_bytes < bytes) {
