@@ -78,6 +78,10 @@
 #ifndef RO_PREFETCH
 #define RO_PREFETCH 0
 #endif
+// load the path class alongside the fast flag (1) or only for non-fast samples (0)
+#ifndef RO_PATH_EAGER
+#define RO_PATH_EAGER 0
+#endif
 // brick-run histogram (1) or a histogram increment per fetch (0)
 #ifndef RO_RUNLEN
 #define RO_RUNLEN 0
@@ -158,7 +162,8 @@ struct RayArgs {
     int32_t *tile_counter;   // persistent-CTA work counter (zeroed per launch)
     const uint8_t *sub_max;  // [S*nsb] dilated 8^3 sub-block maxima (optional)
     int32_t nsb;             // sub-blocks per slot
-    const uint8_t *node_class;  // [num_nodes] k_classify_nodes output (optional)
+    const uint8_t *node_fast;    // [num_nodes] k_classify_path outputs (optional)
+    const uint64_t *node_path;
 };
 
 __device__ __forceinline__ double lerp(double a, double b, double t) {
@@ -286,9 +291,6 @@ __device__ __forceinline__ void request(unsigned long long *keys, int32_t *, int
 #endif
 #ifndef RO_STATS
 #define RO_STATS 0
-#endif
-#ifndef RO_LEAF_CACHE
-#define RO_LEAF_CACHE 0
 #endif
 #ifndef RO_LOD_INC
 #define RO_LOD_INC 1
@@ -567,50 +569,71 @@ struct SampleCtx {
 // Per-frame node classes for the residency walk (kernels.py:444-517).
 // A node is "plain" for channel ci when the reference's walk would just step
 // through it: valid metadata, not transparent under ci's TF (_is_empty_meta),
-// not homogeneous, and some level resident (mask != 0).  node_class[x] = 1 iff
-// x is plain for every visible channel AND x and all its ancestors are plain
-// for channel 0.  The ray caster takes a sample whose depth-dt node is class 1
-// straight to the page-table probes at dt: channel 0 walks d0..dt through
-// plain nodes, every later channel visits only the (plain) dt node -- exactly
-// dt - d0 + n_ch node visits and no request events, as the reference's walk.
-// One thread per node; ancestors are re-read (L1/L2 hits, ~0.3 M nodes at D=6).
-__global__ void __launch_bounds__(256) k_classify_nodes(const __grid_constant__ ro_frame F,
-                                                        const uint32_t *__restrict__ words,
-                                                        int m, int D, int64_t n_nodes,
-                                                        uint8_t *__restrict__ out) {
+// not homogeneous, and some level resident (mask != 0).
+//   k_classify_own:  own[x] bit ci = x is plain for channel ci.
+//   k_classify_path: path[x] byte ci = the plain bits of channel ci along the
+//     root -> x path (bit a = the depth-a ancestor, bit depth(x) = x itself);
+//     fast[x] = x is plain for every channel and x and all its ancestors are
+//     plain for channel 0.
+// A sample whose depth-dt node is fast goes straight to the page-table probes
+// at dt (channel 0 walks d0..dt through plain nodes, every later channel
+// visits only the plain dt node: dt - d0 + n_ch visits, no request events).
+// Any other sample reads path[] of its dt node once and every channel steps
+// through the plain run of its byte from the cursor, resuming the exact walk
+// at the first non-plain node (or probing at dt) -- the reference's visits
+// and request events, one 8-byte load instead of a word load per plain node.
+// path[] needs D <= 7 (8 depths per byte).
+__global__ void __launch_bounds__(256) k_classify_own(const __grid_constant__ ro_frame F,
+                                                      const uint32_t *__restrict__ words, int m,
+                                                      int64_t n_nodes, uint8_t *__restrict__ own) {
     __shared__ uint16_t eb[RO_MAX_CH][256];
     const int n_ch = F.n_ch;
     for (int i = threadIdx.x; i < n_ch * 256; i += blockDim.x)
         eb[i >> 8][i & 255] = F.ch[i >> 8].empty_below[i & 255];
     __syncthreads();
     const int eps_i = F.eps_h >= 255.0 ? 255 : (F.eps_h < 0.0 ? -1 : (int)F.eps_h);
-    auto plain = [&](int64_t node, int ci) -> bool {
-        const uint32_t w = __ldg(words + node * m + F.ch[ci].slot);
-        const int mn = (w >> 16) & 0xFF, mx = (int)(w >> 24);
-        if (mn == 255 && mx == 0) return false;        // INVALID: metadata request
-        if (mx < (int)eb[ci][mn]) return false;         // K_ZERO
-        if (mx - mn <= eps_i) return false;             // K_CONST
-        return (w & 0xFFFFu) != 0;                      // else K_MISSU
-    };
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n_nodes; x += stride) {
+        uint32_t r = 0;
+        for (int ci = 0; ci < n_ch; ++ci) {
+            const uint32_t w = __ldg(words + x * m + F.ch[ci].slot);
+            const int mn = (w >> 16) & 0xFF, mx = (int)(w >> 24);
+            const bool p = !(mn == 255 && mx == 0) &&   // INVALID: metadata request
+                           mx >= (int)eb[ci][mn] &&     // K_ZERO
+                           mx - mn > eps_i &&           // K_CONST
+                           (w & 0xFFFFu) != 0;          // K_MISSU
+            r |= (uint32_t)p << ci;
+        }
+        own[x] = (uint8_t)r;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_classify_path(int n_ch, int D, int64_t n_nodes,
+                                                       const uint8_t *__restrict__ own,
+                                                       uint8_t *__restrict__ fast,
+                                                       uint64_t *__restrict__ path) {
+    const uint32_t all = (1u << n_ch) - 1;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n_nodes; x += stride) {
         int d = 0;
         while (d < D && level_offset(d + 1) <= x) ++d;
-        bool ok = true;
-        for (int ci = 0; ci < n_ch && ok; ++ci) ok = plain(x, ci);
-        if (ok && d > 0) {
-            const int64_t local = x - level_offset(d);
-            const int side_mask = (1 << d) - 1;
-            const int nx = (int)(local & side_mask), ny = (int)((local >> d) & side_mask),
-                      nz = (int)(local >> (2 * d));
-            for (int a = d - 1; a >= 0 && ok; --a) {
-                const int sh = d - a;
-                const int64_t anc = level_offset(a) +
-                                    ((((int64_t)(nz >> sh) << a) + (ny >> sh)) << a) + (nx >> sh);
-                ok = plain(anc, 0);
-            }
+        const int64_t local = x - level_offset(d);
+        const int side_mask = (1 << d) - 1;
+        const int nx = (int)(local & side_mask), ny = (int)((local >> d) & side_mask),
+                  nz = (int)(local >> (2 * d));
+        const uint32_t ox = __ldg(own + x);
+        uint32_t ch0 = ox & 1u;  // channel 0 plain along the whole path
+        uint64_t pc = 0;
+        for (int a = d; a >= 0; --a) {
+            const int sh = d - a;
+            const uint32_t oa = a == d ? ox
+                : __ldg(own + level_offset(a) +
+                        ((((int64_t)(nz >> sh) << a) + (ny >> sh)) << a) + (nx >> sh));
+            ch0 &= oa;
+            for (int ci = 0; ci < n_ch; ++ci) pc |= (uint64_t)((oa >> ci) & 1u) << (8 * ci + a);
         }
-        out[x] = ok ? 1 : 0;
+        fast[x] = (ox == all && (ch0 & 1u)) ? 1 : 0;
+        if (path != nullptr) path[x] = pc;
     }
 }
 
@@ -820,13 +843,6 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
     // recomputed when t / t0 reaches the next level's threshold
     int raw_c = 0;
     double next_thr = -1.0;
-#endif
-#if RO_LEAF_CACHE
-    // the last node word vector / class read by this ray (frame-constant
-    // state: reusable by the next sample in the same node)
-    int cur_node = -1, cls_node = -1;
-    bool cls_fast = false;
-    uint4 wv = make_uint4(0, 0, 0, 0);
 #endif
     [[maybe_unused]] int n_probe = 0;  // CHECK: cursor-resolved samples (max_samples)
 
@@ -1098,27 +1114,22 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                 if (d > dt_) d = dt_;
                 bool all_cz = true;
                 int ix = 0, iy = 0, iz = 0;
-#if !RO_LEAF_CACHE
                 int cur_node = -1;
                 uint4 wv = make_uint4(0, 0, 0, 0);
-#endif
                 const int d0 = d;
-                // pre-classified depth-dt node (k_classify_nodes): every
-                // channel reaches dt through plain nodes and probes there
+                // pre-classified depth-dt node (k_classify_path): every
+                // channel reaches dt through plain nodes and probes there;
+                // otherwise its path class drives the walk below
                 bool fast = false;
-                if (A.node_class != nullptr) {
+                uint64_t pcls = 0;
+                if (A.node_fast != nullptr) {
                     const int sh = D - dt_;
                     const int lx = qx >> sh, lyy = qy >> sh, lz = qz >> sh;
                     const int leaf = S.lvl_off[dt_] + (((lz << dt_) + lyy) << dt_) + lx;
                     RO_ASSERT(leaf >= 0 && leaf < A.L.num_nodes);
-#if RO_LEAF_CACHE
-                    if (leaf != cls_node) {
-                        cls_node = leaf;
-                        cls_fast = __ldg(A.node_class + leaf) != 0;
-                    }
-                    fast = cls_fast;
-#else
-                    fast = __ldg(A.node_class + leaf) != 0;
+                    fast = __ldg(A.node_fast + leaf) != 0;
+#if RO_PATH_EAGER
+                    if (A.node_path != nullptr) pcls = __ldg(A.node_path + leaf);
 #endif
                     if (fast) {
                         c_steps += dt_ - d0 + n_ch;
@@ -1130,6 +1141,11 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                             wv = ld_meta4(reinterpret_cast<const uint4 *>(A.words) + leaf);
                         cur_node = leaf;
                     }
+#if !RO_PATH_EAGER
+                    else if (A.node_path != nullptr) {
+                        pcls = __ldg(A.node_path + leaf);
+                    }
+#endif
                 }
 #if RO_FAST_DESCENT
                 // Channel 0 walks d0 -> dt through nodes known up front (the
@@ -1139,7 +1155,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                 // resident); the generic loop below resumes exactly there.  Any
                 // INVALID ancestor (it would issue a metadata request) stops the
                 // fast walk at that node, so requests stay in program order.
-                if (!fast && dt_ - d0 >= 1 && dt_ - d0 <= kFastDepth) {
+                if (!fast && A.node_path == nullptr && dt_ - d0 >= 1 && dt_ - d0 <= kFastDepth) {
                     const int slot0 = CH_SLOT(0);
                     uint32_t pw[kFastDepth];
 #pragma unroll
@@ -1220,6 +1236,15 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                         mask = (vec4 ? word_of_slot(wv, slot)
                                      : __ldg(A.words + cur_node * m + slot)) & 0xFFFFu;
                     } else {
+                    // step through the plain run of ci's path class from the
+                    // cursor: those visits neither request nor terminate
+                    if (d < dt_) {
+                        const uint32_t pm = (uint32_t)(pcls >> (8 * ci)) & 0xFFu;
+                        int t = d + __ffs(~(pm >> d)) - 1;
+                        if (t > dt_) t = dt_;
+                        c_steps += t - d;
+                        d = t;
+                    }
                     bool probe = false;
                     while (true) {
                         const int sh = D - d;
@@ -1650,7 +1675,8 @@ int warm_b() {
 
 int raycast_warm(ro_ctx *c) {
     cudaFuncAttributes fa;
-    RO_CUDA(cudaFuncGetAttributes(&fa, k_classify_nodes));
+    RO_CUDA(cudaFuncGetAttributes(&fa, k_classify_own));
+    RO_CUDA(cudaFuncGetAttributes(&fa, k_classify_path));
     RO_CUDA(cudaFuncGetAttributes(&fa, k_gather_rows));
     const int *b = c->layout.brick;
     if (b[0] == 32 && b[1] == 32 && b[2] == 32) return warm_b<32, 32, 32>();
@@ -1741,7 +1767,8 @@ int render(ro_ctx *c, const ro_frame *F, const ro_state *st,
     A.sub_max = sub_ok ? st->sub_max : nullptr;
     A.nsb = sub_ok ? (c->layout.brick[0] >> RO_SUB_LOG) * (c->layout.brick[1] >> RO_SUB_LOG) *
                          (c->layout.brick[2] >> RO_SUB_LOG) : 0;
-    A.node_class = nullptr;
+    A.node_fast = nullptr;
+    A.node_path = nullptr;
     A.local_rows = (int32_t)ro_local_rows(F->height, F->n_parts, F->part, F->tile_rows);
     if (!F->shared_outputs) {  // shared outputs are cleared once by their owner
         RO_CUDA(cudaMemsetAsync(out->required, 0, (size_t)c->E, s));
@@ -1759,14 +1786,17 @@ int render(ro_ctx *c, const ro_frame *F, const ro_state *st,
     c->keys_dirty = true;
     if (A.local_rows == 0) return RO_OK;
     RO_CUDA(cudaMemsetAsync(A.tile_counter, 0, sizeof(int32_t), s));
-    if (F->mode == RO_MODE_RESIDENCY && c->node_class != nullptr && st->words != nullptr) {
+    if (F->mode == RO_MODE_RESIDENCY && c->node_fast != nullptr && st->words != nullptr) {
         int64_t blocks = (c->num_nodes + 255) / 256;
         if (blocks > 148 * 8) blocks = 148 * 8;
-        k_classify_nodes<<<(unsigned)blocks, 256, 0, s>>>(*F, st->words, c->layout.m,
-                                                           c->layout.depth, c->num_nodes,
-                                                           c->node_class);
+        k_classify_own<<<(unsigned)blocks, 256, 0, s>>>(*F, st->words, c->layout.m,
+                                                         c->num_nodes, c->node_own);
+        k_classify_path<<<(unsigned)blocks, 256, 0, s>>>(F->n_ch, c->layout.depth, c->num_nodes,
+                                                          c->node_own, c->node_fast,
+                                                          c->node_path);
         RO_CUDA(cudaGetLastError());
-        A.node_class = c->node_class;
+        A.node_fast = c->node_fast;
+        A.node_path = c->node_path;
     }
     cudaError_t e;
     if (F->mode == RO_MODE_REFERENCE) {

@@ -31,8 +31,8 @@ REGIONS = [
     ("baseline modes", "            if (MODE == RO_MODE_PAGETABLE)", "                // kernels.py:431-558 -- one cursor shared"),
     ("residency: leaf class", "                // kernels.py:431-558 -- one cursor shared", "#if RO_FAST_DESCENT"),
     ("residency: slow descent", "#if RO_FAST_DESCENT", "                // Fast path, channels 0..3"),
-    ("residency: prefetch", "                // Fast path, channels 0..3", "#pragma unroll 1\n                for (int ci = 0; ci < n_ch; ++ci) {\n#if RO_CHI"),
-    ("residency: channel loop head + walk", "#pragma unroll 1\n                for (int ci = 0; ci < n_ch; ++ci) {\n#if RO_CHI", "                    // at traversal depth: probe the desired brick"),
+    ("residency: prefetch", "                // Fast path, channels 0..3", "                // one channel of the sample, in the reference's channel order"),
+    ("residency: channel loop head + walk", "                // one channel of the sample, in the reference's channel order", "                    // at traversal depth: probe the desired brick"),
     ("residency: probe + request", "                    // at traversal depth: probe the desired brick", "                        // nearest resident level in this node"),
     ("residency: substitute call", "                        // nearest resident level in this node", "            if (skippable) {"),
     ("skip loop", "            if (skippable) {", "            } else {\n                stall = 0;"),
