@@ -199,7 +199,8 @@ struct ro_ctx {
     // k_classify_nodes): [num_nodes] bytes, allocated with the context
     // per-frame node classes (k_classify_own / k_classify_path): own plain
     // bits, the fast flag, the path classes (depth <= 7 only)
-    uint8_t *node_own = nullptr, *node_fast = nullptr;
+    uint16_t *node_own = nullptr;
+    uint8_t *node_fast = nullptr;
     uint64_t *node_path = nullptr;
     // a ray-cast pass left first-seen keys that no ro_feedback_collect has
     // consumed (and reset) yet

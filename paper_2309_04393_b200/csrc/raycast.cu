@@ -78,9 +78,10 @@
 #ifndef RO_PREFETCH
 #define RO_PREFETCH 0
 #endif
-// load the path class alongside the fast flag (1) or only for non-fast samples (0)
-#ifndef RO_PATH_EAGER
-#define RO_PATH_EAGER 0
+// path classes also carry each channel's ZERO nodes: a walk ending on one
+// terminates without reading the node's word (1)
+#ifndef RO_PATH_ZERO
+#define RO_PATH_ZERO 1
 #endif
 // brick-run histogram (1) or a histogram increment per fetch (0)
 #ifndef RO_RUNLEN
@@ -570,9 +571,11 @@ struct SampleCtx {
 // A node is "plain" for channel ci when the reference's walk would just step
 // through it: valid metadata, not transparent under ci's TF (_is_empty_meta),
 // not homogeneous, and some level resident (mask != 0).
-//   k_classify_own:  own[x] bit ci = x is plain for channel ci.
+//   k_classify_own:  own[x] bit ci = x is plain for channel ci, bit 8 + ci =
+//     x is ZERO for ci (valid and transparent: the walk ends there).
 //   k_classify_path: path[x] byte ci = the plain bits of channel ci along the
-//     root -> x path (bit a = the depth-a ancestor, bit depth(x) = x itself);
+//     root -> x path (bit a = the depth-a ancestor, bit depth(x) = x itself)
+//     and, with at most 4 channels, byte 4 + ci the same for the ZERO bits;
 //     fast[x] = x is plain for every channel and x and all its ancestors are
 //     plain for channel 0.
 // A sample whose depth-dt node is fast goes straight to the page-table probes
@@ -581,11 +584,12 @@ struct SampleCtx {
 // Any other sample reads path[] of its dt node once and every channel steps
 // through the plain run of its byte from the cursor, resuming the exact walk
 // at the first non-plain node (or probing at dt) -- the reference's visits
-// and request events, one 8-byte load instead of a word load per plain node.
+// and request events, one 8-byte load instead of a word load per plain node
+// (and, up to 4 channels, none for a ZERO terminal).
 // path[] needs D <= 7 (8 depths per byte).
 __global__ void __launch_bounds__(256) k_classify_own(const __grid_constant__ ro_frame F,
                                                       const uint32_t *__restrict__ words, int m,
-                                                      int64_t n_nodes, uint8_t *__restrict__ own) {
+                                                      int64_t n_nodes, uint16_t *__restrict__ own) {
     __shared__ uint16_t eb[RO_MAX_CH][256];
     const int n_ch = F.n_ch;
     for (int i = threadIdx.x; i < n_ch * 256; i += blockDim.x)
@@ -598,18 +602,19 @@ __global__ void __launch_bounds__(256) k_classify_own(const __grid_constant__ ro
         for (int ci = 0; ci < n_ch; ++ci) {
             const uint32_t w = __ldg(words + x * m + F.ch[ci].slot);
             const int mn = (w >> 16) & 0xFF, mx = (int)(w >> 24);
-            const bool p = !(mn == 255 && mx == 0) &&   // INVALID: metadata request
-                           mx >= (int)eb[ci][mn] &&     // K_ZERO
+            const bool valid = !(mn == 255 && mx == 0);  // else INVALID: metadata request
+            const bool zero = valid && mx < (int)eb[ci][mn];  // K_ZERO
+            const bool p = valid && !zero &&
                            mx - mn > eps_i &&           // K_CONST
                            (w & 0xFFFFu) != 0;          // K_MISSU
-            r |= (uint32_t)p << ci;
+            r |= ((uint32_t)p << ci) | ((uint32_t)zero << (8 + ci));
         }
-        own[x] = (uint8_t)r;
+        own[x] = (uint16_t)r;
     }
 }
 
 __global__ void __launch_bounds__(256) k_classify_path(int n_ch, int D, int64_t n_nodes,
-                                                       const uint8_t *__restrict__ own,
+                                                       const uint16_t *__restrict__ own,
                                                        uint8_t *__restrict__ fast,
                                                        uint64_t *__restrict__ path) {
     const uint32_t all = (1u << n_ch) - 1;
@@ -623,17 +628,20 @@ __global__ void __launch_bounds__(256) k_classify_path(int n_ch, int D, int64_t 
                   nz = (int)(local >> (2 * d));
         const uint32_t ox = __ldg(own + x);
         uint32_t ch0 = ox & 1u;  // channel 0 plain along the whole path
-        uint64_t pc = 0;
+        uint64_t pc = 0, zc = 0;
         for (int a = d; a >= 0; --a) {
             const int sh = d - a;
             const uint32_t oa = a == d ? ox
                 : __ldg(own + level_offset(a) +
                         ((((int64_t)(nz >> sh) << a) + (ny >> sh)) << a) + (nx >> sh));
             ch0 &= oa;
-            for (int ci = 0; ci < n_ch; ++ci) pc |= (uint64_t)((oa >> ci) & 1u) << (8 * ci + a);
+            for (int ci = 0; ci < n_ch; ++ci) {
+                pc |= (uint64_t)((oa >> ci) & 1u) << (8 * ci + a);
+                zc |= (uint64_t)((oa >> (8 + ci)) & 1u) << (8 * ci + a);
+            }
         }
-        fast[x] = (ox == all && (ch0 & 1u)) ? 1 : 0;
-        if (path != nullptr) path[x] = pc;
+        fast[x] = ((ox & 0xFFu) == all && (ch0 & 1u)) ? 1 : 0;
+        if (path != nullptr) path[x] = n_ch <= 4 ? pc | (zc << 32) : pc;
     }
 }
 
@@ -1113,7 +1121,6 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                 if (F.start_level < d) d = F.start_level;
                 if (d > dt_) d = dt_;
                 bool all_cz = true;
-                int ix = 0, iy = 0, iz = 0;
                 int cur_node = -1;
                 uint4 wv = make_uint4(0, 0, 0, 0);
                 const int d0 = d;
@@ -1128,24 +1135,15 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                     const int leaf = S.lvl_off[dt_] + (((lz << dt_) + lyy) << dt_) + lx;
                     RO_ASSERT(leaf >= 0 && leaf < A.L.num_nodes);
                     fast = __ldg(A.node_fast + leaf) != 0;
-#if RO_PATH_EAGER
-                    if (A.node_path != nullptr) pcls = __ldg(A.node_path + leaf);
-#endif
                     if (fast) {
                         c_steps += dt_ - d0 + n_ch;
                         d = dt_;
-                        ix = lx;
-                        iy = lyy;
-                        iz = lz;
                         if (vec4 && leaf != cur_node)
                             wv = ld_meta4(reinterpret_cast<const uint4 *>(A.words) + leaf);
                         cur_node = leaf;
-                    }
-#if !RO_PATH_EAGER
-                    else if (A.node_path != nullptr) {
+                    } else if (A.node_path != nullptr) {
                         pcls = __ldg(A.node_path + leaf);
                     }
-#endif
                 }
 #if RO_FAST_DESCENT
                 // Channel 0 walks d0 -> dt through nodes known up front (the
@@ -1238,20 +1236,30 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                     } else {
                     // step through the plain run of ci's path class from the
                     // cursor: those visits neither request nor terminate
-                    if (d < dt_) {
-                        const uint32_t pm = (uint32_t)(pcls >> (8 * ci)) & 0xFFu;
-                        int t = d + __ffs(~(pm >> d)) - 1;
-                        if (t > dt_) t = dt_;
+                    {
+                        int t = d;
+                        if (d < dt_) {
+                            const uint32_t pm = (uint32_t)(pcls >> (8 * ci)) & 0xFFu;
+                            t = d + __ffs(~(pm >> d)) - 1;
+                            if (t > dt_) t = dt_;
+                        }
+#if RO_PATH_ZERO
+                        // a ZERO node there: the walk ends on it (K_ZERO)
+                        if (n_ch <= 4 && ((pcls >> (32 + 8 * ci + t)) & 1u)) {
+                            c_steps += t - d + 1;
+                            d = t;
+                            zero_mask |= 1u << ci;
+                            return;
+                        }
+#endif
                         c_steps += t - d;
                         d = t;
                     }
                     bool probe = false;
                     while (true) {
                         const int sh = D - d;
-                        ix = qx >> sh;
-                        iy = qy >> sh;
-                        iz = qz >> sh;
-                        const int nidx = S.lvl_off[d] + (((iz << d) + iy) << d) + ix;
+                        const int nidx = S.lvl_off[d] +
+                            ((((qz >> sh) << d) + (qy >> sh)) << d) + (qx >> sh);
                         c_steps += 1;
                         uint32_t w;
                         if (vec4) {
@@ -1447,6 +1455,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                 if (all_cz) {
                     skippable = true;
                     const double s = 1.0 / (double)(1 << d);
+                    const int ix = qx >> (D - d), iy = qy >> (D - d), iz = qz >> (D - d);
                     skip_exit = box_exit(ox, oy, oz, dx, dy, dz, ix * s, iy * s, iz * s,
                                          (ix + 1) * s, (iy + 1) * s, (iz + 1) * s);
                 }
