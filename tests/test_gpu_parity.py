@@ -289,6 +289,44 @@ def test_gpu_partial_residency_matches_oracle(seed, eps, ranges):
         assert np.array_equal(ref.level_histogram, wr.level_histogram)
 
 
+@pytest.mark.parametrize("depth,m", [(7, 4), (8, 1), (5, 6), (4, 8)])
+def test_gpu_path_class_layouts_match_oracle(depth, m):
+    """The residency walk's per-frame node classes in every layout the ray
+    caster switches between: D <= 7 with <= 4 channels (plain + ZERO bits
+    per path), D <= 7 with 5..8 channels (plain bits only), D = 8 (no path
+    classes: fast flag + channel-0 parallel descent).  Random residency and
+    INVALID metadata; image, requests, usage, histogram and counters equal
+    the oracle's."""
+    from oracle import raycast as orc
+    from paper_2309_04393_b200 import (ChannelSettings, RenderConfig, TransferFunction,
+                                       grayscale_ramp_tf, orbit_pose, render_frame)
+    eng = _random_partial_engine(20 + depth, depth=depth, m=m)
+    tfs = [grayscale_ramp_tf(40.0),
+           TransferFunction(points=((0.0, (0, 0, 0, 0)), (20.0, (0.1, 0.9, 0.2, 0.0)),
+                                    (90.0, (1.0, 0.2, 0.1, 0.5)), (255.0, (0.2, 0.4, 1.0, 0.8)))),
+           grayscale_ramp_tf(10.0, max_alpha=0.4),
+           TransferFunction(points=((0.0, (0, 0, 0, 0)), (100.0, (1, 1, 0, 0.9)),
+                                    (101.0, (0, 0, 0, 0)), (255.0, (0, 0, 0, 0))))]
+    chans = [ChannelSettings(slot=s, tf=tfs[s % 4], level_range=(s % 2, 2)) for s in range(m)]
+    ost = oracle_state_from_device(eng)
+    och = [orc.OracleChannel(slot=c.slot, points=c.tf.points, level_range=c.level_range)
+           for c in chans]
+    for angle, dims, step, budget in ((0.4, (48, 40), 1 / 80, 60), (3.3, (40, 32), 1 / 200, 500)):
+        cfg = RenderConfig(image_dims=dims, base_step=step, max_requests_per_frame=budget,
+                           traversal_start_level=min(depth, 2))
+        pose = orbit_pose(angle, radius=1.7)
+        out = render_frame(eng.paging, eng.octree, chans, pose, cfg)
+        want = orc.render(ost, och, cam_tuple(pose), dims, step, budget=budget,
+                          start_level=cfg.traversal_start_level)
+        assert np.array_equal(out.image, want.image), int((out.image != want.image).sum())
+        assert out.brick_requests == want.brick_requests
+        assert out.metadata_requests == want.metadata_requests
+        assert np.array_equal(out.required_mask, want.required_mask)
+        assert np.array_equal(out.level_histogram, want.level_histogram)
+        assert [out.stats.traversal_steps, out.stats.samples_evaluated,
+                out.stats.samples_skipped] == list(want.counters[:3])
+
+
 def test_gpu_wide_request_keys_match_oracle():
     """Request keys wider than 32 bits end to end: a 4096x2048 frame (pixel
     index >= 2^22) whose rows 1024..1031 are rendered (sort-first part 128
