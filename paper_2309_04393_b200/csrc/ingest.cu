@@ -35,6 +35,12 @@ constexpr int kLz4Warps = 4;  // warps (frames) per CTA (one-warp decoder)
 #ifndef RO_LZ4_PIPE
 #define RO_LZ4_PIPE 1
 #endif
+#ifndef RO_LZ4_MAP
+#define RO_LZ4_MAP 1
+#endif
+#ifndef RO_LZ4_FAST
+#define RO_LZ4_FAST 1
+#endif
 
 enum : int32_t {
     LZ4_OK = 0,
@@ -424,6 +430,352 @@ k_lz4_decode_pipe(int64_t n, const uint8_t *__restrict__ src, const int64_t *__r
     }
 }
 
+// ---- one-CTA decode through a source map (bricks up to 32 KB) ---------------
+// The pipe decoder executes the sequences strictly in order, one record per
+// warp step, behind a parser whose every step is a chain of dependent byte
+// reads: a noise-floor brick of ~6,700 sequences takes ~1.8 ms however many
+// SMs are idle.  Here the whole CTA decodes one frame and only one dependent
+// load per sequence stays serial:
+//   A. every byte position p of the block is parsed AS IF a sequence started
+//      there (all threads): next[p] = where the following token would be
+//      (or "impossible"), next2[p] = next[next[p]];
+//   B. one thread follows the chain from position 0 -- one shared-memory
+//      load per TWO sequences -- and marks the true sequence starts;
+//   C. all threads re-parse the marked sequences, place them with a CTA
+//      prefix sum of their lengths, and write a SOURCE per output byte:
+//      literal j of the frame (flagged) or output byte op - offset (a match;
+//      overlapping matches just point a few bytes back), checking offsets
+//      against the output position;
+//   D. pointer jumping (map[i] = map[map[i]]) until every byte points at a
+//      literal, O(log chain) rounds, then one parallel gather writes the
+//      brick.
+// Frames of anything but one data block (+ EndMark), any position the
+// fast path cannot vouch for, or any malformed sequence re-run the serial
+// parser over the whole frame (MapSink, warp 0), which yields the exact
+// LZ4_E_* code -- the accept / reject set and the bytes are the serial
+// decoder's.
+constexpr uint32_t kLitRef = 0x80000000u;
+constexpr int kMapThreads = 512;
+constexpr int64_t kFallback = -100;  // internal: re-run the serial parser
+
+struct MapSink {
+    uint32_t *map;
+    int lane;
+    __device__ void seq(int64_t lit_at, int64_t lit, int64_t off, int64_t ml, int64_t op) {
+        const int o = (int)op, la = (int)lit_at, l = (int)lit;
+        for (int q = lane; q < l; q += 32) map[o + q] = kLitRef | (uint32_t)(la + q);
+        if (!ml) return;
+        const int mo = o + l, of = (int)off, m = (int)ml;
+        for (int j = lane; j < m; j += 32) map[mo + j] = (uint32_t)(mo + j - of);
+    }
+    __device__ bool content_ok(int64_t, uint32_t) { return true; }  // checked after the gather
+};
+
+// One sequence parsed at block position p (block bytes b[0, bl)).  Returns
+// false when no valid sequence can start there.  last = the block ends right
+// after its literals.  A non-last sequence ending exactly at bl is invalid
+// (the next token read would overrun), as in lz4_block_parse.
+__device__ __forceinline__ bool seq_at(const uint8_t *b, int bl, int p, int cap, int &lit_at,
+                                       int &lit, int &off, int &ml, int &nx, bool &last) {
+    const uint32_t token = b[p];
+    int q = p + 1;
+    lit = (int)(token >> 4);
+    if (lit == 15) {
+        uint32_t x;
+        do {
+            if (q >= bl || lit > cap) return false;
+            x = b[q++];
+            lit += (int)x;
+        } while (x == 255);
+    }
+    if (lit > cap || q + lit > bl) return false;
+    lit_at = q;
+    q += lit;
+    if (q == bl) {
+        last = true;
+        off = 0;
+        ml = 0;
+        nx = bl;
+        return true;
+    }
+    last = false;
+    if (q + 2 > bl) return false;
+    off = (int)b[q] | ((int)b[q + 1] << 8);
+    q += 2;
+    ml = (int)(token & 15);
+    if (ml == 15) {
+        uint32_t x;
+        do {
+            if (q >= bl || ml > cap) return false;
+            x = b[q++];
+            ml += (int)x;
+        } while (x == 255);
+    }
+    ml += 4;
+    if (lit + ml > cap || q >= bl) return false;
+    nx = q;
+    return true;
+}
+
+// exclusive prefix sum over the CTA (kMapThreads threads); *total = the sum
+__device__ __forceinline__ int cta_exclusive_scan(int v, int *scratch, int *total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, d);
+        if (lane >= d) x += y;
+    }
+    if (lane == 31) scratch[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        int w = lane < kMapThreads / 32 ? scratch[lane] : 0;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, w, d);
+            if (lane >= d) w += y;
+        }
+        if (lane < kMapThreads / 32) scratch[lane] = w;  // inclusive warp totals
+    }
+    __syncthreads();
+    const int before = (warp ? scratch[warp - 1] : 0) + x - v;
+    *total = scratch[kMapThreads / 32 - 1];
+    __syncthreads();  // scratch reusable
+    return before;
+}
+
+// Phases A-C for one compressed block at frame offset bpos (whole CTA).
+// The map region (u32[pcap]) first holds next[] and next2[] (u16 each; the
+// top bit of next[] marks true sequence starts), then the map.  Returns the
+// output end or kFallback.
+__device__ int64_t block_fast(const uint8_t *fin, int bpos, int bl, int op0, int low, int limit,
+                              uint32_t *map, int pcap, int *s_bad, int *scan) {
+    const uint8_t *b = fin + bpos;
+    const int tid = threadIdx.x;
+    const int cap = limit - op0;
+    constexpr uint32_t kErr = 0x7FFF, kMark = 0x8000;
+    if (bl < 1 || bl >= (int)kErr || bl > pcap || cap > 0xFFFF) return kFallback;
+    uint16_t *nx1 = reinterpret_cast<uint16_t *>(map);
+    uint16_t *nx2 = nx1 + pcap;
+    // A: where the next token would be if a sequence started at p (bl: the
+    // block ends after p's literals; kErr: no valid sequence at p)
+    for (int p = tid; p < bl; p += kMapThreads) {
+        int la, l, o, m, nx;
+        bool last;
+        nx1[p] = (uint16_t)(seq_at(b, bl, p, cap, la, l, o, m, nx, last) ? nx : kErr);
+    }
+    __syncthreads();
+    for (int p = tid; p < bl; p += kMapThreads) {
+        const uint32_t q = nx1[p];
+        nx2[p] = (uint16_t)(q < (uint32_t)bl ? nx1[q] : q);
+    }
+    __syncthreads();
+    // B: the true chain from position 0, two sequences per dependent load;
+    // every start is marked in next[]
+    if (tid == 0) {
+        uint32_t s = 0;
+        int bad = 0;
+        while (true) {
+            const uint32_t a1 = nx1[s], a2 = nx2[s];
+            nx1[s] = (uint16_t)(a1 | kMark);
+            if (a1 >= (uint32_t)bl) { bad = a1 != (uint32_t)bl; break; }
+            nx1[a1] = (uint16_t)(a2 | kMark);  // nx1[a1] == a2
+            if (a2 >= (uint32_t)bl) { bad = a2 != (uint32_t)bl; break; }
+            s = a2;
+        }
+        *s_bad = bad;
+    }
+    __syncthreads();
+    if (*s_bad) return kFallback;
+    // C: output offsets of the marked starts (CTA scan over position chunks),
+    // then the sources of every output byte
+    constexpr int kChunk = 64;  // bl <= 32 K positions over 512 threads
+    const int c0 = tid * kChunk, c1 = min(bl, c0 + kChunk);
+    uint64_t marks = 0;
+    int sum = 0;
+    for (int p = c0; p < c1; ++p) {
+        if (nx1[p] & kMark) {
+            marks |= 1ull << (p - c0);
+            int la, l, of, m, nx;
+            bool last;
+            seq_at(b, bl, p, cap, la, l, of, m, nx, last);
+            sum += l + m;
+        }
+    }
+    int total;
+    int o = op0 + cta_exclusive_scan(sum, scan, &total);  // also orders the reads above
+    if (total > cap) return kFallback;
+    int bad = 0;
+    while (marks) {
+        const int p = c0 + __ffsll((long long)marks) - 1;
+        marks &= marks - 1;
+        int la, l, of, m, nx;
+        bool last;
+        seq_at(b, bl, p, cap, la, l, of, m, nx, last);
+        const uint32_t lsrc = (uint32_t)(bpos + la);
+        for (int q = 0; q < l; ++q) map[o + q] = kLitRef | (lsrc + q);
+        o += l;
+        if (!last) {
+            if (of == 0 || of > o - low) bad = 1;
+            for (int q = 0; q < m; ++q) map[o + q] = (uint32_t)(o + q - of);
+            o += m;
+        }
+    }
+    if (__syncthreads_or(bad)) return kFallback;
+    return op0 + total;
+}
+
+// The frame when it is exactly [header][one block][EndMark][checksums]: all
+// threads walk the header (validated as lz4_frame_parse does); the block is
+// decoded by block_fast, a raw block mapped directly.
+__device__ int64_t frame_fast(const uint8_t *src, int64_t len, int64_t cap, uint32_t *P,
+                              int pcap, int *s_bad, int *scan, int64_t *cchk_at) {
+    if (len < 7 || rd32(src) != 0x184D2204u) return kFallback;
+    const uint32_t flg = src[4], bd = src[5];
+    if ((flg >> 6) != 1 || (flg & 0x02) || (bd & 0x8F)) return kFallback;
+    const int bsid = (bd >> 4) & 7;
+    if (bsid < 4) return kFallback;
+    const int64_t bmax = (int64_t)1 << (8 + 2 * bsid);
+    const bool bchk = flg & 0x10, has_size = flg & 0x08, cchk = flg & 0x04,
+               has_dict = flg & 0x01;
+    int64_t pos = 6, csize = -1;
+    if (has_size) {
+        if (len < pos + 8) return kFallback;
+        csize = (int64_t)rd32(src + pos) | ((int64_t)rd32(src + pos + 4) << 32);
+        pos += 8;
+    }
+    if (has_dict) pos += 4;
+    if (len < pos + 1) return kFallback;
+    if (((xxh32(src + 4, pos - 4, 0) >> 8) & 0xFF) != src[pos]) return kFallback;
+    pos += 1;
+    if (pos + 4 > len) return kFallback;
+    const uint32_t bs = rd32(src + pos);
+    pos += 4;
+    int64_t op = 0;
+    if (bs != 0) {
+        const bool raw = bs >> 31;
+        const int64_t bl = bs & 0x7FFFFFFFu;
+        if (bl > bmax || pos + bl + (bchk ? 4 : 0) + 4 > len) return kFallback;
+        if (bchk && xxh32(src + pos, bl, 0) != rd32(src + pos + bl)) return kFallback;
+        const int64_t limit = min(cap, bmax);
+        if (raw) {
+            if (bl > limit) return kFallback;
+            for (int q = threadIdx.x; q < (int)bl; q += kMapThreads)
+                P[q] = kLitRef | (uint32_t)(pos + q);
+            op = bl;
+        } else {
+            op = block_fast(src, (int)pos, (int)bl, 0, 0, (int)limit, P, pcap, s_bad, scan);
+            if (op < 0) return kFallback;
+        }
+        pos += bl + (bchk ? 4 : 0);
+        if (rd32(src + pos) != 0) return kFallback;  // a second block: serial path
+        pos += 4;
+    }
+    if (cchk) {
+        if (pos + 4 > len) return kFallback;
+        *cchk_at = pos;
+        pos += 4;
+    }
+    if (has_size && op != csize) return kFallback;
+    if (pos != len) return kFallback;
+    return op;
+}
+
+__global__ void __launch_bounds__(kMapThreads)
+k_lz4_decode_map(int64_t n, const uint8_t *__restrict__ src, const int64_t *__restrict__ off,
+                 uint8_t *__restrict__ dst, int64_t stride, int64_t expected,
+                 int32_t *__restrict__ status, int32_t *__restrict__ first_bad,
+                 int64_t fin_cap, int pcap) {
+    extern __shared__ __align__(16) uint8_t sh[];
+    uint32_t *map = reinterpret_cast<uint32_t *>(sh);
+    uint8_t *fin = reinterpret_cast<uint8_t *>(map + pcap);  // 16-byte aligned
+    __shared__ long long s_result, s_cchk;
+    __shared__ int s_bad, s_scan[kMapThreads / 32];
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int64_t i = blockIdx.x;
+    if (i >= n) return;
+    const int64_t o0 = off[0];
+    const int64_t a = off[i] - o0, b = off[i + 1] - o0;
+    const uint8_t *f = src + a;
+    const bool staged = b >= a && b - a <= fin_cap;
+    if (staged) {
+        const int64_t len = b - a;
+        for (int64_t j = tid; j < len; j += kMapThreads) fin[j] = f[j];
+        for (int64_t j = len + tid; j < len + 16; j += kMapThreads) fin[j] = 0;  // window slack
+        f = fin;
+    }
+    __syncthreads();
+    int64_t cchk = -1;
+    int64_t r = kFallback;
+#if RO_LZ4_FAST
+    if (staged) r = frame_fast(f, b - a, stride, map, pcap, &s_bad, s_scan, &cchk);
+#endif
+    if (r == kFallback) {
+        __syncthreads();
+        if (tid < 32) {
+            MapSink sink{map, lane};
+            int64_t rr;
+            cchk = -1;
+            if (b < a)
+                rr = LZ4_E_TRUNCATED;
+            else if (staged)
+                rr = lz4_frame_parse(f, b - a, stride, sink, &cchk,
+                                     SmemBytes{reinterpret_cast<const uint32_t *>(fin)});
+            else
+                rr = lz4_frame_parse(f, b - a, stride, sink, &cchk);
+            if (lane == 0) {
+                s_result = rr;
+                s_cchk = cchk;
+            }
+        }
+        __syncthreads();
+        r = s_result;
+        cchk = s_cchk;
+    }
+    if (r >= 0 && expected >= 0 && r != expected) r = LZ4_E_SIZE;
+    if (r >= 0) {
+        const int nr = (int)r;
+        // pointer jumping: every entry ends on a literal reference.  An entry
+        // read while another thread rewrites it is either value -- both lie
+        // on the same chain -- so rounds need no ordering beyond the barrier.
+        while (true) {
+            int pending = 0;
+            for (int q = tid; q < nr; q += kMapThreads) {
+                const uint32_t v = map[q];
+                if (!(v & kLitRef)) {
+                    const uint32_t w = map[v];
+                    map[q] = w;
+                    pending |= !(w & kLitRef);
+                }
+            }
+            if (!__syncthreads_or(pending)) break;
+        }
+        uint8_t *outp = dst + i * stride;
+        if ((((uintptr_t)outp) & 3) == 0) {
+            const int n4 = nr >> 2;
+            for (int q = tid; q < n4; q += kMapThreads) {
+                const uint4 m4 = reinterpret_cast<const uint4 *>(map)[q];
+                const uint32_t v = (uint32_t)f[m4.x & ~kLitRef] |
+                                   ((uint32_t)f[m4.y & ~kLitRef] << 8) |
+                                   ((uint32_t)f[m4.z & ~kLitRef] << 16) |
+                                   ((uint32_t)f[m4.w & ~kLitRef] << 24);
+                reinterpret_cast<uint32_t *>(outp)[q] = v;
+            }
+            for (int q = (n4 << 2) + tid; q < nr; q += kMapThreads) outp[q] = f[map[q] & ~kLitRef];
+        } else {
+            for (int q = tid; q < nr; q += kMapThreads) outp[q] = f[map[q] & ~kLitRef];
+        }
+        if (cchk >= 0) {  // content checksum over the written brick
+            __syncthreads();
+            if (xxh32(outp, r, 0) != rd32(f + cchk)) r = LZ4_E_CHECKSUM;
+        }
+    }
+    if (tid == 0) {
+        status[i] = r < 0 ? (int32_t)r : 0;
+        if (r < 0 && first_bad) atomicMin(first_bad, (int32_t)i);
+    }
+}
+
 __global__ void __launch_bounds__(32 * kLz4Warps)
 k_lz4_decode(int64_t n, const uint8_t *__restrict__ src, const int64_t *__restrict__ off,
              uint8_t *__restrict__ dst, int64_t stride, int64_t expected,
@@ -576,6 +928,32 @@ int lz4_decode(ro_ctx *c, const uint8_t *src, const int64_t *off, int64_t n, uin
                cudaStream_t s) {
     (void)c;
     if (n <= 0) return RO_OK;
+#if RO_LZ4_MAP
+    // Small batches of bricks up to 32 KB: one CTA per frame
+    // (k_lz4_decode_map: parallel parse + serial chain + pointer jumping)
+    if (stride <= 32 * 1024) {
+        const int64_t fin_cap = std::max<int64_t>(48 * 1024, stride + stride / 2 + 64);
+        const int pcap = (int)((std::max<int64_t>(stride, 32 * 1024) + 3) & ~(int64_t)3);
+        const size_t smem = sizeof(uint32_t) * (size_t)pcap + (size_t)fin_cap + 16;
+        int dev = 0, optin = 0, sms = 0;
+        RO_CUDA(cudaGetDevice(&dev));
+        RO_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+        RO_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        if (smem + 64 <= (size_t)optin && n <= sms) {
+            static size_t attr = 0;
+            if (attr < smem) {
+                RO_CUDA(cudaFuncSetAttribute(k_lz4_decode_map,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem));
+                attr = smem;
+            }
+            k_lz4_decode_map<<<(unsigned)n, kMapThreads, smem, s>>>(
+                n, src, off, dst, stride, expected, status, first_bad, fin_cap, pcap);
+            RO_CUDA(cudaGetLastError());
+            return RO_OK;
+        }
+    }
+#endif
 #if RO_LZ4_PIPE
     // Small batches (one wave of resident CTAs) are latency-bound: the
     // pipelined two-warp decoder finishes a brick sooner.  Larger batches are
