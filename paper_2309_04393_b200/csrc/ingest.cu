@@ -438,10 +438,10 @@ k_lz4_decode_pipe(int64_t n, const uint8_t *__restrict__ src, const int64_t *__r
 // load per sequence stays serial:
 //   A. every byte position p of the block is parsed AS IF a sequence started
 //      there (all threads): next[p] = where the following token would be
-//      (or "impossible"), next2[p] = next[next[p]];
+//      (or "impossible"), next2[p] = next[next[p]], next4[p] likewise;
 //   B. one thread follows the chain from position 0 -- one shared-memory
-//      load per TWO sequences -- and marks the true sequence starts;
-//   C. all threads re-parse the marked sequences, place them with a CTA
+//      load per FOUR sequences -- and marks where each group of four starts;
+//   C. all threads re-parse the marked groups, place them with a CTA
 //      prefix sum of their lengths, and write a SOURCE per output byte:
 //      literal j of the frame (flagged) or output byte op - offset (a match;
 //      overlapping matches just point a few bytes back), checking offsets
@@ -545,11 +545,12 @@ __device__ __forceinline__ int cta_exclusive_scan(int v, int *scratch, int *tota
 }
 
 // Phases A-C for one compressed block at frame offset bpos (whole CTA).
-// The map region (u32[pcap]) first holds next[] and next2[] (u16 each; the
-// top bit of next[] marks true sequence starts), then the map.  Returns the
-// output end or kFallback.
+// The map region (u32[pcap]) first holds next[] and next2[] (u16 each), nx4
+// (u16[pcap], its own region) next4[] whose top bit marks the starts of the
+// true chain's groups of four sequences; the map region then receives the
+// map.  Returns the output end or kFallback.
 __device__ int64_t block_fast(const uint8_t *fin, int bpos, int bl, int op0, int low, int limit,
-                              uint32_t *map, int pcap, int *s_bad, int *scan) {
+                              uint32_t *map, uint16_t *nx4, int pcap, int *s_bad, int *scan) {
     const uint8_t *b = fin + bpos;
     const int tid = threadIdx.x;
     const int cap = limit - op0;
@@ -558,7 +559,8 @@ __device__ int64_t block_fast(const uint8_t *fin, int bpos, int bl, int op0, int
     uint16_t *nx1 = reinterpret_cast<uint16_t *>(map);
     uint16_t *nx2 = nx1 + pcap;
     // A: where the next token would be if a sequence started at p (bl: the
-    // block ends after p's literals; kErr: no valid sequence at p)
+    // block ends after p's literals; kErr: no valid sequence at p), then
+    // two and four sequences on (bl / kErr propagate)
     for (int p = tid; p < bl; p += kMapThreads) {
         int la, l, o, m, nx;
         bool last;
@@ -570,36 +572,53 @@ __device__ int64_t block_fast(const uint8_t *fin, int bpos, int bl, int op0, int
         nx2[p] = (uint16_t)(q < (uint32_t)bl ? nx1[q] : q);
     }
     __syncthreads();
-    // B: the true chain from position 0, two sequences per dependent load;
-    // every start is marked in next[]
+    for (int p = tid; p < bl; p += kMapThreads) {
+        const uint32_t q = nx2[p];
+        nx4[p] = (uint16_t)(q < (uint32_t)bl ? nx2[q] : q);
+    }
+    __syncthreads();
+    // B: the true chain from position 0, FOUR sequences per dependent load
+    // (next4 < bl implies the three in between are valid); the group starts
+    // are marked in next4[]; the last group is checked one step at a time
     if (tid == 0) {
         uint32_t s = 0;
         int bad = 0;
         while (true) {
-            const uint32_t a1 = nx1[s], a2 = nx2[s];
-            nx1[s] = (uint16_t)(a1 | kMark);
-            if (a1 >= (uint32_t)bl) { bad = a1 != (uint32_t)bl; break; }
-            nx1[a1] = (uint16_t)(a2 | kMark);  // nx1[a1] == a2
-            if (a2 >= (uint32_t)bl) { bad = a2 != (uint32_t)bl; break; }
-            s = a2;
+            const uint32_t a4 = nx4[s];
+            nx4[s] = (uint16_t)(a4 | kMark);
+            if (a4 >= (uint32_t)bl) {
+                uint32_t c = s;
+                for (int k = 0; k < 4; ++k) {
+                    c = nx1[c];
+                    if (c >= (uint32_t)bl) break;
+                }
+                bad = c != (uint32_t)bl;
+                break;
+            }
+            s = a4;
         }
         *s_bad = bad;
     }
     __syncthreads();
     if (*s_bad) return kFallback;
-    // C: output offsets of the marked starts (CTA scan over position chunks),
+    // C: output offsets of the marked groups (CTA scan over position chunks),
     // then the sources of every output byte
     constexpr int kChunk = 64;  // bl <= 32 K positions over 512 threads
     const int c0 = tid * kChunk, c1 = min(bl, c0 + kChunk);
     uint64_t marks = 0;
     int sum = 0;
     for (int p = c0; p < c1; ++p) {
-        if (nx1[p] & kMark) {
+        if (nx4[p] & kMark) {
             marks |= 1ull << (p - c0);
-            int la, l, of, m, nx;
-            bool last;
-            seq_at(b, bl, p, cap, la, l, of, m, nx, last);
-            sum += l + m;
+            int c = p;
+            for (int k = 0; k < 4; ++k) {
+                int la, l, of, m, nx;
+                bool last;
+                seq_at(b, bl, c, cap, la, l, of, m, nx, last);
+                sum += l + m;
+                if (last) break;
+                c = nx;
+            }
         }
     }
     int total;
@@ -607,18 +626,20 @@ __device__ int64_t block_fast(const uint8_t *fin, int bpos, int bl, int op0, int
     if (total > cap) return kFallback;
     int bad = 0;
     while (marks) {
-        const int p = c0 + __ffsll((long long)marks) - 1;
+        int c = c0 + __ffsll((long long)marks) - 1;
         marks &= marks - 1;
-        int la, l, of, m, nx;
-        bool last;
-        seq_at(b, bl, p, cap, la, l, of, m, nx, last);
-        const uint32_t lsrc = (uint32_t)(bpos + la);
-        for (int q = 0; q < l; ++q) map[o + q] = kLitRef | (lsrc + q);
-        o += l;
-        if (!last) {
+        for (int k = 0; k < 4; ++k) {
+            int la, l, of, m, nx;
+            bool last;
+            seq_at(b, bl, c, cap, la, l, of, m, nx, last);
+            const uint32_t lsrc = (uint32_t)(bpos + la);
+            for (int q = 0; q < l; ++q) map[o + q] = kLitRef | (lsrc + q);
+            o += l;
+            if (last) break;
             if (of == 0 || of > o - low) bad = 1;
             for (int q = 0; q < m; ++q) map[o + q] = (uint32_t)(o + q - of);
             o += m;
+            c = nx;
         }
     }
     if (__syncthreads_or(bad)) return kFallback;
@@ -629,7 +650,7 @@ __device__ int64_t block_fast(const uint8_t *fin, int bpos, int bl, int op0, int
 // threads walk the header (validated as lz4_frame_parse does); the block is
 // decoded by block_fast, a raw block mapped directly.
 __device__ int64_t frame_fast(const uint8_t *src, int64_t len, int64_t cap, uint32_t *P,
-                              int pcap, int *s_bad, int *scan, int64_t *cchk_at) {
+                              uint16_t *nx4, int pcap, int *s_bad, int *scan, int64_t *cchk_at) {
     if (len < 7 || rd32(src) != 0x184D2204u) return kFallback;
     const uint32_t flg = src[4], bd = src[5];
     if ((flg >> 6) != 1 || (flg & 0x02) || (bd & 0x8F)) return kFallback;
@@ -664,7 +685,7 @@ __device__ int64_t frame_fast(const uint8_t *src, int64_t len, int64_t cap, uint
                 P[q] = kLitRef | (uint32_t)(pos + q);
             op = bl;
         } else {
-            op = block_fast(src, (int)pos, (int)bl, 0, 0, (int)limit, P, pcap, s_bad, scan);
+            op = block_fast(src, (int)pos, (int)bl, 0, 0, (int)limit, P, nx4, pcap, s_bad, scan);
             if (op < 0) return kFallback;
         }
         pos += bl + (bchk ? 4 : 0);
@@ -688,7 +709,8 @@ k_lz4_decode_map(int64_t n, const uint8_t *__restrict__ src, const int64_t *__re
                  int64_t fin_cap, int pcap) {
     extern __shared__ __align__(16) uint8_t sh[];
     uint32_t *map = reinterpret_cast<uint32_t *>(sh);
-    uint8_t *fin = reinterpret_cast<uint8_t *>(map + pcap);  // 16-byte aligned
+    uint16_t *nx4 = reinterpret_cast<uint16_t *>(map + pcap);
+    uint8_t *fin = reinterpret_cast<uint8_t *>(nx4 + pcap);  // 16-byte aligned
     __shared__ long long s_result, s_cchk;
     __shared__ int s_bad, s_scan[kMapThreads / 32];
     const int tid = threadIdx.x, lane = tid & 31;
@@ -708,7 +730,7 @@ k_lz4_decode_map(int64_t n, const uint8_t *__restrict__ src, const int64_t *__re
     int64_t cchk = -1;
     int64_t r = kFallback;
 #if RO_LZ4_FAST
-    if (staged) r = frame_fast(f, b - a, stride, map, pcap, &s_bad, s_scan, &cchk);
+    if (staged) r = frame_fast(f, b - a, stride, map, nx4, pcap, &s_bad, s_scan, &cchk);
 #endif
     if (r == kFallback) {
         __syncthreads();
@@ -932,9 +954,12 @@ int lz4_decode(ro_ctx *c, const uint8_t *src, const int64_t *off, int64_t n, uin
     // Small batches of bricks up to 32 KB: one CTA per frame
     // (k_lz4_decode_map: parallel parse + serial chain + pointer jumping)
     if (stride <= 32 * 1024) {
-        const int64_t fin_cap = std::max<int64_t>(48 * 1024, stride + stride / 2 + 64);
-        const int pcap = (int)((std::max<int64_t>(stride, 32 * 1024) + 3) & ~(int64_t)3);
-        const size_t smem = sizeof(uint32_t) * (size_t)pcap + (size_t)fin_cap + 16;
+        // frames of one block up to 32 KB + framing are staged (any larger
+        // one is parsed serially from global memory)
+        const int64_t fin_cap = 32 * 1024 + 64;
+        const int pcap = 32 * 1024;
+        const size_t smem = (sizeof(uint32_t) + sizeof(uint16_t)) * (size_t)pcap +
+                            (size_t)fin_cap + 16;
         int dev = 0, optin = 0, sms = 0;
         RO_CUDA(cudaGetDevice(&dev));
         RO_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
