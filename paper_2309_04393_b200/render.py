@@ -689,20 +689,19 @@ class ClassicMetadata:
         (z, y, x), numpy or torch."""
         if not 0 <= slot < self.paging.config.m:
             raise RenderError(f"channel slot {slot} out of range")
-        vol = torch.as_tensor(volume).to(self.min_arr.device)
+        from .metadata import node_minmax
+        vol = torch.as_tensor(volume)
+        if vol.dtype != torch.uint8:
+            raise RenderError("classic metadata volumes are u8 (normalised level 0)")
+        vol = vol.to(self.min_arr.device).contiguous()
         g = 1 << self.depth
         nz, ny, nx = vol.shape
         if nz % g or ny % g or nx % g:
             raise RenderError("volume dims must divide the leaf node grid")
-        blocks = vol.reshape(g, nz // g, g, ny // g, g, nx // g)
-        lo = torch.amin(blocks, dim=(1, 3, 5))
-        hi = torch.amax(blocks, dim=(1, 3, 5))
+        # every depth's exact block min / max straight from level 0
+        # (ro_node_minmax with no dilation: the windows are the blocks)
         for d in range(self.depth, -1, -1):
             off = int(self.lvl_off[d])
-            n = 1 << (3 * d)
-            self.min_arr[off:off + n, slot] = lo.reshape(-1).to(torch.uint8)
-            self.max_arr[off:off + n, slot] = hi.reshape(-1).to(torch.uint8)
-            if d:
-                h = (1 << d) // 2
-                lo = torch.amin(lo.reshape(h, 2, h, 2, h, 2), dim=(1, 3, 5))
-                hi = torch.amax(hi.reshape(h, 2, h, 2, h, 2), dim=(1, 3, 5))
+            lo, hi = node_minmax(vol, d, 0)
+            self.min_arr[off:off + lo.numel(), slot] = lo
+            self.max_arr[off:off + hi.numel(), slot] = hi
