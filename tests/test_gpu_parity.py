@@ -763,6 +763,59 @@ def test_gpu_config2_full_frame_matches_oracle(budget):
         assert len(out.brick_requests) > 256  # the complete order, not just a prefix
 
 
+@pytest.mark.parametrize("part", [40, 135, 230])
+def test_gpu_config5_row_bands_match_oracle(part):
+    """BASELINE config 5 (3840x2160, m = 6 visible channels, the config-2
+    volume builder): one sort-first part of 8 rows rendered by the product
+    path (FramePass with partition (270, part, 8), bricks-first feedback)
+    equals the C oracle over the same rows -- image, ordered brick / metadata
+    request lists, usage mask, level histogram and work counters.  4K pixel
+    indices take 23 bits, so request keys are wider than 32 bits whenever a
+    pixel passes 2^9 request events."""
+    import os
+    from oracle import raycast as orc
+    from paper_2309_04393_b200 import orbit_path, scenarios
+    from paper_2309_04393_b200.render import MODE_RESIDENCY, FramePass
+    scn = _config5_scene()
+    eng = scenarios.build_engine(scn)
+    cfg = scn.render
+    w, h = cfg.image_dims
+    cam = orbit_path(120)[part % 120]
+    fp = FramePass(MODE_RESIDENCY, eng.paging, eng.octree, scn.channels, cam, cfg,
+                   partition=(h // 8, part, 8), bricks_first=True)
+    fp.render()
+    fp.collect()
+    b = fp.buf
+    m = eng.paging.config.m
+    nb, nm = b.n_bricks, b.n_metas
+    fb = b.fb.cpu().numpy()
+    ref = orc.OracleState(**scenarios.reference_state(scn))
+    och = [orc.OracleChannel(slot=c.slot, points=c.tf.points, level_range=c.level_range)
+           for c in scn.channels]
+    r0 = 8 * part
+    want = orc.render(ref, och, cam_tuple(cam), (w, h), cfg.base_step,
+                      budget=cfg.max_requests_per_frame, rows=(r0, r0 + 8),
+                      threads=os.cpu_count() or 1)
+    assert np.array_equal(b.image.cpu().numpy().reshape(8, w, 4), want.image[r0:r0 + 8])
+    assert fb[1][:nb].tolist() == want.brick_requests
+    assert [divmod(int(v), m) for v in fb[3][:nm]] == want.metadata_requests
+    assert np.array_equal(b.required.cpu().numpy(), want.required_mask)
+    assert np.array_equal(b.hist.cpu().numpy(), want.level_histogram)
+    c = b.counters.cpu().numpy()
+    assert [int(c[0]), int(c[1]), int(c[2])] == [int(v) for v in want.counters[:3]]
+
+
+_C5 = {}
+
+
+def _config5_scene():
+    from paper_2309_04393_b200 import scenarios
+    if "scn" not in _C5:
+        _C5["scn"] = scenarios.cycif(device="cuda", dataset_channels=(0, 3, 6, 9, 12, 15),
+                                     image_dims=(3840, 2160))
+    return _C5["scn"]
+
+
 def test_gpu_capacity_mode_parts_converge_to_single_gpu_image():
     """Sort-first capacity mode: two part sessions, each
     with its own cache / LRU / octree fed only by its own rows' requests,
