@@ -90,7 +90,19 @@
 // per-channel (slot, lo, hi, zero_upto) as one shared-memory int4 (1) or
 // from the kernel-parameter bank (0)
 #ifndef RO_CHI
-#define RO_CHI 0
+#define RO_CHI 1
+#endif
+// experiment: the channel's zero_upto kept in a register (from S.chi)
+#ifndef RO_ZU_REG
+#define RO_ZU_REG 1
+#endif
+// experiment: 32-bit sub-block table index (slots * sub-blocks < 2^31, checked on the host)
+#ifndef RO_SUB32
+#define RO_SUB32 1
+#endif
+// experiment: the channel loop unrolled by two
+#ifndef RO_CH_UNROLL2
+#define RO_CH_UNROLL2 0
 #endif
 
 namespace ro {
@@ -353,11 +365,16 @@ __device__ __forceinline__ void level_pos(LevelPos &lp, int lev, double px, doub
 // Position at a coarser level `lev` from a finer one when every level in
 // between halves the dims exactly (dims[l] == 2 dims[l+1] on every axis):
 // fl(p * dims[l]) = 2^j fl(p * dims[l + j]) exactly (power-of-two scaling
-// commutes with rounding), so int(P) at lev is int(P) at src.lev >> j.
+// commutes with rounding), so int(P) at lev is int(P) at src.lev >> j.  The
+// fp64 coordinates P themselves are left unset (P[0] = -1): taps_of, the
+// only reader, computes them on the rare sample that loads taps.
 __device__ __forceinline__ void level_pos_from(LevelPos &lp, int lev, const LevelPos &src,
                                                const FrameSmem &S, int lbx, int lby, int lbz) {
     const int j = lev - src.lev;
     lp.lev = lev;
+#if !RO_LP_NOP
+    lp.P[0] = -1.0;
+#endif
     const int lb3[3] = {lbx, lby, lbz};
     int sb[3];
 #pragma unroll
@@ -470,10 +487,13 @@ struct Taps {
 __device__ __forceinline__ void taps_of(Taps &tp, const LevelPos &lp, double px, double py,
                                         double pz, int bx, int by, int bz, const FrameSmem &S) {
     const int B[3] = {bx, by, bz};
-#if RO_LP_NOP
+#if RO_LP_NOP || RO_NEST_DERIVE
     const double p3[3] = {px, py, pz};
 #else
     (void)px, (void)py, (void)pz;
+#endif
+#if RO_NEST_DERIVE && !RO_LP_NOP
+    const bool derived = lp.P[0] < 0.0;  // level_pos_from left P unset
 #endif
     int i0[3];
     double tw[3];
@@ -482,6 +502,8 @@ __device__ __forceinline__ void taps_of(Taps &tp, const LevelPos &lp, double px,
         // lx = P - c*B exactly; fx = lx - 0.5 exactly; clamped to [0, B-1]
 #if RO_LP_NOP
         const double P = p3[a] * S.dimd[lp.lev][a];  // the same rounding as level_pos
+#elif RO_NEST_DERIVE
+        const double P = derived ? p3[a] * S.dimd[lp.lev][a] : lp.P[a];
 #else
         const double P = lp.P[a];
 #endif
@@ -898,6 +920,12 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
 
             // usage mask / histogram / per-pixel brick switches of a sampled
             // channel (kernels.py:670-676)
+#if RO_ZU_REG
+            int zu_cur = 0;  // zero_upto of the channel being sampled (set per channel)
+#define RO_ZU(ci) zu_cur
+#else
+#define RO_ZU(ci) S.zero_upto[ci]
+#endif
             auto account = [&](int ci, int lev, int32_t e) {
 #if !RO_RUNLEN && RO_SMEM_ASM
                 {
@@ -949,8 +977,13 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                 if (A.sub_max == nullptr) return false;
                 RO_ASSERT(slot_lin >= 0 && slot_lin < A.L.num_slots && lp.sub >= 0 &&
                           lp.sub < A.nsb);
+#if RO_SUB32
+                return (int)__ldg(A.sub_max + (uint32_t)(slot_lin * A.nsb + lp.sub)) <=
+                       RO_ZU(ci);
+#else
                 return (int)__ldg(A.sub_max + (int64_t)slot_lin * A.nsb + lp.sub) <=
-                       S.zero_upto[ci];
+                       RO_ZU(ci);
+#endif
 #else
                 return false;
 #endif
@@ -967,7 +1000,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                 // (1 - a) is 1: the channel adds exactly nothing -- skip it.
                 const int mt = max(max(max(tv[0], tv[1]), max(tv[2], tv[3])),
                                    max(max(tv[4], tv[5]), max(tv[6], tv[7])));
-                if (mt <= S.zero_upto[ci]) return;
+                if (mt <= RO_ZU(ci)) return;
                 RO_STAT(c_s7);
                 const double val = trilerp(tv, tp);
                 double r, g, b, a;
@@ -1225,6 +1258,9 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                 auto channel = [&](const int ci) {
 #if RO_CHI
                     const int4 chc = S.chi[ci];
+#if RO_ZU_REG
+                    zu_cur = chc.w;
+#endif
 #else
                     const int4 chc = make_int4(CH_SLOT(ci), CH_LO(ci), CH_HI(ci), 0);
 #endif
@@ -1448,7 +1484,11 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                 } else
 #endif
                 {
+#if RO_CH_UNROLL2
+#pragma unroll 2
+#else
 #pragma unroll 1
+#endif
                     for (int ci = 0; ci < n_ch; ++ci) channel(ci);
                 }
                 end_depth = d;
@@ -1776,6 +1816,9 @@ int render(ro_ctx *c, const ro_frame *F, const ro_state *st,
     A.sub_max = sub_ok ? st->sub_max : nullptr;
     A.nsb = sub_ok ? (c->layout.brick[0] >> RO_SUB_LOG) * (c->layout.brick[1] >> RO_SUB_LOG) *
                          (c->layout.brick[2] >> RO_SUB_LOG) : 0;
+#if RO_SUB32
+    if ((int64_t)A.L.num_slots * A.nsb >= ((int64_t)1 << 31)) A.sub_max = nullptr;
+#endif
     A.node_fast = nullptr;
     A.node_path = nullptr;
     A.local_rows = (int32_t)ro_local_rows(F->height, F->n_parts, F->part, F->tile_rows);
