@@ -1,7 +1,8 @@
 """Summarise a k_raycast `ncu --set full` report into
 profiles/ncu_raycast_summary.json (the `traffic` source of bench.py).
 
-    python tools/ncu_summary.py gpurun_out/r1_raycast.ncu-rep [out.json]
+    python tools/ncu_summary.py gpurun_out/r1_raycast.ncu-rep [out.json] \
+        [--commit SHA] [--camera "orbit_path(1)[0]"]
 """
 import csv
 import io
@@ -31,8 +32,15 @@ STALLS = ["wait", "long_scoreboard", "selected", "short_scoreboard", "branch_res
 
 
 def main():
-    rep = sys.argv[1]
-    out = sys.argv[2] if len(sys.argv) > 2 else "profiles/ncu_raycast_summary.json"
+    args = sys.argv[1:]
+    opts = {}
+    for key in ("--commit", "--camera"):
+        if key in args:
+            i = args.index(key)
+            opts[key[2:]] = args[i + 1]
+            del args[i:i + 2]
+    rep = args[0]
+    out = args[1] if len(args) > 1 else "profiles/ncu_raycast_summary.json"
     metrics = list(M.values()) + [f"smsp__pcsamp_warps_issue_stalled_{s}" for s in STALLS]
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics",
                           ",".join(metrics)], capture_output=True, text=True, check=True).stdout
@@ -52,7 +60,7 @@ def main():
         return v
 
     name = vals[hdr.index("Kernel Name")]
-    s = {"kernel": name, "config": "bench.py config 2 (1920x1080, m=4)"}
+    s = {"kernel": name, "config": "bench.py config 2 (1920x1080, m=4)", **opts}
     for k, m in M.items():
         s[k] = get(m)
     st = {}
