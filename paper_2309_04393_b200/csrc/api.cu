@@ -190,7 +190,6 @@ int ro_create(const ro_layout *layout, ro_ctx **out) {
     TRY(cudaMemset(c->claim, 0, sizeof(uint32_t) * c->E));
     TRY(cudaMallocHost(&c->pinned_small, sizeof(int64_t) * 64));
     if (L.depth <= 9) {
-        TRY(cudaMalloc(&c->node_own, sizeof(uint16_t) * c->num_nodes));
         TRY(cudaMalloc(&c->node_fast, (size_t)c->num_nodes));
     }
     if (L.depth <= 7) TRY(cudaMalloc(&c->node_path, sizeof(uint64_t) * c->num_nodes));
@@ -212,7 +211,6 @@ int ro_destroy(ro_ctx *c) {
     cudaFree(c->meta_touched);
     cudaFree(c->touched_n);
     cudaFree(c->claim);
-    cudaFree(c->node_own);
     cudaFree(c->node_fast);
     cudaFree(c->node_path);
     for (int i = 0; i < 16; ++i) cudaFree(c->scratch[i]);

@@ -197,9 +197,7 @@ struct ro_ctx {
     uint32_t epoch = 0;
     // per-frame node classes of the ray caster's residency walk (raycast.cu
     // k_classify_nodes): [num_nodes] bytes, allocated with the context
-    // per-frame node classes (k_classify_own / k_classify_path): own plain
-    // bits, the fast flag, the path classes (depth <= 7 only)
-    uint16_t *node_own = nullptr;
+    // per-frame node classes (k_classify): fast flags, path classes (depth <= 7)
     uint8_t *node_fast = nullptr;
     uint64_t *node_path = nullptr;
     // a ray-cast pass left first-seen keys that no ro_feedback_collect has

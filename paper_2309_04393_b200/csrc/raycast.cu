@@ -175,7 +175,7 @@ struct RayArgs {
     int32_t *tile_counter;   // persistent-CTA work counter (zeroed per launch)
     const uint8_t *sub_max;  // [S*nsb] dilated 8^3 sub-block maxima (optional)
     int32_t nsb;             // sub-blocks per slot
-    const uint8_t *node_fast;    // [num_nodes] k_classify_path outputs (optional)
+    const uint8_t *node_fast;    // [num_nodes] k_classify outputs (optional)
     const uint64_t *node_path;
 };
 
@@ -593,13 +593,15 @@ struct SampleCtx {
 // A node is "plain" for channel ci when the reference's walk would just step
 // through it: valid metadata, not transparent under ci's TF (_is_empty_meta),
 // not homogeneous, and some level resident (mask != 0).
-//   k_classify_own:  own[x] bit ci = x is plain for channel ci, bit 8 + ci =
-//     x is ZERO for ci (valid and transparent: the walk ends there).
-//   k_classify_path: path[x] byte ci = the plain bits of channel ci along the
-//     root -> x path (bit a = the depth-a ancestor, bit depth(x) = x itself)
-//     and, with at most 4 channels, byte 4 + ci the same for the ZERO bits;
-//     fast[x] = x is plain for every channel and x and all its ancestors are
-//     plain for channel 0.
+//   path[x] byte ci = the plain bits of channel ci along the root -> x path
+//     (bit a = the depth-a ancestor, bit depth(x) = x itself) and, with at
+//     most 4 channels, byte 4 + ci the same for the ZERO bits (valid and
+//     transparent: the walk ends there);
+//   fast[x] bit 0 = x is plain for every channel and x and all its ancestors
+//     are plain for channel 0 (bit 1: the latter alone).
+// One kernel, top-down: CTA b owns the subtree under depth-s node b and
+// walks it level by level (a node's classes = its parent's + its own
+// words), so every node reads one parent entry instead of its ancestors.
 // A sample whose depth-dt node is fast goes straight to the page-table probes
 // at dt (channel 0 walks d0..dt through plain nodes, every later channel
 // visits only the plain dt node: dt - d0 + n_ch visits, no request events).
@@ -609,61 +611,87 @@ struct SampleCtx {
 // and request events, one 8-byte load instead of a word load per plain node
 // (and, up to 4 channels, none for a ZERO terminal).
 // path[] needs D <= 7 (8 depths per byte).
-__global__ void __launch_bounds__(256) k_classify_own(const __grid_constant__ ro_frame F,
-                                                      const uint32_t *__restrict__ words, int m,
-                                                      int64_t n_nodes, uint16_t *__restrict__ own) {
+__global__ void __launch_bounds__(256) k_classify(const __grid_constant__ ro_frame F,
+                                                  const uint32_t *__restrict__ words, int m,
+                                                  int D, int s, uint8_t *__restrict__ fast,
+                                                  uint64_t *__restrict__ path) {
     __shared__ uint16_t eb[RO_MAX_CH][256];
+    __shared__ unsigned long long s_root;  // path class of the subtree root's parent
+    __shared__ uint32_t s_chain;           // channel 0 plain along it
     const int n_ch = F.n_ch;
-    for (int i = threadIdx.x; i < n_ch * 256; i += blockDim.x)
+    const int tid = threadIdx.x;
+    for (int i = tid; i < n_ch * 256; i += blockDim.x)
         eb[i >> 8][i & 255] = F.ch[i >> 8].empty_below[i & 255];
     __syncthreads();
     const int eps_i = F.eps_h >= 255.0 ? 255 : (F.eps_h < 0.0 ? -1 : (int)F.eps_h);
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n_nodes; x += stride) {
+    const uint32_t all = (1u << n_ch) - 1;
+    const bool zbits = n_ch <= 4;
+    // bit ci: plain for channel ci; bit 8 + ci: ZERO for channel ci
+    auto own_of = [&](int64_t node) -> uint32_t {
         uint32_t r = 0;
         for (int ci = 0; ci < n_ch; ++ci) {
-            const uint32_t w = __ldg(words + x * m + F.ch[ci].slot);
+            const uint32_t w = __ldg(words + node * m + F.ch[ci].slot);
             const int mn = (w >> 16) & 0xFF, mx = (int)(w >> 24);
-            const bool valid = !(mn == 255 && mx == 0);  // else INVALID: metadata request
-            const bool zero = valid && mx < (int)eb[ci][mn];  // K_ZERO
-            const bool p = valid && !zero &&
-                           mx - mn > eps_i &&           // K_CONST
-                           (w & 0xFFFFu) != 0;          // K_MISSU
+            const bool valid = !(mn == 255 && mx == 0);       // else INVALID: metadata request
+            const bool zero = valid && mx < (int)eb[ci][mn];   // K_ZERO
+            const bool p = valid && !zero && mx - mn > eps_i &&  // K_CONST
+                           (w & 0xFFFFu) != 0;                    // K_MISSU
             r |= ((uint32_t)p << ci) | ((uint32_t)zero << (8 + ci));
         }
-        own[x] = (uint16_t)r;
-    }
-}
-
-__global__ void __launch_bounds__(256) k_classify_path(int n_ch, int D, int64_t n_nodes,
-                                                       const uint16_t *__restrict__ own,
-                                                       uint8_t *__restrict__ fast,
-                                                       uint64_t *__restrict__ path) {
-    const uint32_t all = (1u << n_ch) - 1;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n_nodes; x += stride) {
-        int d = 0;
-        while (d < D && level_offset(d + 1) <= x) ++d;
-        const int64_t local = x - level_offset(d);
-        const int side_mask = (1 << d) - 1;
-        const int nx = (int)(local & side_mask), ny = (int)((local >> d) & side_mask),
-                  nz = (int)(local >> (2 * d));
-        const uint32_t ox = __ldg(own + x);
-        uint32_t ch0 = ox & 1u;  // channel 0 plain along the whole path
-        uint64_t pc = 0, zc = 0;
-        for (int a = d; a >= 0; --a) {
-            const int sh = d - a;
-            const uint32_t oa = a == d ? ox
-                : __ldg(own + level_offset(a) +
-                        ((((int64_t)(nz >> sh) << a) + (ny >> sh)) << a) + (nx >> sh));
-            ch0 &= oa;
-            for (int ci = 0; ci < n_ch; ++ci) {
-                pc |= (uint64_t)((oa >> ci) & 1u) << (8 * ci + a);
-                zc |= (uint64_t)((oa >> (8 + ci)) & 1u) << (8 * ci + a);
-            }
+        return r;
+    };
+    // path class of a node at depth d from its parent's and its own bits
+    auto compose = [&](uint64_t pp, uint32_t own, int d) -> uint64_t {
+        for (int ci = 0; ci < n_ch; ++ci) {
+            pp |= (uint64_t)((own >> ci) & 1u) << (8 * ci + d);
+            if (zbits) pp |= (uint64_t)((own >> (8 + ci)) & 1u) << (32 + 8 * ci + d);
         }
-        fast[x] = ((ox & 0xFFu) == all && (ch0 & 1u)) ? 1 : 0;
-        if (path != nullptr) path[x] = n_ch <= 4 ? pc | (zc << 32) : pc;
+        return pp;
+    };
+    const int side_s = 1 << s;
+    const int sx = blockIdx.x & (side_s - 1), sy = (blockIdx.x >> s) & (side_s - 1),
+              sz = blockIdx.x >> (2 * s);
+    if (tid == 0) {  // the root's ancestors (shared with other subtrees: same values)
+        uint64_t pc = 0;
+        uint32_t ch0 = 1;
+        for (int a = 0; a < s; ++a) {
+            const int sh = s - a;
+            const int64_t node = level_offset(a) +
+                                 ((((int64_t)(sz >> sh) << a) + (sy >> sh)) << a) + (sx >> sh);
+            const uint32_t o = own_of(node);
+            pc = compose(pc, o, a);
+            ch0 &= o & 1u;
+            fast[node] = (uint8_t)(((o & 0xFFu) == all && ch0) | (ch0 << 1));
+            if (path) path[node] = pc;
+        }
+        s_root = pc;
+        s_chain = ch0;
+    }
+    __syncthreads();
+    for (int d = s; d <= D; ++d) {
+        const int e = d - s, n = 1 << (3 * e), em = (1 << e) - 1;
+        for (int i = tid; i < n; i += blockDim.x) {
+            const int gx = (sx << e) + (i & em), gy = (sy << e) + ((i >> e) & em),
+                      gz = (sz << e) + (i >> (2 * e));
+            const int64_t x = level_offset(d) + ((((int64_t)gz << d) + gy) << d) + gx;
+            uint64_t pp;
+            uint32_t ch0;
+            if (e == 0) {
+                pp = s_root;
+                ch0 = s_chain;
+            } else {  // the parent was written by this CTA one level up
+                const int64_t par = level_offset(d - 1) +
+                                    ((((int64_t)(gz >> 1) << (d - 1)) + (gy >> 1)) << (d - 1)) +
+                                    (gx >> 1);
+                ch0 = ((uint32_t)fast[par] >> 1) & 1u;
+                pp = path ? path[par] : 0;
+            }
+            const uint32_t o = own_of(x);
+            ch0 &= o & 1u;
+            fast[x] = (uint8_t)(((o & 0xFFu) == all && ch0) | (ch0 << 1));
+            if (path) path[x] = compose(pp, o, d);
+        }
+        __syncthreads();  // this level's classes visible to the next level's threads
     }
 }
 
@@ -1157,7 +1185,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                 int cur_node = -1;
                 uint4 wv = make_uint4(0, 0, 0, 0);
                 const int d0 = d;
-                // pre-classified depth-dt node (k_classify_path): every
+                // pre-classified depth-dt node (k_classify): every
                 // channel reaches dt through plain nodes and probes there;
                 // otherwise its path class drives the walk below
                 bool fast = false;
@@ -1167,7 +1195,7 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                     const int lx = qx >> sh, lyy = qy >> sh, lz = qz >> sh;
                     const int leaf = S.lvl_off[dt_] + (((lz << dt_) + lyy) << dt_) + lx;
                     RO_ASSERT(leaf >= 0 && leaf < A.L.num_nodes);
-                    fast = __ldg(A.node_fast + leaf) != 0;
+                    fast = (__ldg(A.node_fast + leaf) & 1u) != 0;
                     if (fast) {
                         c_steps += dt_ - d0 + n_ch;
                         d = dt_;
@@ -1724,8 +1752,7 @@ int warm_b() {
 
 int raycast_warm(ro_ctx *c) {
     cudaFuncAttributes fa;
-    RO_CUDA(cudaFuncGetAttributes(&fa, k_classify_own));
-    RO_CUDA(cudaFuncGetAttributes(&fa, k_classify_path));
+    RO_CUDA(cudaFuncGetAttributes(&fa, k_classify));
     RO_CUDA(cudaFuncGetAttributes(&fa, k_gather_rows));
     const int *b = c->layout.brick;
     if (b[0] == 32 && b[1] == 32 && b[2] == 32) return warm_b<32, 32, 32>();
@@ -1839,13 +1866,9 @@ int render(ro_ctx *c, const ro_frame *F, const ro_state *st,
     if (A.local_rows == 0) return RO_OK;
     RO_CUDA(cudaMemsetAsync(A.tile_counter, 0, sizeof(int32_t), s));
     if (F->mode == RO_MODE_RESIDENCY && c->node_fast != nullptr && st->words != nullptr) {
-        int64_t blocks = (c->num_nodes + 255) / 256;
-        if (blocks > 148 * 8) blocks = 148 * 8;
-        k_classify_own<<<(unsigned)blocks, 256, 0, s>>>(*F, st->words, c->layout.m,
-                                                         c->num_nodes, c->node_own);
-        k_classify_path<<<(unsigned)blocks, 256, 0, s>>>(F->n_ch, c->layout.depth, c->num_nodes,
-                                                          c->node_own, c->node_fast,
-                                                          c->node_path);
+        const int D = c->layout.depth, sub = D < 3 ? D : 3;
+        k_classify<<<1u << (3 * sub), 256, 0, s>>>(*F, st->words, c->layout.m, D, sub,
+                                                   c->node_fast, c->node_path);
         RO_CUDA(cudaGetLastError());
         A.node_fast = c->node_fast;
         A.node_path = c->node_path;
