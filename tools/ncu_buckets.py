@@ -20,7 +20,7 @@ REGIONS = [
     ("load_taps", "__device__ __forceinline__ void load_taps", "// audit value"),
     ("lod_raw", "__device__ __forceinline__ int lod_raw(", "__device__ __forceinline__ int clampi("),
     ("pow_pow2", "__device__ __forceinline__ double pow_pow2(", "// raw LOD level"),
-    ("classify kernels", "__global__ void __launch_bounds__(256) k_classify(", "__host__ __device__ constexpr int ilog2c"),
+    ("classify kernels", "// Per-frame node classes for the residency walk", "__host__ __device__ constexpr int ilog2c"),
     ("staging", "    // ---- stage frame tables ----", "#if RO_PERSISTENT\n    // Persistent CTAs"),
     ("tile / packet setup", "#if RO_PERSISTENT\n    // Persistent CTAs", "    // Warp-uniform sample loop"),
     ("sample head (pos, LOD)", "    // Warp-uniform sample loop", "            // usage mask / histogram / per-pixel brick switches"),
