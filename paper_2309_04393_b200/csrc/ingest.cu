@@ -41,6 +41,14 @@ constexpr int kLz4Warps = 4;  // warps (frames) per CTA (one-warp decoder)
 #ifndef RO_LZ4_FAST
 #define RO_LZ4_FAST 1
 #endif
+#ifndef RO_DEBUG_CHECKS
+#define RO_DEBUG_CHECKS 0
+#endif
+#if RO_DEBUG_CHECKS  // debug builds: trap on any out-of-range index
+#define LZ_ASSERT(c) do { if (!(c)) __trap(); } while (0)
+#else
+#define LZ_ASSERT(c) do { } while (0)
+#endif
 
 enum : int32_t {
     LZ4_OK = 0,
@@ -456,6 +464,7 @@ k_lz4_decode_pipe(int64_t n, const uint8_t *__restrict__ src, const int64_t *__r
 // decoder's.
 constexpr uint32_t kLitRef = 0x80000000u;
 constexpr int kMapThreads = 512;
+[[maybe_unused]] constexpr int kMapCap = 32 * 1024;  // output bytes (map entries) per frame
 constexpr int64_t kFallback = -100;  // internal: re-run the serial parser
 
 struct MapSink {
@@ -463,9 +472,11 @@ struct MapSink {
     int lane;
     __device__ void seq(int64_t lit_at, int64_t lit, int64_t off, int64_t ml, int64_t op) {
         const int o = (int)op, la = (int)lit_at, l = (int)lit;
+        LZ_ASSERT(o >= 0 && o + l + (int)ml <= kMapCap);
         for (int q = lane; q < l; q += 32) map[o + q] = kLitRef | (uint32_t)(la + q);
         if (!ml) return;
         const int mo = o + l, of = (int)off, m = (int)ml;
+        LZ_ASSERT(mo - of >= 0);
         for (int j = lane; j < m; j += 32) map[mo + j] = (uint32_t)(mo + j - of);
     }
     __device__ bool content_ok(int64_t, uint32_t) { return true; }  // checked after the gather
@@ -633,10 +644,15 @@ __device__ int64_t block_fast(const uint8_t *fin, int bpos, int bl, int op0, int
             bool last;
             seq_at(b, bl, c, cap, la, l, of, m, nx, last);
             const uint32_t lsrc = (uint32_t)(bpos + la);
+            LZ_ASSERT(o >= 0 && o + l + m <= pcap && la + l <= bl);
             for (int q = 0; q < l; ++q) map[o + q] = kLitRef | (lsrc + q);
             o += l;
             if (last) break;
             if (of == 0 || of > o - low) bad = 1;
+            if (bad) {  // the CTA falls back to the serial parser
+                marks = 0;
+                break;
+            }
             for (int q = 0; q < m; ++q) map[o + q] = (uint32_t)(o + q - of);
             o += m;
             c = nx;
@@ -765,6 +781,7 @@ k_lz4_decode_map(int64_t n, const uint8_t *__restrict__ src, const int64_t *__re
             for (int q = tid; q < nr; q += kMapThreads) {
                 const uint32_t v = map[q];
                 if (!(v & kLitRef)) {
+                    LZ_ASSERT(v < (uint32_t)q);
                     const uint32_t w = map[v];
                     map[q] = w;
                     pending |= !(w & kLitRef);
