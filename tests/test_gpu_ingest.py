@@ -95,6 +95,45 @@ def test_gpu_lz4_frame_options(opts, size):
         assert np.array_equal(got[j], p), (opts, j)
 
 
+@pytest.mark.parametrize("level", [0, 9])
+def test_gpu_lz4_map_decoder_corpus(level):
+    """One wave of 32^3 frames (148: the one-CTA map decoder's batch) of
+    every compressibility class plus noise-floor bricks (values 0..k: tens
+    of thousands of short matches, deep match chains for the pointer
+    jumping) and mixed bricks (noise + runs, offsets up to 64 KB), compared
+    with liblz4's decode byte for byte."""
+    from oracle import lz4_ref
+    from paper_2309_04393_b200 import ingest
+    rng = np.random.default_rng(7 + level)
+    size = (32, 32, 32)
+    n = 32 * 32 * 32
+    pays = _payloads(rng, 60, size)
+    for i in range(60):
+        kind = i % 3
+        if kind == 0:   # noise floor
+            p = rng.integers(0, 1 + i % 5, size=n, dtype=np.uint8)
+        elif kind == 1:  # noise floor with bright blobs
+            p = rng.integers(0, 3, size=n, dtype=np.uint8)
+            for _ in range(8):
+                a = int(rng.integers(0, n - 900))
+                p[a:a + int(rng.integers(10, 900))] = rng.integers(100, 256, dtype=np.uint8)
+        else:           # repeats of an earlier region (long offsets) + noise
+            p = rng.integers(0, 256, size=n, dtype=np.uint8)
+            for _ in range(20):
+                a, b = sorted(int(v) for v in rng.integers(0, n - 600, size=2))
+                L = int(rng.integers(4, 600))
+                p[b:b + L] = p[a:a + L]
+        pays.append(p.reshape(32, 32, 32))
+    pays = pays[:148] + [np.zeros(size, np.uint8)] * (148 - len(pays))
+    frames = [lz4_ref.prefs_frame(p.tobytes(), level=level) for p in pays]
+    out, st = ingest.decompress_bricks(frames, size)
+    assert (st == 0).all(), st
+    got = out.cpu().numpy()
+    for j, f in enumerate(frames):
+        want = np.frombuffer(lz4_ref.decompress(f, expected_size=n), np.uint8)
+        assert np.array_equal(got[j].reshape(-1), want), j
+
+
 def test_gpu_lz4_rejects_what_liblz4_rejects():
     """Mutated frames: whenever liblz4 (lz4io.decompress semantics) rejects a
     frame the GPU status is non-zero; whenever liblz4 accepts it the GPU
