@@ -121,6 +121,7 @@ constexpr int kPPT = (kTileW / kPackW) * (kTileH / kPackH);  // packets per tile
 static_assert(kTileW % kPackW == 0 && kTileH % kPackH == 0 && kPPT % kWarps == 0,
               "tile shape");
 constexpr int kFastDepth = 6;  // longest channel-0 descent handled in parallel
+constexpr int kRunBytes = RO_RUNLEN ? 8 : 4;  // per-thread brick-run record
 constexpr double kClampHi = 1.0 - 1e-9;
 constexpr double kTwo52 = 4503599627370496.0;
 
@@ -795,8 +796,10 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
     // per channel: the current brick run (kernels.py:672-676 prev_brick) as
     // entry | level << 32 | fetch count << 36; the histogram is credited
     // when the run ends, not per fetch
+    // (RO_RUNLEN = 0: only the 32-bit entry, 4 bytes per thread and channel)
     unsigned long long *run = reinterpret_cast<unsigned long long *>(dyn);  // n_ch
-    int32_t *last_breq = reinterpret_cast<int32_t *>(run + kChStride);    // n_ch
+    int32_t *last_breq = reinterpret_cast<int32_t *>(reinterpret_cast<uint8_t *>(dyn) +
+                                                     kRunBytes * kChStride);  // n_ch
     int32_t *last_mreq = last_breq + kChStride;       // n_ch
     uint32_t *hist_t = reinterpret_cast<uint32_t *>(last_mreq + kChStride);
     for (int i = 0; i < n_ch * k; ++i) hist_t[i * kBlock + tid] = 0;
@@ -1670,7 +1673,10 @@ cudaError_t launch_b(const ro_frame &F, const RayArgs &A, cudaStream_t s) {
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev);
     }
-    size_t dyn = (size_t)F.n_ch * kBlock * (8 + 4 * 2) + (size_t)F.n_ch * A.L.k * kBlock * 4;
+    // 4 CTAs of 128 threads stay within the 164 KB shared-memory carveout
+    // (more L1) for up to 4 channels x 7 levels
+    size_t dyn = (size_t)F.n_ch * kBlock * (kRunBytes + 4 * 2) +
+                 (size_t)F.n_ch * A.L.k * kBlock * 4;
 #ifdef RO_EXTRA_SMEM
     dyn += RO_EXTRA_SMEM;  // experiment knob: shared-memory / L1 split sensitivity
 #endif
