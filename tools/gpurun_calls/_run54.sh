@@ -1,5 +1,5 @@
 timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_render_units.py tests/test_gpu_acceptance.py -m gpu -x -q > gpurun_out/r54_pytest.log 2>&1; tail -2 gpurun_out/r54_pytest.log
-bash tools/_run33.sh
+bash tools/gpurun_calls/_run33.sh
 for v in base onekernel; do
   RESOCT_LIB=$PWD/paper_2309_04393_b200/_variants/libresoct_$v.so timeout 900 python tools/bench_config4.py --cold-frames 10 --orbit-frames 6 > gpurun_out/r54_c4_$v.json 2>/dev/null
   python -c "

@@ -1,2 +1,2 @@
 RESOCT_LIB=$PWD/paper_2309_04393_b200/_variants/libresoct_subent.so timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_render_units.py tests/test_gpu_acceptance.py -m gpu -x -q > gpurun_out/r66_pytest.log 2>&1; tail -2 gpurun_out/r66_pytest.log
-bash tools/_run33.sh
+bash tools/gpurun_calls/_run33.sh
