@@ -195,6 +195,7 @@ int ro_create(const ro_layout *layout, ro_ctx **out) {
     if (L.depth <= 7) TRY(cudaMalloc(&c->node_path, sizeof(uint64_t) * c->num_nodes));
     TRY(cudaStreamCreateWithFlags(&c->upload, cudaStreamNonBlocking));
     TRY(cudaEventCreateWithFlags(&c->upload_done, cudaEventDisableTiming));
+    for (auto &ev : c->chunk_done) TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     TRY(cudaEventCreateWithFlags(&c->host_done, cudaEventDisableTiming));
     TRY(cudaDeviceSynchronize());
 #undef TRY
@@ -218,6 +219,8 @@ int ro_destroy(ro_ctx *c) {
     if (c->staging) cudaFreeHost(c->staging);
     if (c->upload) cudaStreamDestroy(c->upload);
     if (c->upload_done) cudaEventDestroy(c->upload_done);
+    for (auto &ev : c->chunk_done)
+        if (ev) cudaEventDestroy(ev);
     if (c->host_done) cudaEventDestroy(c->host_done);
     delete c;
     return RO_OK;

@@ -188,6 +188,9 @@ struct ro_ctx {
     size_t staging_bytes = 0;
     cudaStream_t upload = nullptr;
     cudaEvent_t upload_done = nullptr;
+    // the payload upload in chunks: chunk q landed (apply_bricks)
+    static constexpr int kUploadChunks = 8;
+    cudaEvent_t chunk_done[kUploadChunks] = {};
     cudaEvent_t host_done = nullptr;
     uint32_t *claim = nullptr;  // [E] batch dedupe stamps
     // caller-owned key arrays (ro_set_feedback_buffers; possibly another

@@ -106,7 +106,7 @@ constexpr int kSubMaxThreads = 256;
 __global__ void __launch_bounds__(kSubMaxThreads)
 k_sub_max_smem(int32_t n, int bx, int by, int bz, const uint8_t *__restrict__ src,
                const int32_t *__restrict__ slots, const uint8_t *__restrict__ final_flag,
-               uint8_t *__restrict__ sub_max) {
+               uint8_t *__restrict__ sub_max, uint8_t *__restrict__ cache) {
     extern __shared__ __align__(16) uint8_t sm[];
     const int i = blockIdx.x;
     if (i >= n || !final_flag[i]) return;
@@ -124,8 +124,14 @@ k_sub_max_smem(int32_t n, int bx, int by, int bz, const uint8_t *__restrict__ sr
     }
     const uint8_t *b = src + (int64_t)i * bvox;
     if ((((uintptr_t)b) & 15) == 0 && (bvox & 15) == 0) {
-        for (int j = threadIdx.x; j < bvox / 16; j += blockDim.x)
-            reinterpret_cast<uint4 *>(v)[j] = reinterpret_cast<const uint4 *>(b)[j];
+        // (cache != null: the brick also lands in its cache slot from here,
+        // the caller guarantees 16-byte alignment)
+        uint4 *c4 = cache ? reinterpret_cast<uint4 *>(cache + (int64_t)slots[i] * bvox) : nullptr;
+        for (int j = threadIdx.x; j < bvox / 16; j += blockDim.x) {
+            const uint4 w = reinterpret_cast<const uint4 *>(b)[j];
+            reinterpret_cast<uint4 *>(v)[j] = w;
+            if (c4) c4[j] = w;
+        }
     } else {
         for (int j = threadIdx.x; j < bvox; j += blockDim.x) v[j] = b[j];
     }
@@ -806,8 +812,12 @@ int apply_bricks(ro_ctx *c, const ro_state *st, const int64_t *ids_h, int64_t n6
         if ((rc = scratch(c, 12, bytes, &dp))) return rc;
     }
 
-    // payload upload on the side stream (overlaps the checks and the LRU)
+    // payload upload on the side stream (overlaps the checks, the LRU, the
+    // octree update and -- chunk by chunk -- the cache copy)
     const uint8_t *d_payload = nullptr;
+    const int32_t chunk = std::max<int32_t>(256, (n + ro_ctx::kUploadChunks - 1) /
+                                                     ro_ctx::kUploadChunks);
+    const int n_chunks = (int)((n + chunk - 1) / chunk);
     bool queued = false, caller_pinned = false;
     // once the DMA is queued, every return makes the stream wait for it, and
     // a caller-pinned source buffer is released only when the DMA is done
@@ -848,7 +858,15 @@ int apply_bricks(ro_ctx *c, const ro_state *st, const int64_t *ids_h, int64_t n6
             }
             RO_CUDA(cudaEventRecord(c->host_done, s));
             RO_CUDA(cudaStreamWaitEvent(c->upload, c->host_done, 0));
-            RO_CUDA(cudaMemcpyAsync(dp, src, bytes, cudaMemcpyHostToDevice, c->upload));
+            // in chunks: each chunk's cache copy / sub-block maxima start as
+            // soon as it has landed, under the rest of the DMA
+            for (int q = 0; q < n_chunks; ++q) {
+                const int64_t b0 = (int64_t)q * chunk, nb = std::min<int64_t>(chunk, n - b0);
+                RO_CUDA(cudaMemcpyAsync((uint8_t *)dp + b0 * bvox,
+                                        (const uint8_t *)src + b0 * bvox, (size_t)(nb * bvox),
+                                        cudaMemcpyHostToDevice, c->upload));
+                RO_CUDA(cudaEventRecord(c->chunk_done[q], c->upload));
+            }
             RO_CUDA(cudaEventRecord(c->upload_done, c->upload));
             queued = true;
             d_payload = (const uint8_t *)dp;
@@ -887,34 +905,60 @@ int apply_bricks(ro_ctx *c, const ro_state *st, const int64_t *ids_h, int64_t n6
     void *args[] = {&A};
     RO_CUDA(cudaLaunchCooperativeKernel((const void *)k_lru_batch, dim3(grid),
                                         dim3(kCoopThreads), args, topk::kSortSmem, s));
-    if (d_payload) {
-        if (queued) RO_CUDA(cudaStreamWaitEvent(s, c->upload_done, 0));
-        if (bvox % 16 == 0 && ((uintptr_t)d_payload & 15) == 0 &&
-            ((uintptr_t)st->cache & 15) == 0)
-            k_copy_payloads<<<blocks_for((bvox / 16) * n), kThreads, 0, s>>>(
-                n, bvox, d_payload, d_slots, d_final, st->cache);
-        else
-            k_copy_payloads_bytes<<<blocks_for(bvox * n), kThreads, 0, s>>>(
-                n, bvox, d_payload, d_slots, d_final, st->cache);
-        RO_CUDA(cudaGetLastError());
-    }
-    if (st->sub_max && c->layout.brick[0] >= RO_SUB_E && c->layout.brick[1] >= RO_SUB_E &&
-        c->layout.brick[2] >= RO_SUB_E) {
-        const int bx = c->layout.brick[0], by = c->layout.brick[1], bz = c->layout.brick[2];
-        const size_t smem = (size_t)bx * by * bz + (size_t)bz * by * (bx >> RO_SUB_LOG) +
-                            (size_t)bz * (by >> RO_SUB_LOG) * (bx >> RO_SUB_LOG);
-        if (smem <= 48 * 1024)
-            k_sub_max_smem<<<n, kSubMaxThreads, smem, s>>>(n, bx, by, bz, d_payload, d_slots,
-                                                           d_final, st->sub_max);
-        else
-            k_sub_max<<<n, 128, 0, s>>>(n, bx, by, bz, d_payload, d_slots, d_final,
-                                        st->sub_max);
-        RO_CUDA(cudaGetLastError());
-    }
+    // the octree update needs the ids / evictions only: it runs while the
+    // payloads are still crossing PCIe
     if (update_octree && st->words) {
         // changed = batch bricks + evicted residents
         rc = octree_update(c, st, d_ids, 2 * n, s);
         if (rc) return rc;
+    }
+    const bool sub_ok = st->sub_max && c->layout.brick[0] >= RO_SUB_E &&
+                        c->layout.brick[1] >= RO_SUB_E && c->layout.brick[2] >= RO_SUB_E;
+    const int bx = c->layout.brick[0], by = c->layout.brick[1], bz = c->layout.brick[2];
+    const size_t sub_smem = (size_t)bx * by * bz + (size_t)bz * by * (bx >> RO_SUB_LOG) +
+                            (size_t)bz * (by >> RO_SUB_LOG) * (bx >> RO_SUB_LOG);
+    const bool aligned = bvox % 16 == 0 && ((uintptr_t)d_payload & 15) == 0 &&
+                         ((uintptr_t)st->cache & 15) == 0;
+    // the sub-block maxima kernel stages each brick in shared memory anyway:
+    // it also stores it into the cache slot (one read of the payload)
+    const bool fused = sub_ok && sub_smem <= 48 * 1024 && aligned;
+    if (d_payload) {
+        const int nq = queued ? n_chunks : 1;
+        const int32_t cq = queued ? chunk : n;
+        for (int q = 0; q < nq; ++q) {
+            const int32_t b0 = q * cq, nb = std::min<int32_t>(cq, n - b0);
+            if (queued) RO_CUDA(cudaStreamWaitEvent(s, c->chunk_done[q], 0));
+            const uint8_t *pq = d_payload + (int64_t)b0 * bvox;
+            if (fused) {
+                k_sub_max_smem<<<nb, kSubMaxThreads, sub_smem, s>>>(
+                    nb, bx, by, bz, pq, d_slots + b0, d_final + b0, st->sub_max, st->cache);
+            } else {
+                if (aligned)
+                    k_copy_payloads<<<blocks_for((bvox / 16) * nb), kThreads, 0, s>>>(
+                        nb, bvox, pq, d_slots + b0, d_final + b0, st->cache);
+                else
+                    k_copy_payloads_bytes<<<blocks_for(bvox * nb), kThreads, 0, s>>>(
+                        nb, bvox, pq, d_slots + b0, d_final + b0, st->cache);
+                if (sub_ok) {
+                    if (sub_smem <= 48 * 1024)
+                        k_sub_max_smem<<<nb, kSubMaxThreads, sub_smem, s>>>(
+                            nb, bx, by, bz, pq, d_slots + b0, d_final + b0, st->sub_max,
+                            nullptr);
+                    else
+                        k_sub_max<<<nb, 128, 0, s>>>(nb, bx, by, bz, pq, d_slots + b0,
+                                                     d_final + b0, st->sub_max);
+                }
+            }
+            RO_CUDA(cudaGetLastError());
+        }
+    } else if (sub_ok) {  // payload unknown: "may be anything" (255) rows
+        if (sub_smem <= 48 * 1024)
+            k_sub_max_smem<<<n, kSubMaxThreads, sub_smem, s>>>(n, bx, by, bz, nullptr, d_slots,
+                                                               d_final, st->sub_max, nullptr);
+        else
+            k_sub_max<<<n, 128, 0, s>>>(n, bx, by, bz, nullptr, d_slots, d_final,
+                                        st->sub_max);
+        RO_CUDA(cudaGetLastError());
     }
     if (slots_out) RO_CUDA(cudaMemcpyAsync(slots_out, d_slots, sizeof(int32_t) * n,
                                            cudaMemcpyDeviceToHost, s));

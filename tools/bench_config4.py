@@ -136,7 +136,14 @@ def main():
         payload = (np.stack(pays) if args.pageable else pinned.stack(pays)) if ids else None
         t_fetch = (time.perf_counter() - a) * 1e3
         t_apply = 0.0
-        if ids:
+        if ids and os.environ.get("C4_PROFILE_FRAME") == str(eng.frame):
+            from torch.profiler import ProfilerActivity, profile
+            with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
+                _, t_apply = timed(lambda: eng.apply_bricks(ids, payload))
+            print(f"--- apply of {len(ids)} bricks: {t_apply:.3f} ms (wall)", file=sys.stderr)
+            print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=14),
+                  file=sys.stderr)
+        elif ids:
             _, t_apply = timed(lambda: eng.apply_bricks(ids, payload))
         a = time.perf_counter()
         metas = list(out.metadata_requests)
