@@ -309,6 +309,10 @@ __device__ __forceinline__ void request(unsigned long long *keys, int32_t *, int
 #ifndef RO_LOD_INC
 #define RO_LOD_INC 1
 #endif
+// the empty-space skip loop keeps the incremental LOD state too
+#ifndef RO_SKIP_LOD_INC
+#define RO_SKIP_LOD_INC 1
+#endif
 #ifndef RO_LP2_LOCAL
 #define RO_LP2_LOCAL 0
 #endif
@@ -1572,9 +1576,23 @@ k_raycast(const __grid_constant__ ro_frame F, const __grid_constant__ RayArgs A)
                             }
                         }
                     }
+#if RO_LOD_INC && RO_SKIP_LOD_INC
+                    // the raw level only grows with t: step / jexp change only
+                    // when t / t0 crosses the next level's threshold
+                    {
+                        const double ratio = S.t0_pow2 ? t * S.inv_t0 : t / t0;
+                        if (ratio >= next_thr) {
+                            raw_c = lod_raw(t, t0, S.inv_t0, S.t0_pow2, S);
+                            next_thr = S.lod_thr[raw_c + 1];
+                        }
+                        step = S.step_tab[raw_c];
+                        jexp = S.maxlev[raw_c];
+                    }
+#else
                     const int raw2 = lod_raw(t, t0, S.inv_t0, S.t0_pow2, S);
                     step = S.step_tab[raw2];
                     jexp = S.maxlev[raw2];
+#endif
                     t += step;
                 }
                 prev_depth = end_depth;
